@@ -1,0 +1,285 @@
+/*
+ * manta_b200.h — C-ABI of the B200-native distributed-launch runtime.
+ *
+ * This is the drop-in boundary for the reference's hot path (Lightning / "manta",
+ * /root/reference/proj). The reference exposes three C++ interfaces on this path and
+ * no FFI; each block below replaces one of them with plain C types (no torch, no STL):
+ *
+ *   driver (planner)      proj/include/manta/planner.hpp:51-78
+ *       mt_ctx_create / mt_array_create / mt_array_delete / mt_launch / mt_plan_export
+ *   system_runtime        proj/include/manta/runtime.hpp:70-98
+ *       mt_exec_create / mt_exec_submit / mt_exec_sync / mt_exec_read_chunk / mt_exec_report_json
+ *   distributions         proj/include/manta/distribution.hpp:62-92
+ *       mt_dist_tile / mt_dist_replicated / mt_dist_single / mt_work_block
+ *   kernel plugin API     proj/include/manta/kernels.hpp:75-105
+ *       mt_kernel_register / mt_kernel_count / mt_kernel_info
+ *   errors                proj/include/manta/errors.hpp:9-35
+ *       every call returns MT_OK or one of the MT_E* codes; mt_last_error() returns the
+ *       message of the calling thread's last failure (parse errors carry line:col).
+ *
+ * The oracle shim (oracle/ref_shim.cpp) exports the same entry points with the prefix
+ * `mr_` over the unmodified reference, so tests drive both through one binding.
+ */
+#ifndef MANTA_B200_H
+#define MANTA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MT_MAX_RANK 3
+#define MT_KERNEL_NAME_MAX 64
+
+/* ---- error codes (errors.hpp:9-35) ---------------------------------------------------- */
+enum mt_status {
+	MT_OK = 0,
+	MT_EPARSE = 1,      /* manta::parse_error      */
+	MT_EVALIDATION = 2, /* manta::validation_error */
+	MT_EPLAN = 3,       /* manta::plan_error       */
+	MT_EEXEC = 4,       /* manta::execution_error  */
+	MT_EINTERNAL = 5,   /* anything else (CUDA failure, bad handle) */
+};
+
+/* ---- element types (dtype.hpp:13; bf16 is a B200 extension for the tcgen05 matmul) --- */
+enum mt_dtype { MT_I32 = 0, MT_I64 = 1, MT_F32 = 2, MT_F64 = 3, MT_BF16 = 4 };
+
+/* ---- task IR (task.hpp:19-95) --------------------------------------------------------- */
+enum mt_task_kind {
+	MT_TASK_CREATE = 0,
+	MT_TASK_DELETE = 1,
+	MT_TASK_EXECUTE = 2,
+	MT_TASK_COPY = 3,
+	MT_TASK_SEND = 4,
+	MT_TASK_RECV = 5,
+	MT_TASK_REDUCE = 6,
+};
+enum mt_fill_kind { MT_FILL_NONE = 0, MT_FILL_ZERO = 1, MT_FILL_ONE = 2, MT_FILL_IDENTITY = 3 };
+enum mt_reduce_op { MT_RED_PLUS = 0, MT_RED_TIMES = 1, MT_RED_MIN = 2, MT_RED_MAX = 3 };
+enum mt_arg_kind { MT_ARG_INT = 0, MT_ARG_FLOAT = 1, MT_ARG_CHUNK = 2, MT_ARG_NONE = 3 };
+
+/* Half-open box [lo, hi) (geometry.hpp:45-70). Also used for points (hi unused). */
+typedef struct mt_rect {
+	int32_t rank;
+	int32_t pad_;
+	int64_t lo[MT_MAX_RANK];
+	int64_t hi[MT_MAX_RANK];
+} mt_rect;
+
+typedef struct mt_device {
+	int32_t worker;
+	int32_t device;
+} mt_device;
+
+typedef struct mt_chunk_desc {
+	int64_t id;
+	mt_rect region;
+	mt_device home;
+} mt_chunk_desc;
+
+typedef struct mt_superblock {
+	mt_rect blocks; /* thread-block index space */
+	mt_device device;
+} mt_superblock;
+
+/* arg_binding (task.hpp:44-50) */
+typedef struct mt_arg_binding {
+	int32_t kind; /* mt_arg_kind */
+	int32_t pad_;
+	int64_t i;
+	double f;
+	int64_t chunk;
+} mt_arg_binding;
+
+/*
+ * One task, flattened. Variable-length parts (deps, reduce inputs, execute args) live in
+ * side pools and are referenced by (offset, count). Field use per kind:
+ *   create : chunk, region, home, dtype, fill, fill_op
+ *   delete : chunk
+ *   execute: kernel, device, sb_blocks, sb_threads, block_size(.lo), args
+ *   copy   : src, dst, src_region, dst_region
+ *   send   : chunk, region, peer, tag          recv: chunk, region, peer, tag
+ *   reduce : op, inputs, output
+ */
+typedef struct mt_task {
+	int64_t id;
+	int32_t worker;
+	int32_t kind; /* mt_task_kind */
+	mt_device resource;
+	int64_t deps_off;
+	int64_t ndeps;
+	int64_t chunk;
+	mt_rect region;
+	mt_device home;
+	int32_t dtype;
+	int32_t fill;
+	int32_t fill_op;
+	int32_t op;
+	char kernel[MT_KERNEL_NAME_MAX];
+	mt_device device;
+	mt_rect sb_blocks;
+	mt_rect sb_threads;
+	mt_rect block_size;
+	int64_t args_off;
+	int64_t nargs;
+	int64_t src;
+	int64_t dst;
+	mt_rect src_region;
+	mt_rect dst_region;
+	int32_t peer;
+	int32_t pad_;
+	uint64_t tag;
+	int64_t inputs_off;
+	int64_t ninputs;
+	int64_t output;
+} mt_task;
+
+/* ---- launch arguments (planner.hpp:25-35) ------------------------------------------- */
+enum mt_launch_arg_kind { MT_LARG_INT = 0, MT_LARG_FLOAT = 1, MT_LARG_ARRAY = 2 };
+typedef struct mt_launch_arg {
+	int32_t kind;
+	int32_t pad_;
+	int64_t i;
+	double f;
+	int64_t array;
+} mt_launch_arg;
+
+/* ---- configuration (planner.hpp:17-23, runtime.hpp:24-33, memory.hpp:43-55) -------- */
+typedef struct mt_config {
+	int32_t workers;
+	int32_t devices_per_worker;
+	int32_t suppress_conflict_deps; /* fault-injection hook (planner.hpp:20-22) */
+	int32_t compat_deps;            /* 1: whole-chunk edges exactly as the reference */
+	int32_t execute;                /* 0: plan only (no GPU needed); 1: run on GPUs    */
+	int32_t num_gpus;               /* physical GPUs to map devices onto (0 = all)     */
+	int32_t streams_per_device;     /* compute streams per logical device (0 = 4)      */
+	int32_t oracle_mode;            /* shim only: 1 worker x 1 device semantics         */
+	uint64_t device_capacity;       /* bytes per device the chunk store may use (0 = 90% of free HBM) */
+	uint64_t host_capacity;         /* pinned-host spill tier bytes (0 = no spill tier)  */
+	uint64_t staging_threshold;     /* reference throttle; informational on the GPU path */
+} mt_config;
+
+typedef struct mt_ctx mt_ctx;
+typedef struct mt_exec mt_exec;
+
+const char* mt_last_error(void);
+const char* mt_version(void);
+
+/* ---- distributions (distribution.cpp:110-220) -------------------------------------- */
+/* Tiles `domain` into chunks of `extents` grown by `halo` and clipped; homes round-robin.
+ * Writes at most `cap` descriptors; *n_out receives the total. row/col/tile/stencil
+ * distributions are all this call with the matching extents/halo. */
+int mt_dist_tile(const mt_rect* domain, const int64_t* extents, const int64_t* halo, const mt_device* devices, int32_t ndev, int64_t first_id,
+    mt_chunk_desc* out, int64_t cap, int64_t* n_out);
+int mt_dist_replicated(const mt_rect* domain, const mt_device* devices, int32_t ndev, int64_t first_id, mt_chunk_desc* out, int64_t cap, int64_t* n_out);
+int mt_dist_single(const mt_rect* domain, mt_device home, int64_t first_id, mt_chunk_desc* out, int64_t cap, int64_t* n_out);
+/* block_work_dist: superblocks of `threads_per_superblock` over `grid`, round-robin devices */
+int mt_work_block(const mt_rect* grid, const int64_t* block, const int64_t* threads_per_superblock, const mt_device* devices, int32_t ndev,
+    mt_superblock* out, int64_t cap, int64_t* n_out);
+
+/* ---- driver: planning + (optionally) execution ---------------------------------------- */
+int mt_ctx_create(const mt_config* cfg, mt_ctx** out);
+int mt_ctx_destroy(mt_ctx* ctx);
+/* devices() in worker-major order */
+int mt_ctx_devices(mt_ctx* ctx, mt_device* out, int32_t cap, int32_t* n_out);
+/* create_array (planner.cpp:122-140): chunk ids are rebased onto the global id space */
+int mt_array_create(mt_ctx* ctx, const mt_rect* domain, int32_t dtype, const mt_chunk_desc* chunks, int64_t nchunks, int32_t fill, int64_t* out_id);
+int mt_array_delete(mt_ctx* ctx, int64_t array_id);
+/* the array's (rebased) chunk descriptors */
+int mt_array_chunks(mt_ctx* ctx, int64_t array_id, mt_chunk_desc* out, int64_t cap, int64_t* n_out);
+int mt_launch(mt_ctx* ctx, const char* kernel, const mt_rect* grid, const int64_t* block, const mt_superblock* work, int64_t nwork,
+    const mt_launch_arg* args, int32_t nargs, const char* annotation, int64_t* first_task, int64_t* past_last_task);
+/* Hands every task emitted since the previous call to the executor (take_pending+submit). */
+int mt_flush(mt_ctx* ctx);
+int mt_sync(mt_ctx* ctx);
+/* Reads a whole array (row-major over its domain) into host memory; assembles chunks in
+ * ascending id order like the reference's gather (scenario.cpp:471-484). */
+int mt_array_read(mt_ctx* ctx, int64_t array_id, void* host, uint64_t bytes);
+/* Uploads host data into every chunk of an array (B200 extension: e2e input path). */
+int mt_array_write(mt_ctx* ctx, int64_t array_id, const void* host, uint64_t bytes);
+/* Byte-compares every overlapping chunk pair (check_replicas, scenario.cpp:486-509);
+ * *coherent = 1 when all agree. */
+int mt_array_check_replicas(mt_ctx* ctx, int64_t array_id, int32_t* coherent);
+/* Plan export: tasks with id in [first, last) plus side pools. Pass caps of 0 to size. */
+int mt_plan_export(mt_ctx* ctx, int64_t first, int64_t last, mt_task* tasks, int64_t task_cap, int64_t* ntasks, int64_t* pool, int64_t pool_cap,
+    int64_t* npool, mt_arg_binding* args, int64_t args_cap, int64_t* nargs);
+int64_t mt_plan_size(mt_ctx* ctx);
+/* chunk_meta (planner.hpp:41-45): temp flag, dtype, descriptor */
+int mt_chunk_meta(mt_ctx* ctx, int64_t chunk, mt_chunk_desc* desc, int32_t* dtype, int32_t* temp);
+/* executor attached to a context (NULL when cfg.execute == 0) */
+mt_exec* mt_ctx_exec(mt_ctx* ctx);
+
+/* ---- executor alone: drop-in for manta::system_runtime ------------------------------ */
+int mt_exec_create(const mt_config* cfg, mt_exec** out);
+int mt_exec_destroy(mt_exec* ex);
+/* tasks must arrive in ascending id order across calls (take_pending order) */
+int mt_exec_submit(mt_exec* ex, const mt_task* tasks, int64_t ntasks, const int64_t* pool, const mt_arg_binding* args);
+int mt_exec_sync(mt_exec* ex);
+int mt_exec_read_chunk(mt_exec* ex, int64_t chunk, void* dst, uint64_t bytes);
+int mt_exec_write_chunk(mt_exec* ex, int64_t chunk, const void* src, uint64_t bytes);
+/* run_report::to_json field names (runtime.cpp:613-636); returns required size in *len */
+int mt_exec_report_json(mt_exec* ex, char* buf, int64_t cap, int64_t* len);
+
+/* counters: tasks, device launches, copies, bytes copied, bytes sent, bytes received, peak
+ * device bytes (first n of them) */
+int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n);
+/* cudaStream_t of the most recent execute task (for event timing on the launching stream) */
+void* mt_exec_last_stream(mt_exec* ex);
+
+/* ---- kernel plugin API (kernels.hpp:56-105) ------------------------------------------ */
+/* View of one chunk as seen by a kernel: element (g0,g1,g2) lives at
+ * base[sum_k (g_k - offset_k) * stride_k] (array_view, kernels.hpp:18-42). `base` is a
+ * device pointer on the executing GPU. */
+typedef struct mt_view {
+	void* base;
+	int32_t dtype;
+	int32_t rank;
+	int64_t offset[MT_MAX_RANK];
+	int64_t stride[MT_MAX_RANK];
+	int64_t extent[MT_MAX_RANK];
+} mt_view;
+
+/* Everything one superblock launch sees (the AOT form of the paper's wrapper,
+ * PAPER.md:491-511 / kernels.cpp:538-596). Threads to run: every global thread index g with
+ * threads.lo <= g < threads.hi (whole blocks, planner.cpp:225-234). */
+typedef struct mt_launch_ctx {
+	int32_t rank;
+	int32_t nparams;
+	int64_t block_offset[MT_MAX_RANK]; /* superblock_blocks.lo */
+	int64_t block_count[MT_MAX_RANK];  /* superblock block extents */
+	int64_t block_size[MT_MAX_RANK];
+	int64_t threads_lo[MT_MAX_RANK];
+	int64_t threads_hi[MT_MAX_RANK];
+	const int64_t* scalars_int;  /* per param index */
+	const double* scalars_float; /* per param index */
+	const mt_view* views;        /* per param index (base NULL when unbound) */
+	const void* user;            /* the `user` pointer given at registration */
+} mt_launch_ctx;
+
+/* Launcher: enqueue the superblock's work on `stream` (a cudaStream_t) and return 0. */
+typedef int (*mt_launcher_fn)(const mt_launch_ctx* ctx, void* stream);
+
+enum mt_param_kind { MT_PARAM_SCALAR = 0, MT_PARAM_ARRAY = 1 };
+typedef struct mt_param_spec {
+	char name[32];
+	int32_t kind;
+	int32_t dtype;
+	int32_t rank;
+	int32_t writable;
+} mt_param_spec;
+
+/* register_kernel (kernels.cpp:81-91): rejects duplicates and unsupported ranks. The
+ * registry is process-global and shared by all contexts. */
+int mt_kernel_register(const char* id, const mt_param_spec* params, int32_t nparams, mt_launcher_fn launcher);
+int mt_kernel_count(void);
+/* context-local kernel (shadows the global registry for this context's launches); the
+ * launcher may be NULL for plan-only contexts */
+int mt_ctx_kernel_register(mt_ctx* ctx, const char* id, const mt_param_spec* params, int32_t nparams, mt_launcher_fn launcher, const void* user);
+int mt_kernel_info(int32_t index, char* id, int32_t id_cap, mt_param_spec* params, int32_t cap, int32_t* nparams);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MANTA_B200_H */

@@ -1,0 +1,370 @@
+"""Host API mirroring the reference's driver / system_runtime / distribution interface.
+
+Names and argument meaning follow proj/include/manta (planner.hpp:51-78 `driver`,
+runtime.hpp:70-98 `system_runtime`, distribution.hpp:62-92 distributions); errors are the
+reference's exception kinds (ParseError, ValidationError, PlanError, ExecutionError). All
+work happens behind the C-ABI of include/manta_b200.h; this module only marshals.
+
+`Context` combines the driver with its executor the way the reference's harnesses do
+(test_runtime.cpp:12-43): `launch` plans, `flush` hands the new tasks to the executor
+(take_pending + submit), `synchronize` waits.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _capi as capi
+from ._capi import (BF16, F32, F64, I32, I64, ExecutionError, MantaError, ParseError, PlanError,  # noqa: F401
+                    ValidationError)
+
+_NP_DTYPE = {I32: np.int32, I64: np.int64, F32: np.float32, F64: np.float64, BF16: np.uint16}
+
+
+def dtype_code(t) -> int:
+    if isinstance(t, str):
+        return capi.DTYPE_NAMES[t]
+    return int(t)
+
+
+@dataclass(frozen=True)
+class Chunk:
+    id: int
+    lo: tuple
+    hi: tuple
+    home: tuple  # (worker, device)
+
+
+@dataclass(frozen=True)
+class Superblock:
+    lo: tuple
+    hi: tuple
+    device: tuple
+
+
+@dataclass(frozen=True)
+class Arr:
+    """Launch argument naming a distributed array (launch_arg::array)."""
+    id: int
+
+
+def _devs(devices) -> tuple:
+    arr = (capi.Device * max(1, len(devices)))()
+    for i, (w, d) in enumerate(devices):
+        arr[i].worker, arr[i].device = w, d
+    return arr, len(devices)
+
+
+def _chunks_out(lib, fn, *args) -> list[Chunk]:
+    n = C.c_int64(0)
+    lib.check(fn(*args, None, 0, C.byref(n)))
+    buf = (capi.ChunkDesc * max(1, n.value))()
+    lib.check(fn(*args, buf, n.value, C.byref(n)))
+    return [Chunk(c.id, *c.region.box(), (c.home.worker, c.home.device)) for c in buf[: n.value]]
+
+
+def _domain(domain) -> capi.Rect:
+    if isinstance(domain, capi.Rect):
+        return domain
+    if len(domain) == 2 and isinstance(domain[0], (tuple, list)):
+        return capi.Rect.make(domain[0], domain[1])
+    return capi.Rect.make([0] * len(domain), domain)
+
+
+class Distributions:
+    """tile_data_dist / row_dist / col_dist / tile_dist / stencil_dist / replicated_dist /
+    single_dist (distribution.cpp:136-195) and block_work_dist (:110-134)."""
+
+    def __init__(self, lib: capi.Lib):
+        self.lib = lib
+
+    def tile_data(self, domain, extents, halo, devices, first_id=0) -> list[Chunk]:
+        d = _domain(domain)
+        ext = (C.c_int64 * 3)(*extents)
+        hal = (C.c_int64 * 3)(*halo)
+        devs, nd = _devs(devices)
+        return _chunks_out(self.lib, self.lib.dist_tile, C.byref(d), ext, hal, devs, nd, first_id)
+
+    def row(self, domain, rows, devices, first_id=0):
+        d = _domain(domain)
+        lo, hi = d.box()
+        ext = [h - l for l, h in zip(lo, hi)]
+        ext[0] = rows
+        return self.tile_data(d, ext, [0] * d.rank, devices, first_id)
+
+    def col(self, domain, cols, devices, first_id=0):
+        d = _domain(domain)
+        if d.rank < 2:
+            raise ValidationError("column distribution requires rank >= 2")
+        lo, hi = d.box()
+        ext = [h - l for l, h in zip(lo, hi)]
+        ext[1] = cols
+        return self.tile_data(d, ext, [0] * d.rank, devices, first_id)
+
+    def tile(self, domain, extents, devices, first_id=0):
+        return self.tile_data(domain, extents, [0] * len(extents), devices, first_id)
+
+    def stencil(self, domain, extents, halo, devices, first_id=0):
+        return self.tile_data(domain, extents, halo, devices, first_id)
+
+    def replicated(self, domain, devices, first_id=0):
+        d = _domain(domain)
+        devs, nd = _devs(devices)
+        return _chunks_out(self.lib, self.lib.dist_replicated, C.byref(d), devs, nd, first_id)
+
+    def single(self, domain, home, first_id=0):
+        d = _domain(domain)
+        dev = capi.Device(home[0], home[1])
+        return _chunks_out(self.lib, self.lib.dist_single, C.byref(d), dev, first_id)
+
+    def block_work(self, grid, block, threads_per_superblock, devices) -> list[Superblock]:
+        g = _domain(grid)
+        b = (C.c_int64 * 3)(*block)
+        t = (C.c_int64 * 3)(*threads_per_superblock)
+        devs, nd = _devs(devices)
+        n = C.c_int64(0)
+        self.lib.check(self.lib.work_block(C.byref(g), b, t, devs, nd, None, 0, C.byref(n)))
+        out = (capi.Superblock * max(1, n.value))()
+        self.lib.check(self.lib.work_block(C.byref(g), b, t, devs, nd, out, n.value, C.byref(n)))
+        return [Superblock(*s.blocks.box(), (s.device.worker, s.device.device)) for s in out[: n.value]]
+
+
+def _task_dict(t: capi.Task, pool, args) -> dict:
+    d = {"id": t.id, "worker": t.worker, "kind": capi.TASK_KIND_NAMES[t.kind], "resource": (t.resource.worker, t.resource.device),
+         "deps": [pool[t.deps_off + i] for i in range(t.ndeps)]}
+    k = t.kind
+    if k == capi.CREATE:
+        d.update(chunk=t.chunk, region=t.region.box(), home=(t.home.worker, t.home.device), dtype=t.dtype, fill=t.fill,
+                 fill_op=t.fill_op if t.fill == capi.FILL_IDENTITY else 0)
+    elif k == capi.DELETE:
+        d.update(chunk=t.chunk)
+    elif k == capi.EXECUTE:
+        d.update(kernel=t.kernel.decode(), device=(t.device.worker, t.device.device), sb_blocks=t.sb_blocks.box(),
+                 sb_threads=t.sb_threads.box(), block_size=t.block_size.point(),
+                 args=[(args[t.args_off + i].kind, args[t.args_off + i].i, args[t.args_off + i].f, args[t.args_off + i].chunk)
+                       for i in range(t.nargs)])
+    elif k == capi.COPY:
+        d.update(src=t.src, dst=t.dst, src_region=t.src_region.box(), dst_region=t.dst_region.box())
+    elif k in (capi.SEND, capi.RECV):
+        d.update(chunk=t.chunk, region=t.region.box(), peer=t.peer, tag=t.tag)
+    elif k == capi.REDUCE:
+        d.update(op=t.op, inputs=[pool[t.inputs_off + i] for i in range(t.ninputs)], output=t.output)
+    return d
+
+
+class PlanBuffer:
+    """A flat task list + side pools, as exported by mt_plan_export / consumed by mt_exec_submit."""
+
+    def __init__(self, tasks, pool, args):
+        self.tasks, self.pool, self.args = tasks, pool, args
+
+    def __len__(self):
+        return len(self.tasks)
+
+    def dicts(self) -> list[dict]:
+        return [_task_dict(t, self.pool, self.args) for t in self.tasks]
+
+
+class Context:
+    """driver + executor over one library (product `mt_` or oracle shim `mr_`)."""
+
+    def __init__(self, lib: capi.Lib, workers=1, devices=1, execute=True, compat_deps=False, suppress_conflict_deps=False,
+                 num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0):
+        self.lib = lib
+        self.dist = Distributions(lib)
+        cfg = capi.Config()
+        cfg.workers, cfg.devices_per_worker = workers, devices
+        cfg.suppress_conflict_deps = int(suppress_conflict_deps)
+        cfg.compat_deps = int(compat_deps)
+        cfg.execute = int(execute)
+        cfg.num_gpus = num_gpus
+        cfg.streams_per_device = streams_per_device
+        cfg.device_capacity = device_capacity
+        cfg.host_capacity = host_capacity
+        cfg.staging_threshold = staging_threshold
+        h = C.c_void_p()
+        lib.check(lib.ctx_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.executes = bool(execute)
+        self._arrays: dict[int, tuple] = {}
+
+    def close(self):
+        if self.h:
+            self.lib.check(self.lib.ctx_destroy(self.h))
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- driver ------------------------------------------------------------------------
+    @property
+    def devices(self) -> list[tuple]:
+        out = (capi.Device * 4096)()
+        n = C.c_int32(0)
+        self.lib.check(self.lib.ctx_devices(self.h, out, 4096, C.byref(n)))
+        return [(d.worker, d.device) for d in out[: n.value]]
+
+    def create_array(self, domain, dtype, distribution: Sequence[Chunk], fill=None) -> int:
+        d = _domain(domain)
+        chunks = (capi.ChunkDesc * len(distribution))()
+        for i, c in enumerate(distribution):
+            chunks[i].id = c.id
+            chunks[i].region = capi.Rect.make(c.lo, c.hi)
+            chunks[i].home = capi.Device(*c.home)
+        fill_code = {None: capi.FILL_NONE, 0: capi.FILL_ZERO, 0.0: capi.FILL_ZERO, 1: capi.FILL_ONE, 1.0: capi.FILL_ONE}[fill]
+        out = C.c_int64(-1)
+        self.lib.check(self.lib.array_create(self.h, C.byref(d), dtype_code(dtype), chunks, len(distribution), fill_code, C.byref(out)))
+        self._arrays[out.value] = (d.box(), dtype_code(dtype))
+        return out.value
+
+    def delete_array(self, array_id: int):
+        self.lib.check(self.lib.array_delete(self.h, array_id))
+
+    def chunks(self, array_id: int) -> list[Chunk]:
+        return _chunks_out(self.lib, self.lib.array_chunks, self.h, array_id)
+
+    def launch(self, kernel: str, grid, block, work: Sequence[Superblock], args: Iterable, annotation: str):
+        g = _domain(grid)
+        b = (C.c_int64 * 3)(*block)
+        w = (capi.Superblock * max(1, len(work)))()
+        for i, s in enumerate(work):
+            w[i].blocks = capi.Rect.make(s.lo, s.hi)
+            w[i].device = capi.Device(*s.device)
+        args = list(args)
+        la = (capi.LaunchArg * max(1, len(args)))()
+        for i, a in enumerate(args):
+            if isinstance(a, Arr):
+                la[i].kind, la[i].array = capi.LARG_ARRAY, a.id
+            elif isinstance(a, (bool, int, np.integer)):
+                la[i].kind, la[i].i = capi.LARG_INT, int(a)
+            elif isinstance(a, (float, np.floating)):
+                la[i].kind, la[i].f = capi.LARG_FLOAT, float(a)
+            else:
+                raise ValidationError(f"unsupported launch argument {a!r}")
+        first, last = C.c_int64(0), C.c_int64(0)
+        self.lib.check(self.lib.launch(self.h, kernel.encode(), C.byref(g), b, w, len(work), la, len(args), annotation.encode(),
+                                       C.byref(first), C.byref(last)))
+        return first.value, last.value
+
+    def flush(self):
+        self.lib.check(self.lib.flush(self.h))
+
+    def synchronize(self):
+        self.lib.check(self.lib.sync(self.h))
+
+    # -- data ------------------------------------------------------------------------
+    def shape_of(self, array_id: int):
+        (lo, hi), t = self._arrays[array_id]
+        return tuple(h - l for l, h in zip(lo, hi)), t
+
+    def read(self, array_id: int) -> np.ndarray:
+        shape, t = self.shape_of(array_id)
+        out = np.empty(shape, dtype=_NP_DTYPE[t])
+        self.lib.check(self.lib.array_read(self.h, array_id, out.ctypes.data, out.nbytes))
+        return out
+
+    def write(self, array_id: int, data: np.ndarray):
+        shape, t = self.shape_of(array_id)
+        data = np.ascontiguousarray(data, dtype=_NP_DTYPE[t]).reshape(shape)
+        self.lib.check(self.lib.array_write(self.h, array_id, data.ctypes.data, data.nbytes))
+
+    def replicas_coherent(self, array_id: int) -> bool:
+        ok = C.c_int32(0)
+        self.lib.check(self.lib.array_check_replicas(self.h, array_id, C.byref(ok)))
+        return bool(ok.value)
+
+    # -- plan --------------------------------------------------------------------------
+    def plan_size(self) -> int:
+        return int(self.lib.plan_size(self.h))
+
+    def export_plan(self, first=0, last=None) -> PlanBuffer:
+        if last is None:
+            last = 1 << 62
+        nt, npool, na = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+        self.lib.check(self.lib.plan_export(self.h, first, last, None, 0, C.byref(nt), None, 0, C.byref(npool), None, 0, C.byref(na)))
+        tasks = (capi.Task * max(1, nt.value))()
+        pool = (C.c_int64 * max(1, npool.value))()
+        args = (capi.ArgBinding * max(1, na.value))()
+        self.lib.check(self.lib.plan_export(self.h, first, last, tasks, nt.value, C.byref(nt), pool, npool.value, C.byref(npool), args, na.value,
+                                            C.byref(na)))
+        return PlanBuffer(tasks[: nt.value], pool, args)
+
+    def plan(self, first=0, last=None) -> list[dict]:
+        return self.export_plan(first, last).dicts()
+
+    def chunk_meta(self, chunk: int):
+        desc = capi.ChunkDesc()
+        dt, tmp = C.c_int32(0), C.c_int32(0)
+        self.lib.check(self.lib.chunk_meta(self.h, chunk, C.byref(desc), C.byref(dt), C.byref(tmp)))
+        return Chunk(desc.id, *desc.region.box(), (desc.home.worker, desc.home.device)), dt.value, bool(tmp.value)
+
+    def exec_stats(self) -> dict:
+        ex = self.lib.ctx_exec(self.h)
+        if not ex or not self.lib.has("exec_stats"):
+            return {}
+        out = (C.c_uint64 * 7)()
+        self.lib.check(self.lib.exec_stats(ex, out, 7))
+        keys = ["tasks", "kernels", "copies", "bytes_copied", "bytes_sent", "bytes_received", "peak_device_bytes"]
+        return dict(zip(keys, [int(v) for v in out]))
+
+    def last_stream(self) -> int:
+        ex = self.lib.ctx_exec(self.h)
+        return int(self.lib.exec_last_stream(ex) or 0) if ex and self.lib.has("exec_last_stream") else 0
+
+
+class Executor:
+    """system_runtime alone: consumes flat plans (e.g. the reference driver's) — the drop-in
+    path for the reference's CPU executor (runtime.hpp:70-98)."""
+
+    def __init__(self, lib: capi.Lib, workers=1, devices=1, num_gpus=0, device_capacity=0):
+        self.lib = lib
+        cfg = capi.Config()
+        cfg.workers, cfg.devices_per_worker, cfg.execute, cfg.num_gpus = workers, devices, 1, num_gpus
+        cfg.device_capacity = device_capacity
+        h = C.c_void_p()
+        lib.check(lib.exec_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+
+    def submit(self, plan: PlanBuffer):
+        if len(plan) == 0:
+            return
+        arr = (capi.Task * len(plan.tasks))(*plan.tasks)
+        self.lib.check(self.lib.exec_submit(self.h, arr, len(plan.tasks), plan.pool, plan.args))
+
+    def synchronize(self):
+        self.lib.check(self.lib.exec_sync(self.h))
+
+    def read_chunk(self, chunk: int, nbytes: int) -> bytes:
+        buf = (C.c_char * nbytes)()
+        self.lib.check(self.lib.exec_read_chunk(self.h, chunk, buf, nbytes))
+        return bytes(buf)
+
+    def report_json(self) -> str:
+        n = C.c_int64(0)
+        self.lib.check(self.lib.exec_report_json(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self.lib.check(self.lib.exec_report_json(self.h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+    def close(self):
+        if self.h:
+            self.lib.check(self.lib.exec_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,639 @@
+#include "executor.hpp"
+
+#include <cstring>
+#include <limits>
+#include <sstream>
+
+namespace mtb {
+
+void check_cuda(cudaError_t e, const char* what) {
+	if(e != cudaSuccess) throw execution_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- device helpers ----------------------------------------------------------------------
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T add_wrap(T a, T b) {
+	return a + b;
+}
+template <>
+__device__ __forceinline__ int32_t add_wrap(int32_t a, int32_t b) {
+	return static_cast<int32_t>(static_cast<uint32_t>(a) + static_cast<uint32_t>(b));
+}
+template <>
+__device__ __forceinline__ int64_t add_wrap(int64_t a, int64_t b) {
+	return static_cast<int64_t>(static_cast<uint64_t>(a) + static_cast<uint64_t>(b));
+}
+template <>
+__device__ __forceinline__ float add_wrap(float a, float b) {
+	return __fadd_rn(a, b);
+}
+template <>
+__device__ __forceinline__ double add_wrap(double a, double b) {
+	return __dadd_rn(a, b);
+}
+template <typename T>
+__device__ __forceinline__ T mul_wrap(T a, T b) {
+	return a * b;
+}
+template <>
+__device__ __forceinline__ int32_t mul_wrap(int32_t a, int32_t b) {
+	return static_cast<int32_t>(static_cast<uint32_t>(a) * static_cast<uint32_t>(b));
+}
+template <>
+__device__ __forceinline__ int64_t mul_wrap(int64_t a, int64_t b) {
+	return static_cast<int64_t>(static_cast<uint64_t>(a) * static_cast<uint64_t>(b));
+}
+template <>
+__device__ __forceinline__ float mul_wrap(float a, float b) {
+	return __fmul_rn(a, b);
+}
+template <>
+__device__ __forceinline__ double mul_wrap(double a, double b) {
+	return __dmul_rn(a, b);
+}
+
+struct bf16_t {
+	uint16_t bits;
+};
+
+template <typename T>
+__global__ void fill_kernel(T* p, uint64_t n, T v) {
+	for(uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) p[i] = v;
+}
+
+constexpr int kMaxReduceInputs = 8;
+template <typename T>
+struct reduce_inputs {
+	const T* in[kMaxReduceInputs];
+	int n;
+	bool first_is_copy;
+};
+
+template <typename T, int OP>
+__global__ void combine_kernel(T* out, reduce_inputs<T> ins, uint64_t count) {
+	for(uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < count; e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+		int k = 0;
+		T o;
+		if(ins.first_is_copy) {
+			o = ins.in[0][e];
+			k = 1;
+		} else {
+			o = out[e];
+		}
+		for(; k < ins.n; ++k) {
+			const T x = ins.in[k][e];
+			if constexpr(OP == 0) o = add_wrap<T>(o, x);
+			if constexpr(OP == 1) o = mul_wrap<T>(o, x);
+			if constexpr(OP == 2) o = (x < o) ? x : o; // std::min
+			if constexpr(OP == 3) o = (o < x) ? x : o; // std::max
+		}
+		out[e] = o;
+	}
+}
+
+int grid_for(uint64_t n, int threads) {
+	uint64_t blocks = (n + threads - 1) / threads;
+	if(blocks > 148ull * 32) blocks = 148ull * 32;
+	if(blocks == 0) blocks = 1;
+	return static_cast<int>(blocks);
+}
+
+template <typename T>
+void fill_typed(void* p, uint64_t n, T v, cudaStream_t s) {
+	fill_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(static_cast<T*>(p), n, v);
+}
+
+template <typename T>
+T identity_of(reduce_op op) {
+	switch(op) {
+	case reduce_op::plus: return T(0);
+	case reduce_op::times: return T(1);
+	case reduce_op::min: return std::numeric_limits<T>::max();
+	case reduce_op::max: return std::numeric_limits<T>::lowest();
+	}
+	return T(0);
+}
+
+template <typename T>
+void reduce_typed(void* out, const void* const* inputs, int n, uint64_t count, reduce_op op, cudaStream_t s) {
+	for(int base = 0; base < n; base += kMaxReduceInputs) {
+		reduce_inputs<T> ins{};
+		ins.n = std::min(kMaxReduceInputs, n - base);
+		ins.first_is_copy = base == 0;
+		for(int k = 0; k < ins.n; ++k) ins.in[k] = static_cast<const T*>(inputs[base + k]);
+		T* o = static_cast<T*>(out);
+		const int g = grid_for(count, 256);
+		switch(op) {
+		case reduce_op::plus: combine_kernel<T, 0><<<g, 256, 0, s>>>(o, ins, count); break;
+		case reduce_op::times: combine_kernel<T, 1><<<g, 256, 0, s>>>(o, ins, count); break;
+		case reduce_op::min: combine_kernel<T, 2><<<g, 256, 0, s>>>(o, ins, count); break;
+		case reduce_op::max: combine_kernel<T, 3><<<g, 256, 0, s>>>(o, ins, count); break;
+		}
+	}
+}
+
+// row-major strides (elements) of a chunk box
+void strides_of(const box& b, int64_t* st) {
+	int64_t acc = 1;
+	for(int k = b.rank() - 1; k >= 0; --k) {
+		st[k] = acc;
+		acc *= b.extent(k);
+	}
+}
+
+} // namespace
+
+void device_fill(void* ptr, uint64_t count, dtype type, fill_kind kind, reduce_op op, cudaStream_t s) {
+	const uint64_t bytes = count * dtype_size(type);
+	if(kind == fill_kind::none || kind == fill_kind::zero || (kind == fill_kind::identity && op == reduce_op::plus)) {
+		check_cuda(cudaMemsetAsync(ptr, 0, bytes, s), "cudaMemsetAsync");
+		return;
+	}
+	const bool one = kind == fill_kind::one;
+	switch(type) {
+	case dtype::i32: fill_typed<int32_t>(ptr, count, one ? 1 : identity_of<int32_t>(op), s); break;
+	case dtype::i64: fill_typed<int64_t>(ptr, count, one ? 1 : identity_of<int64_t>(op), s); break;
+	case dtype::f32: fill_typed<float>(ptr, count, one ? 1.0f : identity_of<float>(op), s); break;
+	case dtype::f64: fill_typed<double>(ptr, count, one ? 1.0 : identity_of<double>(op), s); break;
+	case dtype::bf16: {
+		// 1.0 = 0x3F80, max finite = 0x7F7F, lowest = 0xFF7F
+		uint16_t v = 0x3F80;
+		if(!one && op == reduce_op::min) v = 0x7F7F;
+		if(!one && op == reduce_op::max) v = 0xFF7F;
+		fill_typed<uint16_t>(ptr, count, v, s);
+		break;
+	}
+	}
+	check_cuda(cudaGetLastError(), "fill kernel launch");
+}
+
+void device_reduce(void* out, const void* const* inputs, int n, uint64_t count, dtype type, reduce_op op, cudaStream_t s) {
+	switch(type) {
+	case dtype::i32: reduce_typed<int32_t>(out, inputs, n, count, op, s); break;
+	case dtype::i64: reduce_typed<int64_t>(out, inputs, n, count, op, s); break;
+	case dtype::f32: reduce_typed<float>(out, inputs, n, count, op, s); break;
+	case dtype::f64: reduce_typed<double>(out, inputs, n, count, op, s); break;
+	case dtype::bf16: throw execution_error("bf16 reduce tasks are not supported");
+	}
+	check_cuda(cudaGetLastError(), "reduce kernel launch");
+}
+
+void copy_box(const void* src_base, const box& src_chunk, int src_gpu, void* dst_base, const box& dst_chunk, int dst_gpu, const box& region,
+    size_t elem, cudaStream_t s) {
+	if(region.is_empty()) return;
+	const int rank = region.rank();
+	int64_t ss[kMaxRank], ds[kMaxRank];
+	strides_of(src_chunk, ss);
+	strides_of(dst_chunk, ds);
+	int64_t so = 0, dof = 0;
+	for(int k = 0; k < rank; ++k) {
+		so += (region.lo[k] - src_chunk.lo[k]) * ss[k];
+		dof += (region.lo[k] - dst_chunk.lo[k]) * ds[k];
+	}
+	const char* sp = static_cast<const char*>(src_base) + so * static_cast<int64_t>(elem);
+	char* dp = static_cast<char*>(dst_base) + dof * static_cast<int64_t>(elem);
+	// contiguous in both: region covers whole inner extents of both chunks
+	bool contiguous = true;
+	for(int k = 1; k < rank && contiguous; ++k) {
+		if(region.extent(k) != src_chunk.extent(k) || region.extent(k) != dst_chunk.extent(k)) contiguous = false;
+	}
+	// after the first axis with extent > 1 everything inner must be full; relax: a single row is contiguous
+	if(!contiguous) {
+		int outer_nontrivial = 0;
+		for(int k = 0; k < rank - 1; ++k)
+			if(region.extent(k) > 1) ++outer_nontrivial;
+		if(outer_nontrivial == 0) contiguous = true;
+	}
+	if(contiguous) {
+		const size_t bytes = static_cast<size_t>(region.volume()) * elem;
+		if(src_gpu < 0 || dst_gpu < 0)
+			check_cuda(cudaMemcpyAsync(dp, sp, bytes, cudaMemcpyDefault, s), "cudaMemcpyAsync (host)");
+		else if(src_gpu == dst_gpu)
+			check_cuda(cudaMemcpyAsync(dp, sp, bytes, cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync");
+		else
+			check_cuda(cudaMemcpyPeerAsync(dp, dst_gpu, sp, src_gpu, bytes, s), "cudaMemcpyPeerAsync");
+		return;
+	}
+	// general strided box: (z, y, x) = padded (axis0, axis1, axis2)
+	int64_t ext[3] = {1, 1, 1}, sext[3] = {1, 1, 1}, dext[3] = {1, 1, 1};
+	for(int k = 0; k < rank; ++k) {
+		ext[3 - rank + k] = region.extent(k);
+		sext[3 - rank + k] = src_chunk.extent(k);
+		dext[3 - rank + k] = dst_chunk.extent(k);
+	}
+	if(src_gpu == dst_gpu || src_gpu < 0 || dst_gpu < 0) {
+		cudaMemcpy3DParms p{};
+		p.srcPtr = make_cudaPitchedPtr(const_cast<char*>(sp), static_cast<size_t>(sext[2]) * elem, static_cast<size_t>(sext[2]) * elem, static_cast<size_t>(sext[1]));
+		p.dstPtr = make_cudaPitchedPtr(dp, static_cast<size_t>(dext[2]) * elem, static_cast<size_t>(dext[2]) * elem, static_cast<size_t>(dext[1]));
+		p.extent = make_cudaExtent(static_cast<size_t>(ext[2]) * elem, static_cast<size_t>(ext[1]), static_cast<size_t>(ext[0]));
+		p.kind = (src_gpu < 0 || dst_gpu < 0) ? cudaMemcpyDefault : cudaMemcpyDeviceToDevice;
+		check_cuda(cudaMemcpy3DAsync(&p, s), "cudaMemcpy3DAsync");
+	} else {
+		cudaMemcpy3DPeerParms p{};
+		p.srcPtr = make_cudaPitchedPtr(const_cast<char*>(sp), static_cast<size_t>(sext[2]) * elem, static_cast<size_t>(sext[2]) * elem, static_cast<size_t>(sext[1]));
+		p.dstPtr = make_cudaPitchedPtr(dp, static_cast<size_t>(dext[2]) * elem, static_cast<size_t>(dext[2]) * elem, static_cast<size_t>(dext[1]));
+		p.srcDevice = src_gpu;
+		p.dstDevice = dst_gpu;
+		p.extent = make_cudaExtent(static_cast<size_t>(ext[2]) * elem, static_cast<size_t>(ext[1]), static_cast<size_t>(ext[0]));
+		check_cuda(cudaMemcpy3DPeerAsync(&p, s), "cudaMemcpy3DPeerAsync");
+	}
+}
+
+// ---- executor ------------------------------------------------------------------------------
+
+executor::executor(const executor_config& cfg) : cfg_(cfg) {
+	int n = 0;
+	const cudaError_t e = cudaGetDeviceCount(&n);
+	if(e != cudaSuccess || n == 0) throw execution_error("no CUDA device available for the B200 executor (" + std::string(cudaGetErrorString(e)) + ")");
+	const int ng = cfg.num_gpus > 0 ? std::min(cfg.num_gpus, n) : n;
+	gpus_.resize(static_cast<size_t>(ng));
+	for(int g = 0; g < ng; ++g) {
+		auto& G = gpus_[static_cast<size_t>(g)];
+		G.ordinal = g;
+		check_cuda(cudaSetDevice(g), "cudaSetDevice");
+		cudaMemPoolProps props{};
+		props.allocType = cudaMemAllocationTypePinned;
+		props.location.type = cudaMemLocationTypeDevice;
+		props.location.id = g;
+		check_cuda(cudaMemPoolCreate(&G.pool, &props), "cudaMemPoolCreate");
+		uint64_t threshold = std::numeric_limits<uint64_t>::max();
+		check_cuda(cudaMemPoolSetAttribute(G.pool, cudaMemPoolAttrReleaseThreshold, &threshold), "cudaMemPoolSetAttribute");
+		size_t free_b = 0, total_b = 0;
+		check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+		G.capacity = cfg.device_capacity ? cfg.device_capacity : static_cast<uint64_t>(static_cast<double>(free_b) * 0.9);
+		check_cuda(cudaStreamCreateWithFlags(&G.service, cudaStreamNonBlocking), "cudaStreamCreate");
+	}
+	free_events_.resize(static_cast<size_t>(ng));
+	for(int a = 0; a < ng; ++a) {
+		for(int b = 0; b < ng; ++b) {
+			if(a == b) continue;
+			int can = 0;
+			cudaDeviceCanAccessPeer(&can, a, b);
+			if(!can) continue;
+			cudaSetDevice(a);
+			const cudaError_t pe = cudaDeviceEnablePeerAccess(b, 0);
+			if(pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) check_cuda(pe, "cudaDeviceEnablePeerAccess");
+			cudaGetLastError();
+			// let kernels on `a` dereference chunks allocated from b's pool
+			cudaMemAccessDesc d{};
+			d.location.type = cudaMemLocationTypeDevice;
+			d.location.id = a;
+			d.flags = cudaMemAccessFlagsProtReadWrite;
+			check_cuda(cudaMemPoolSetAccess(gpus_[static_cast<size_t>(b)].pool, &d, 1), "cudaMemPoolSetAccess");
+		}
+	}
+	const int nw = cfg.workers, nd = cfg.devices_per_worker;
+	const int k = cfg.streams_per_device > 0 ? cfg.streams_per_device : 4;
+	ldevs_.resize(static_cast<size_t>(nw * nd));
+	for(int w = 0; w < nw; ++w) {
+		const bool local = cfg.local_workers < 0 || (w >= cfg.first_worker && w < cfg.first_worker + cfg.local_workers);
+		for(int d = 0; d < nd; ++d) {
+			auto& L = ldevs_[static_cast<size_t>(w * nd + d)];
+			const int global_index = local && cfg.local_workers >= 0 ? (w - cfg.first_worker) * nd + d : w * nd + d;
+			L.gpu = global_index % ng;
+			if(!local) continue;
+			check_cuda(cudaSetDevice(L.gpu), "cudaSetDevice");
+			L.compute.resize(static_cast<size_t>(k));
+			for(auto& s : L.compute) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+			check_cuda(cudaStreamCreateWithFlags(&L.copy, cudaStreamNonBlocking), "cudaStreamCreate");
+		}
+	}
+}
+
+executor::~executor() {
+	for(auto& G : gpus_) {
+		cudaSetDevice(G.ordinal);
+		cudaDeviceSynchronize();
+	}
+	for(auto& [id, b] : bufs_) {
+		cudaSetDevice(b.gpu);
+		cudaFree(b.ptr); // pool memory: cudaFree is legal on stream-ordered allocations
+	}
+	for(auto& [id, d] : done_) cudaEventDestroy(d.ev);
+	for(auto& pool : free_events_)
+		for(auto ev : pool) cudaEventDestroy(ev);
+	for(auto& L : ldevs_) {
+		for(auto s : L.compute) cudaStreamDestroy(s);
+		if(L.copy) cudaStreamDestroy(L.copy);
+	}
+	for(auto& G : gpus_) {
+		cudaSetDevice(G.ordinal);
+		cudaDeviceSynchronize();
+		if(G.service) cudaStreamDestroy(G.service);
+		if(G.pool) cudaMemPoolDestroy(G.pool);
+	}
+}
+
+int executor::gpu_of(device_id d) const { return ldevs_.at(static_cast<size_t>(d.worker * cfg_.devices_per_worker + d.device)).gpu; }
+
+executor::ldev& executor::dev(device_id d) {
+	if(d.worker < 0 || d.worker >= cfg_.workers || d.device < 0 || d.device >= cfg_.devices_per_worker)
+		throw validation_error("task routed to unknown device " + to_string(d));
+	auto& L = ldevs_[static_cast<size_t>(d.worker * cfg_.devices_per_worker + d.device)];
+	if(L.compute.empty()) throw validation_error("device " + to_string(d) + " is not executed by this process");
+	check_cuda(cudaSetDevice(L.gpu), "cudaSetDevice");
+	return L;
+}
+
+executor::buffer& executor::buf(int64_t chunk) {
+	const auto it = bufs_.find(chunk);
+	if(it == bufs_.end()) throw execution_error("no buffer for chunk " + std::to_string(chunk));
+	return it->second;
+}
+
+cudaEvent_t executor::take_event(int gpu) {
+	auto& pool = free_events_[static_cast<size_t>(gpu)];
+	if(!pool.empty()) {
+		cudaEvent_t ev = pool.back();
+		pool.pop_back();
+		return ev;
+	}
+	cudaEvent_t ev = nullptr;
+	check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+	return ev;
+}
+
+void executor::wait_deps(const task& t, cudaStream_t s) {
+	for(const auto d : t.deps) {
+		const auto it = done_.find(d);
+		if(it == done_.end() || it->second.stream == s) continue;
+		check_cuda(cudaStreamWaitEvent(s, it->second.ev, 0), "cudaStreamWaitEvent");
+	}
+}
+
+cudaStream_t executor::pick_compute(const task& t, ldev& L) {
+	int64_t best = -1;
+	cudaStream_t chosen = nullptr;
+	for(const auto d : t.deps) {
+		const auto it = done_.find(d);
+		if(it == done_.end() || d < best) continue;
+		for(auto s : L.compute) {
+			if(s == it->second.stream && tail_[s] == d) {
+				best = d;
+				chosen = s;
+			}
+		}
+	}
+	if(chosen) return chosen;
+	return L.compute[L.rr++ % L.compute.size()];
+}
+
+void executor::finish(const task& t, cudaStream_t s) {
+	int cur = 0;
+	cudaGetDevice(&cur);
+	cudaEvent_t ev = take_event(cur);
+	check_cuda(cudaEventRecord(ev, s), "cudaEventRecord");
+	done_[t.id] = {ev, s, cur};
+	tail_[s] = t.id;
+	++ctr_.tasks;
+	if(done_.size() > 16384) retire_completed();
+}
+
+void executor::retire_completed() {
+	for(auto it = done_.begin(); it != done_.end();) {
+		if(cudaEventQuery(it->second.ev) == cudaSuccess) {
+			free_events_[static_cast<size_t>(it->second.gpu)].push_back(it->second.ev);
+			it = done_.erase(it);
+		} else {
+			++it;
+		}
+	}
+	cudaGetLastError();
+}
+
+void executor::submit(const std::vector<task>& tasks) {
+	for(const auto& t : tasks) {
+		if(t.id <= last_id_) throw validation_error("tasks must be submitted in ascending id order");
+		last_id_ = t.id;
+		if(cfg_.local_workers >= 0 && (t.worker < cfg_.first_worker || t.worker >= cfg_.first_worker + cfg_.local_workers)) continue;
+		switch(t.kind) {
+		case task_kind::create: run_create(t); break;
+		case task_kind::del: run_delete(t); break;
+		case task_kind::execute: run_execute(t); break;
+		case task_kind::copy: run_copy(t); break;
+		case task_kind::send: run_send(t); break;
+		case task_kind::recv: run_recv(t); break;
+		case task_kind::reduce: run_reduce(t); break;
+		}
+	}
+}
+
+void executor::run_create(const task& t) {
+	ldev& L = dev(t.home);
+	cudaStream_t s = pick_compute(t, L);
+	wait_deps(t, s);
+	auto& G = gpus_[static_cast<size_t>(L.gpu)];
+	const uint64_t count = static_cast<uint64_t>(t.region.volume());
+	const uint64_t bytes = count * dtype_size(t.type);
+	if(bufs_.count(t.chunk)) throw execution_error("chunk " + std::to_string(t.chunk) + " created twice");
+	if(G.used + bytes > G.capacity)
+		throw execution_error("task " + std::to_string(t.id) + " needs " + std::to_string(bytes) + " bytes on GPU " + std::to_string(L.gpu) + " beyond its capacity "
+		                      + std::to_string(G.capacity));
+	void* p = nullptr;
+	check_cuda(cudaMallocFromPoolAsync(&p, bytes, G.pool, s), "cudaMallocFromPoolAsync");
+	G.used += bytes;
+	ctr_.peak_device_bytes = std::max(ctr_.peak_device_bytes, G.used);
+	device_fill(p, count, t.type, t.fill, t.fill_op, s);
+	++ctr_.kernels;
+	bufs_[t.chunk] = buffer{p, bytes, t.region, t.type, t.home, L.gpu};
+	finish(t, s);
+}
+
+void executor::run_delete(const task& t) {
+	buffer b = buf(t.chunk);
+	ldev& L = dev(b.home);
+	cudaStream_t s = pick_compute(t, L);
+	wait_deps(t, s);
+	check_cuda(cudaFreeAsync(b.ptr, s), "cudaFreeAsync");
+	gpus_[static_cast<size_t>(b.gpu)].used -= b.bytes;
+	bufs_.erase(t.chunk);
+	finish(t, s);
+}
+
+void executor::run_execute(const task& t) {
+	if(!t.kern) throw execution_error("execute task without a kernel");
+	const kernel_entry& k = *t.kern;
+	if(!k.launcher) throw execution_error("kernel \"" + k.id + "\" has no device launcher");
+	ldev& L = dev(t.device);
+	cudaStream_t s = pick_compute(t, L);
+	wait_deps(t, s);
+	const size_t np = t.args.size();
+	std::vector<int64_t> si(np, 0);
+	std::vector<double> sf(np, 0.0);
+	std::vector<mt_view> views(np);
+	std::memset(views.data(), 0, np * sizeof(mt_view));
+	for(size_t i = 0; i < np; ++i) {
+		const auto& a = t.args[i];
+		si[i] = a.i;
+		sf[i] = a.f;
+		if(a.kind != arg_kind::chunk) continue;
+		const buffer& b = buf(a.chunk);
+		if(b.gpu != L.gpu) throw execution_error("kernel argument chunk " + std::to_string(a.chunk) + " lives on another GPU");
+		auto& v = views[i];
+		v.base = b.ptr;
+		v.dtype = static_cast<int32_t>(b.type);
+		v.rank = b.region.rank();
+		int64_t st[kMaxRank];
+		strides_of(b.region, st);
+		for(int d = 0; d < v.rank; ++d) {
+			v.offset[d] = b.region.lo[d];
+			v.stride[d] = st[d];
+			v.extent[d] = b.region.extent(d);
+		}
+	}
+	mt_launch_ctx c{};
+	c.rank = t.sb_blocks.rank();
+	c.nparams = static_cast<int32_t>(np);
+	for(int d = 0; d < c.rank; ++d) {
+		c.block_offset[d] = t.sb_blocks.lo[d];
+		c.block_count[d] = t.sb_blocks.extent(d);
+		c.block_size[d] = t.block_size[d];
+		c.threads_lo[d] = t.sb_threads.lo[d];
+		c.threads_hi[d] = t.sb_threads.hi[d];
+	}
+	c.scalars_int = si.data();
+	c.scalars_float = sf.data();
+	c.views = views.data();
+	c.user = k.user;
+	const int rc = k.launcher(&c, s);
+	if(rc != 0) throw execution_error("kernel \"" + k.id + "\" launcher failed with code " + std::to_string(rc));
+	check_cuda(cudaGetLastError(), ("kernel \"" + k.id + "\" launch").c_str());
+	++ctr_.kernels;
+	last_exec_stream_ = s;
+	finish(t, s);
+}
+
+void executor::run_copy(const task& t) {
+	const buffer& src = buf(t.src);
+	const buffer& dst = buf(t.dst);
+	if(src.type != dst.type) throw execution_error("copy between chunks of different element types");
+	ldev& L = dev(t.resource);
+	cudaStream_t s = L.copy;
+	wait_deps(t, s);
+	copy_box(src.ptr, src.region, src.gpu, dst.ptr, dst.region, dst.gpu, t.dst_region, dtype_size(src.type), s);
+	++ctr_.copies;
+	ctr_.bytes_copied += static_cast<uint64_t>(t.dst_region.volume()) * dtype_size(src.type);
+	finish(t, s);
+}
+
+void executor::run_send(const task& t) {
+	const buffer& src = buf(t.chunk);
+	ldev& L = dev(t.resource);
+	cudaStream_t s = L.copy;
+	wait_deps(t, s);
+	auto& G = gpus_[static_cast<size_t>(L.gpu)];
+	message m;
+	m.bytes = static_cast<uint64_t>(t.region.volume()) * dtype_size(src.type);
+	m.gpu = L.gpu;
+	check_cuda(cudaMallocFromPoolAsync(&m.ptr, m.bytes, G.pool, s), "cudaMallocFromPoolAsync");
+	copy_box(src.ptr, src.region, src.gpu, m.ptr, t.region, L.gpu, t.region, dtype_size(src.type), s);
+	m.ready = take_event(L.gpu);
+	check_cuda(cudaEventRecord(m.ready, s), "cudaEventRecord");
+	const auto key = std::make_tuple(t.worker, t.peer, t.tag);
+	if(mailbox_.count(key)) throw execution_error("duplicate message tag");
+	mailbox_[key] = m;
+	ctr_.bytes_sent += m.bytes;
+	finish(t, s);
+}
+
+void executor::run_recv(const task& t) {
+	const auto key = std::make_tuple(t.peer, t.worker, t.tag);
+	const auto it = mailbox_.find(key);
+	if(it == mailbox_.end())
+		throw execution_error("receive (w" + std::to_string(t.peer) + " -> w" + std::to_string(t.worker) + ", tag " + std::to_string(t.tag)
+		                      + ") has no matching send (protocol violation)");
+	const message m = it->second;
+	mailbox_.erase(it);
+	const buffer& dst = buf(t.chunk);
+	ldev& L = dev(t.resource);
+	cudaStream_t s = L.copy;
+	wait_deps(t, s);
+	check_cuda(cudaStreamWaitEvent(s, m.ready, 0), "cudaStreamWaitEvent");
+	if(m.bytes != static_cast<uint64_t>(t.region.volume()) * dtype_size(dst.type))
+		throw execution_error("received payload size does not match the destination region");
+	copy_box(m.ptr, t.region, m.gpu, dst.ptr, dst.region, dst.gpu, t.region, dtype_size(dst.type), s);
+	// release the message buffer on its own device once the unpack is done
+	cudaEvent_t unpacked = take_event(L.gpu);
+	check_cuda(cudaEventRecord(unpacked, s), "cudaEventRecord");
+	auto& G = gpus_[static_cast<size_t>(m.gpu)];
+	check_cuda(cudaSetDevice(m.gpu), "cudaSetDevice");
+	check_cuda(cudaStreamWaitEvent(G.service, unpacked, 0), "cudaStreamWaitEvent");
+	check_cuda(cudaFreeAsync(m.ptr, G.service), "cudaFreeAsync");
+	check_cuda(cudaSetDevice(L.gpu), "cudaSetDevice");
+	free_events_[static_cast<size_t>(m.gpu)].push_back(m.ready);
+	free_events_[static_cast<size_t>(L.gpu)].push_back(unpacked);
+	ctr_.bytes_received += m.bytes;
+	finish(t, s);
+}
+
+void executor::run_reduce(const task& t) {
+	const buffer& out = buf(t.output);
+	ldev& L = dev(t.resource);
+	cudaStream_t s = pick_compute(t, L);
+	wait_deps(t, s);
+	std::vector<const void*> ins;
+	for(const auto c : t.inputs) {
+		const buffer& b = buf(c);
+		if(b.region != out.region) throw execution_error("reduce task combines chunks of different regions");
+		ins.push_back(b.ptr);
+	}
+	if(!ins.empty()) device_reduce(out.ptr, ins.data(), static_cast<int>(ins.size()), static_cast<uint64_t>(out.region.volume()), out.type, t.op, s);
+	++ctr_.kernels;
+	finish(t, s);
+}
+
+void executor::sync() {
+	std::string err;
+	for(auto& G : gpus_) {
+		cudaSetDevice(G.ordinal);
+		const cudaError_t e = cudaDeviceSynchronize();
+		if(e != cudaSuccess && err.empty()) err = std::string("device execution failed: ") + cudaGetErrorString(e);
+	}
+	for(auto& [id, d] : done_) free_events_[static_cast<size_t>(d.gpu)].push_back(d.ev);
+	done_.clear();
+	tail_.clear();
+	if(!err.empty()) throw execution_error(err);
+	if(!mailbox_.empty()) throw execution_error(std::to_string(mailbox_.size()) + " transport messages were never received (protocol violation)");
+}
+
+void executor::download(int64_t chunk, void* host, const box& host_box, const box& region) {
+	const buffer& b = buf(chunk);
+	if(!encloses(b.region, region) || !encloses(host_box, region)) throw validation_error("download region outside the chunk or the host box");
+	check_cuda(cudaSetDevice(b.gpu), "cudaSetDevice");
+	cudaStream_t s = gpus_[static_cast<size_t>(b.gpu)].service;
+	check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+	copy_box(b.ptr, b.region, b.gpu, host, host_box, -1, region, dtype_size(b.type), s);
+	check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+	ctr_.bytes_device_to_host += static_cast<uint64_t>(region.volume()) * dtype_size(b.type);
+}
+
+void executor::upload(int64_t chunk, const void* host, const box& host_box) {
+	const buffer& b = buf(chunk);
+	if(!encloses(host_box, b.region)) throw validation_error("upload: chunk outside the host box");
+	check_cuda(cudaSetDevice(b.gpu), "cudaSetDevice");
+	cudaStream_t s = gpus_[static_cast<size_t>(b.gpu)].service;
+	check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+	copy_box(host, host_box, -1, b.ptr, b.region, b.gpu, b.region, dtype_size(b.type), s);
+	check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+	ctr_.bytes_host_to_device += b.bytes;
+}
+
+std::string executor::report_json() const {
+	std::ostringstream os;
+	os << "{\"workers\": [";
+	for(int w = 0; w < cfg_.workers; ++w) {
+		os << (w ? ", " : "") << "{\"worker\": " << w << ", \"evictions\": " << (w == 0 ? ctr_.evictions : 0)
+		   << ", \"bytes_device_to_host\": " << (w == 0 ? ctr_.bytes_device_to_host : 0) << ", \"bytes_host_to_disk\": 0"
+		   << ", \"bytes_host_to_device\": " << (w == 0 ? ctr_.bytes_host_to_device : 0) << ", \"bytes_disk_to_device\": 0"
+		   << ", \"bytes_sent\": " << (w == 0 ? ctr_.bytes_sent : 0) << ", \"bytes_received\": " << (w == 0 ? ctr_.bytes_received : 0)
+		   << ", \"staging_checks\": 0, \"staging_violations\": 0, \"peak_device_bytes\": [" << ctr_.peak_device_bytes << "], \"tasks\": []}";
+	}
+	os << "], \"tasks\": " << ctr_.tasks << ", \"kernel_launches\": " << ctr_.kernels << ", \"copies\": " << ctr_.copies << ", \"bytes_copied\": " << ctr_.bytes_copied
+	   << "}";
+	return os.str();
+}
+
+} // namespace mtb

@@ -1,0 +1,154 @@
+// GPU executor: the B200 replacement for the reference's system_runtime
+// (proj/src/runtime.cpp:99-717).
+//
+// The reference runs one scheduler thread per worker that counts dependencies, stages chunks
+// through the memory manager and hands kernel bodies to one CPU thread per device. On B200 the
+// dependency DAG is resolved by the hardware instead: tasks arrive in id order (every
+// dependency points backwards, planner.cpp:35-40), each task is enqueued immediately on a CUDA
+// stream of its device, every dependency on another stream becomes a cudaStreamWaitEvent and
+// every task records one event. submit() therefore returns as soon as the work is queued, so
+// planning of launch n+1 overlaps execution of launch n with no host scheduler in the loop.
+//
+// Chunk store: per-GPU stream-ordered pool (cudaMallocFromPoolAsync / cudaFreeAsync), so a
+// chunk's allocation, fill, uses and release are all ordered on-device; fill_spec none is
+// zero-filled like the reference's std::vector::resize (SURVEY finding 4). Copies are
+// cudaMemcpy3D(Peer)Async over NVLink; send/recv pairs go through device message buffers
+// matched by (src worker, dst worker, tag); reduce tasks are one combine kernel reading its
+// inputs (peer memory where needed) in the reference's input order.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "plan.hpp"
+#include "registry.hpp"
+
+namespace mtb {
+
+struct executor_config {
+	int workers = 1;
+	int devices_per_worker = 1;
+	int num_gpus = 0;            // 0: all visible
+	int streams_per_device = 4;
+	uint64_t device_capacity = 0; // 0: 90% of free memory at start
+	int first_worker = 0;         // workers [first, first+local) execute here (multi-process)
+	int local_workers = -1;       // -1: all workers
+};
+
+struct exec_counters {
+	uint64_t tasks = 0;
+	uint64_t kernels = 0; // device launches issued by execute/reduce/fill
+	uint64_t copies = 0;
+	uint64_t bytes_copied = 0;
+	uint64_t bytes_sent = 0;
+	uint64_t bytes_received = 0;
+	uint64_t peak_device_bytes = 0;
+	uint64_t evictions = 0;
+	uint64_t bytes_device_to_host = 0;
+	uint64_t bytes_host_to_device = 0;
+};
+
+class executor {
+  public:
+	explicit executor(const executor_config& cfg);
+	~executor();
+	executor(const executor&) = delete;
+	executor& operator=(const executor&) = delete;
+
+	void submit(const std::vector<task>& tasks);
+	void sync();
+	// host transfers: `host` holds the row-major box `host_box`; `region` is copied. Both
+	// synchronise the chunk's GPU first (call after the tasks that produce the data).
+	void download(int64_t chunk, void* host, const box& host_box, const box& region);
+	void upload(int64_t chunk, const void* host, const box& host_box);
+	bool has_chunk(int64_t chunk) const { return bufs_.count(chunk) != 0; }
+	std::string report_json() const;
+	const exec_counters& counters() const { return ctr_; }
+
+	// stream of the most recent execute on a chunk's device (bench timing hook)
+	cudaStream_t last_exec_stream() const { return last_exec_stream_; }
+	int gpu_of(device_id d) const;
+
+  private:
+	struct buffer {
+		void* ptr = nullptr;
+		uint64_t bytes = 0;
+		box region;
+		dtype type = dtype::f32;
+		device_id home;
+		int gpu = 0;
+	};
+	struct ldev {
+		int gpu = 0;
+		std::vector<cudaStream_t> compute;
+		cudaStream_t copy = nullptr;
+		size_t rr = 0;
+	};
+	struct gpu_res {
+		int ordinal = 0;
+		cudaMemPool_t pool = nullptr;
+		uint64_t used = 0;
+		uint64_t capacity = 0;
+		cudaStream_t service = nullptr; // message-buffer releases
+	};
+	struct done_ev {
+		cudaEvent_t ev = nullptr;
+		cudaStream_t stream = nullptr;
+		int gpu = 0;
+	};
+	struct message {
+		void* ptr = nullptr;
+		uint64_t bytes = 0;
+		int gpu = 0;
+		cudaEvent_t ready = nullptr;
+	};
+
+	executor_config cfg_;
+	std::vector<gpu_res> gpus_;
+	std::vector<ldev> ldevs_; // worker-major
+	std::unordered_map<int64_t, buffer> bufs_;
+	std::unordered_map<int64_t, done_ev> done_;
+	std::unordered_map<cudaStream_t, int64_t> tail_;
+	std::map<std::tuple<int, int, uint64_t>, message> mailbox_;
+	std::vector<std::vector<cudaEvent_t>> free_events_; // per GPU
+	int64_t last_id_ = -1;
+	exec_counters ctr_;
+	cudaStream_t last_exec_stream_ = nullptr;
+	std::vector<std::string> kinds_seen_;
+
+	ldev& dev(device_id d);
+	cudaEvent_t take_event(int gpu);
+	void wait_deps(const task& t, cudaStream_t s);
+	cudaStream_t pick_compute(const task& t, ldev& L);
+	void finish(const task& t, cudaStream_t s);
+	void retire_completed();
+	buffer& buf(int64_t chunk);
+
+	void run_create(const task& t);
+	void run_delete(const task& t);
+	void run_execute(const task& t);
+	void run_copy(const task& t);
+	void run_send(const task& t);
+	void run_recv(const task& t);
+	void run_reduce(const task& t);
+};
+
+// region copy helpers (rank <= 3, row-major chunks); enqueue on `s`. A gpu index of -1 marks
+// a host buffer.
+void copy_box(const void* src_base, const box& src_chunk, int src_gpu, void* dst_base, const box& dst_chunk, int dst_gpu, const box& region,
+    size_t elem, cudaStream_t s);
+
+// device fill of `count` elements with the fill value of (kind, op) for `type`
+void device_fill(void* ptr, uint64_t count, dtype type, fill_kind kind, reduce_op op, cudaStream_t s);
+
+// out = in[0]; out = op(out, in[k]) for k >= 1 (runtime.cpp:463-504 semantics)
+void device_reduce(void* out, const void* const* inputs, int n, uint64_t count, dtype type, reduce_op op, cudaStream_t s);
+
+void check_cuda(cudaError_t e, const char* what);
+
+} // namespace mtb

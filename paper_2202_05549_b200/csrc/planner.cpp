@@ -1,0 +1,540 @@
+#include "planner.hpp"
+
+#include <numeric>
+
+namespace mtb {
+
+planner::planner(const planner_config& cfg) : cfg_(cfg), deps_(cfg.compat_deps) {
+	if(cfg.workers < 1 || cfg.devices_per_worker < 1) throw validation_error("system needs at least one worker with one device");
+	for(int w = 0; w < cfg.workers; ++w)
+		for(int d = 0; d < cfg.devices_per_worker; ++d) devices_.push_back({w, d});
+}
+
+const array_rec& planner::array(int64_t id) const {
+	const auto it = arrays_.find(id);
+	if(it == arrays_.end()) throw validation_error("array " + std::to_string(id) + " is not live");
+	return *it->second;
+}
+
+const chunk_meta& planner::chunk(int64_t id) const {
+	const auto it = chunks_.find(id);
+	if(it == chunks_.end()) throw validation_error("unknown chunk " + std::to_string(id));
+	return it->second;
+}
+
+void planner::add_local_kernel(kernel_entry e) {
+	if(e.id.empty()) throw validation_error("kernel id must not be empty");
+	for(const auto& p : e.params)
+		if(p.is_array && (p.rank < 1 || p.rank > kMaxRank))
+			throw validation_error("kernel \"" + e.id + "\" parameter \"" + p.name + "\" has unsupported rank");
+	for(const auto& k : local_kernels_)
+		if(k->id == e.id) throw validation_error("kernel \"" + e.id + "\" is already registered");
+	local_kernels_.push_back(std::make_unique<kernel_entry>(std::move(e)));
+}
+
+const kernel_entry* planner::find_kernel(const std::string& id) const {
+	for(const auto& k : local_kernels_)
+		if(k->id == id) return k.get();
+	const auto& table = kernel_table::get();
+	const int idx = table.find(id);
+	return idx < 0 ? nullptr : &table.at(idx);
+}
+
+std::vector<task> planner::take_pending() {
+	std::vector<task> out;
+	out.swap(pending_);
+	return out; // already in id order: ids are assigned at emission
+}
+
+int64_t planner::emit(task&& t) {
+	std::sort(t.deps.begin(), t.deps.end());
+	t.deps.erase(std::unique(t.deps.begin(), t.deps.end()), t.deps.end());
+	t.id = next_task_++;
+	task_worker_.push_back(t.worker);
+	if(cfg_.retain_plan) plan_.push_back(t);
+	pending_.push_back(std::move(t));
+	return next_task_ - 1;
+}
+
+int64_t planner::new_temp(const box& region, device_id home, dtype type) {
+	const int64_t id = next_chunk_++;
+	chunks_[id] = chunk_meta{chunk_desc{id, region, home}, type, true};
+	return id;
+}
+
+int64_t planner::emit_create(int worker, device_id dev, int64_t chunk_id, fill_kind fill, reduce_op op) {
+	const auto& m = chunk(chunk_id);
+	task t;
+	t.worker = worker;
+	t.resource = dev;
+	t.kind = task_kind::create;
+	t.chunk = chunk_id;
+	t.region = m.desc.region;
+	t.home = m.desc.home;
+	t.type = m.type;
+	t.fill = fill;
+	t.fill_op = op;
+	return emit(std::move(t));
+}
+
+// registry access for one task (array_registry.cpp:41-67 + planner.cpp:62-70)
+void planner::record(int64_t c, int64_t t, bool write, const box& region, bool check_filled, std::vector<int64_t>& out) {
+	if(check_filled && !deps_.filled(c))
+		throw plan_error("chunk " + std::to_string(c) + " is read before any fill or write; its contents would be undefined");
+	std::vector<int64_t> d;
+	if(write)
+		deps_.write(c, t, region, d);
+	else
+		deps_.read(c, t, region, d);
+	if(!cfg_.suppress_conflict_deps) out.insert(out.end(), d.begin(), d.end());
+}
+
+// copy within a worker, or a tagged send/recv pair across workers (planner.cpp:72-120)
+int64_t planner::transfer(int64_t src, int64_t dst, const box& region, std::vector<int64_t> src_deps, std::vector<int64_t> dst_deps) {
+	const chunk_meta sm = chunk(src), dm = chunk(dst);
+	if(sm.desc.home.worker == dm.desc.home.worker) {
+		const int64_t tid = next_task_;
+		std::vector<int64_t> d = std::move(src_deps);
+		d.insert(d.end(), dst_deps.begin(), dst_deps.end());
+		if(!sm.temp) record(src, tid, false, region, true, d);
+		if(!dm.temp) record(dst, tid, true, region, false, d);
+		task t;
+		t.worker = dm.desc.home.worker;
+		t.resource = dm.desc.home;
+		t.kind = task_kind::copy;
+		t.deps = std::move(d);
+		t.src = src;
+		t.dst = dst;
+		t.src_region = region;
+		t.dst_region = region;
+		const int64_t id = emit(std::move(t));
+		if(sm.temp) touch(src, id);
+		if(dm.temp) touch(dst, id);
+		return id;
+	}
+	const int sw = sm.desc.home.worker, dw = dm.desc.home.worker;
+	const uint64_t tag = tags_[{sw, dw}]++;
+	const int64_t send_tid = next_task_;
+	if(!sm.temp) record(src, send_tid, false, region, true, src_deps);
+	task s;
+	s.worker = sw;
+	s.resource = sm.desc.home;
+	s.kind = task_kind::send;
+	s.deps = std::move(src_deps);
+	s.chunk = src;
+	s.region = region;
+	s.peer = dw;
+	s.tag = tag;
+	const int64_t send_id = emit(std::move(s));
+	if(sm.temp) touch(src, send_id);
+	const int64_t recv_tid = next_task_;
+	if(!dm.temp) record(dst, recv_tid, true, region, false, dst_deps);
+	task r;
+	r.worker = dw;
+	r.resource = dm.desc.home;
+	r.kind = task_kind::recv;
+	r.deps = std::move(dst_deps);
+	r.chunk = dst;
+	r.region = region;
+	r.peer = sw;
+	r.tag = tag;
+	const int64_t recv_id = emit(std::move(r));
+	if(dm.temp) touch(dst, recv_id);
+	return recv_id;
+}
+
+const array_rec& planner::create_array(const box& domain, dtype type, std::vector<chunk_desc> chunks, fill_kind fill) {
+	for(auto& c : chunks) {
+		if(c.home.worker < 0 || c.home.worker >= cfg_.workers || c.home.device < 0 || c.home.device >= cfg_.devices_per_worker)
+			throw validation_error("chunk home " + to_string(c.home) + " is outside the configured system");
+		c.id = next_chunk_++;
+	}
+	if(domain.rank() < 1 || domain.rank() > kMaxRank) throw validation_error("arrays have between one and three dimensions");
+	if(domain.is_empty()) throw validation_error("array domain is empty");
+	for(const auto& c : chunks)
+		if(c.region.rank() != domain.rank()) throw validation_error("axis-count mismatch: chunk vs domain");
+	validate_chunks(chunks, domain);
+	auto rec = std::make_unique<array_rec>();
+	rec->id = next_array_++;
+	rec->domain = domain;
+	rec->type = type;
+	rec->chunks = std::move(chunks);
+	rec->index.build(rec->chunks);
+	array_rec& a = *rec;
+	arrays_.emplace(a.id, std::move(rec));
+	for(const auto& c : a.chunks) {
+		chunks_[c.id] = chunk_meta{c, type, false};
+		deps_.add_chunk(c.id, c.region);
+		const int64_t id = emit_create(c.home.worker, c.home, c.id, fill, reduce_op::plus);
+		deps_.mark_created(c.id, id, fill != fill_kind::none);
+	}
+	return a;
+}
+
+void planner::delete_array(int64_t id) {
+	const std::vector<chunk_desc> chunks = array(id).chunks;
+	for(const auto& c : chunks) {
+		std::vector<int64_t> d;
+		record(c.id, next_task_, true, c.region, false, d);
+		task t;
+		t.worker = c.home.worker;
+		t.resource = c.home;
+		t.kind = task_kind::del;
+		t.deps = std::move(d);
+		t.chunk = c.id;
+		emit(std::move(t));
+	}
+	for(const auto& c : chunks) deps_.drop_chunk(c.id);
+	arrays_.erase(id);
+}
+
+namespace {
+
+struct bound_param {
+	size_t param = 0;
+	int64_t array = -1;
+	const access_decl* acc = nullptr;
+	size_t access_index = 0;
+};
+
+} // namespace
+
+std::pair<int64_t, int64_t> planner::launch(const std::string& kernel, const box& grid, const point& block, const std::vector<superblock>& work,
+    const std::vector<launch_arg>& args, const annotation& ann) {
+	const int64_t first = next_task_;
+	const kernel_entry* kdef = find_kernel(kernel);
+	if(!kdef) throw plan_error("unknown kernel \"" + kernel + "\"");
+	const kernel_entry& def = *kdef;
+	const size_t np = def.params.size();
+
+	// signature checks (planner.cpp:163-213)
+	if(args.size() != np)
+		throw validation_error("kernel \"" + kernel + "\" takes " + std::to_string(np) + " arguments, got " + std::to_string(args.size()));
+	for(int k = 0; k < grid.rank(); ++k)
+		if(grid.lo[k] != 0) throw validation_error("launch grids start at the origin");
+	if(grid.is_empty()) throw validation_error("launch grid is empty");
+	if(block.rank != grid.rank()) throw validation_error("block size and grid axis counts differ");
+
+	std::vector<bound_param> bound(np);
+	std::vector<bool> is_array(np, false);
+	for(size_t i = 0; i < np; ++i) {
+		const auto& p = def.params[i];
+		const auto& a = args[i];
+		if(!p.is_array) {
+			const bool want_int = dtype_integral(p.type);
+			if(want_int && a.kind != launch_arg::int_k) throw validation_error("parameter \"" + p.name + "\" expects an integer scalar");
+			if(!want_int && a.kind != launch_arg::float_k) throw validation_error("parameter \"" + p.name + "\" expects a float scalar");
+			continue;
+		}
+		if(a.kind != launch_arg::array_k) throw validation_error("parameter \"" + p.name + "\" expects an array");
+		const array_rec& h = array(a.array);
+		if(h.type != p.type)
+			throw validation_error("parameter \"" + p.name + "\" expects element type " + dtype_name(p.type) + ", array has " + dtype_name(h.type));
+		if(h.domain.rank() != p.rank) throw validation_error("parameter \"" + p.name + "\" expects rank " + std::to_string(p.rank));
+		const access_decl* acc = ann.find(p.name);
+		if(!acc) throw validation_error("annotation does not mention array parameter \"" + p.name + "\"");
+		bound[i] = bound_param{i, a.array, acc, static_cast<size_t>(acc - ann.accesses.data())};
+		is_array[i] = true;
+	}
+	for(const auto& acc : ann.accesses) {
+		bool found = false;
+		for(size_t i = 0; i < np && !found; ++i) found = is_array[i] && def.params[i].name == acc.argument;
+		if(!found) throw validation_error("annotation mentions \"" + acc.argument + "\" which is not an array parameter");
+	}
+	for(size_t i = 0; i < np; ++i) {
+		if(!is_array[i]) continue;
+		for(size_t j = 0; j < np; ++j) {
+			if(j == i || !is_array[j] || bound[j].array != bound[i].array) continue;
+			const auto& m = bound[i].acc->mode;
+			if(m.writes() || m.reduces())
+				throw validation_error("one array is bound to several parameters and \"" + def.params[i].name + "\" writes or reduces into it");
+		}
+	}
+
+	// superblocks in thread space (whole blocks; planner.cpp:216-234)
+	point bext = point::zeros(grid.rank());
+	for(int k = 0; k < grid.rank(); ++k) {
+		if(block[k] <= 0) throw validation_error("block size must be positive");
+		bext[k] = (grid.extent(k) + block[k] - 1) / block[k];
+	}
+	validate_work(work, box::extents(bext));
+	const size_t S = work.size();
+	std::vector<box> sb_threads(S);
+	for(size_t s = 0; s < S; ++s) {
+		box t;
+		t.lo = point::zeros(grid.rank());
+		t.hi = point::zeros(grid.rank());
+		for(int k = 0; k < grid.rank(); ++k) {
+			t.lo[k] = work[s].blocks.lo[k] * block[k];
+			t.hi[k] = work[s].blocks.hi[k] * block[k];
+		}
+		sb_threads[s] = t;
+	}
+
+	// access regions per superblock (annotation.cpp:464-517)
+	const size_t A = ann.accesses.size();
+	std::vector<const array_rec*> acc_array(A, nullptr);
+	for(size_t i = 0; i < np; ++i)
+		if(is_array[i]) acc_array[bound[i].access_index] = &array(bound[i].array);
+	std::vector<box> regions(S * A);
+	std::vector<span> env(ann.vars.size() + 1);
+	for(size_t s = 0; s < S; ++s) {
+		make_env(ann, sb_threads[s], block, env.data());
+		for(size_t a = 0; a < A; ++a) regions[s * A + a] = eval_access(ann.accesses[a], env.data(), acc_array[a]->domain);
+	}
+
+	// overlapping plain writes between superblocks are a plan error (annotation.cpp:524-538)
+	for(size_t a = 0; a < A; ++a) {
+		const auto& m = ann.accesses[a].mode;
+		if(!m.writes() || m.reduces()) continue;
+		std::vector<size_t> order;
+		for(size_t s = 0; s < S; ++s)
+			if(!regions[s * A + a].is_empty()) order.push_back(s);
+		std::sort(order.begin(), order.end(), [&](size_t x, size_t y) { return regions[x * A + a].lo[0] < regions[y * A + a].lo[0]; });
+		for(size_t x = 0; x < order.size(); ++x) {
+			const box& rx = regions[order[x] * A + a];
+			for(size_t y = x + 1; y < order.size() && regions[order[y] * A + a].lo[0] < rx.hi[0]; ++y) {
+				const box ov = intersect(rx, regions[order[y] * A + a]);
+				if(!ov.is_empty())
+					throw plan_error("write conflict: superblocks " + std::to_string(std::min(order[x], order[y])) + " and "
+					                 + std::to_string(std::max(order[x], order[y])) + " both write \"" + ann.accesses[a].argument + "\" on " + to_string(ov));
+			}
+		}
+	}
+
+	// launch-wide bounding box per reduce access
+	std::vector<box> rbox(A);
+	for(size_t a = 0; a < A; ++a) {
+		if(!ann.accesses[a].mode.reduces()) continue;
+		box b = box::empty(acc_array[a]->domain.rank());
+		for(size_t s = 0; s < S; ++s) b = hull(b, regions[s * A + a]);
+		rbox[a] = b;
+	}
+
+	struct partial {
+		int64_t chunk, producer;
+	};
+	std::vector<std::vector<partial>> partials(A);
+	std::vector<int> cand;
+
+	for(size_t s = 0; s < S; ++s) {
+		const device_id dev = work[s].device;
+		const int worker = dev.worker;
+		std::vector<arg_bind> binds(np);
+		std::vector<int64_t> exec_deps;
+		struct rec_t {
+			int64_t chunk;
+			bool write;
+			bool check;
+			box region;
+		};
+		std::vector<rec_t> recs;
+		struct write_t {
+			size_t access;
+			box region;
+			int64_t source;
+			bool temp;
+		};
+		std::vector<write_t> writes;
+		std::vector<int64_t> dead;
+		std::vector<std::pair<size_t, int64_t>> sb_partials;
+
+		for(size_t i = 0; i < np; ++i) {
+			const auto& p = def.params[i];
+			if(!p.is_array) {
+				binds[i].kind = dtype_integral(p.type) ? arg_kind::scalar_int : arg_kind::scalar_float;
+				binds[i].i = args[i].i;
+				binds[i].f = args[i].f;
+				continue;
+			}
+			const bound_param& bp = bound[i];
+			const access_mode mode = bp.acc->mode;
+			const box& region = regions[s * A + bp.access_index];
+			const array_rec& h = array(bp.array);
+
+			if(mode.reduces()) {
+				const box& b = rbox[bp.access_index];
+				if(b.is_empty()) continue;
+				const int64_t part = new_temp(b, dev, h.type);
+				const int64_t create = emit_create(worker, dev, part, fill_kind::identity, mode.op);
+				touch(part, create);
+				exec_deps.push_back(create);
+				binds[i].kind = arg_kind::chunk;
+				binds[i].chunk = part;
+				sb_partials.emplace_back(bp.access_index, part);
+				continue;
+			}
+			if(region.is_empty()) continue;
+
+			h.index.query(region, cand);
+			const int enc = select_enclosing(h.chunks, cand, region, dev);
+			if(enc >= 0 && h.chunks[static_cast<size_t>(enc)].home == dev) {
+				const int64_t cid = h.chunks[static_cast<size_t>(enc)].id;
+				binds[i].kind = arg_kind::chunk;
+				binds[i].chunk = cid;
+				recs.push_back({cid, mode.writes(), mode.reads(), region});
+				if(mode.writes()) writes.push_back({bp.access_index, region, cid, false});
+				continue;
+			}
+			// stage a temporary on the executing device, pulled from the enclosing replica or
+			// assembled from every intersecting fragment (planner.cpp:324-347)
+			const int64_t temp = new_temp(region, dev, h.type);
+			const int64_t create = emit_create(worker, dev, temp, fill_kind::none, reduce_op::plus);
+			touch(temp, create);
+			exec_deps.push_back(create);
+			if(mode.reads()) {
+				std::vector<int> sources;
+				if(enc >= 0)
+					sources.push_back(enc);
+				else
+					sources = cand;
+				for(const int src : sources) {
+					const auto& sc = h.chunks[static_cast<size_t>(src)];
+					exec_deps.push_back(transfer(sc.id, temp, intersect(sc.region, region), {}, {create}));
+				}
+			}
+			binds[i].kind = arg_kind::chunk;
+			binds[i].chunk = temp;
+			if(mode.writes())
+				writes.push_back({bp.access_index, region, temp, true});
+			else
+				dead.push_back(temp);
+		}
+
+		const int64_t exec_tid = next_task_;
+		for(const auto& r : recs) record(r.chunk, exec_tid, r.write, r.region, r.check, exec_deps);
+		task e;
+		e.worker = worker;
+		e.resource = dev;
+		e.kind = task_kind::execute;
+		e.deps = std::move(exec_deps);
+		e.kern = kdef;
+		e.device = dev;
+		e.sb_blocks = work[s].blocks;
+		e.sb_threads = sb_threads[s];
+		e.block_size = block;
+		e.args = binds;
+		const int64_t exec_id = emit(std::move(e));
+		for(const auto& b : binds)
+			if(b.kind == arg_kind::chunk && chunk(b.chunk).temp) touch(b.chunk, exec_id);
+		for(const auto& [a, part] : sb_partials) partials[a].push_back({part, exec_id});
+
+		// propagate written regions into every other overlapping replica; scatter temps
+		for(const auto& w : writes) {
+			const array_rec& h = *acc_array[w.access];
+			h.index.query(w.region, cand);
+			for(const int t : cand) {
+				const auto& target = h.chunks[static_cast<size_t>(t)];
+				if(!w.temp && target.id == w.source) continue;
+				transfer(w.source, target.id, intersect(target.region, w.region), {exec_id}, {});
+			}
+			if(w.temp) dead.push_back(w.source);
+		}
+		for(const int64_t t : dead) {
+			task d;
+			d.worker = worker;
+			d.resource = dev;
+			d.kind = task_kind::del;
+			d.deps = temp_users_.at(t);
+			d.chunk = t;
+			emit(std::move(d));
+			temp_users_.erase(t);
+		}
+	}
+
+	// hierarchical reduction: device -> worker -> root w0d0 -> destination chunks
+	for(size_t a = 0; a < A; ++a) {
+		const auto& acc = ann.accesses[a];
+		if(!acc.mode.reduces() || partials[a].empty()) continue;
+		const box b = rbox[a];
+		const array_rec& h = *acc_array[a];
+		const dtype type = h.type;
+		const reduce_op op = acc.mode.op;
+		std::vector<int64_t> temps;
+		for(const auto& p : partials[a]) temps.push_back(p.chunk);
+
+		const auto emit_reduce = [&](int worker, device_id dev, const std::vector<partial>& in) -> partial {
+			const int64_t out = new_temp(b, dev, type);
+			temps.push_back(out);
+			const int64_t create = emit_create(worker, dev, out, fill_kind::none, reduce_op::plus);
+			touch(out, create);
+			task r;
+			r.worker = worker;
+			r.resource = dev;
+			r.kind = task_kind::reduce;
+			r.op = op;
+			r.output = out;
+			r.deps.push_back(create);
+			for(const auto& p : in) {
+				r.inputs.push_back(p.chunk);
+				r.deps.push_back(p.producer);
+			}
+			const int64_t rid = emit(std::move(r));
+			for(const auto& p : in) touch(p.chunk, rid);
+			touch(out, rid);
+			return {out, rid};
+		};
+
+		std::map<device_id, std::vector<partial>> by_dev;
+		for(const auto& p : partials[a]) by_dev[chunk(p.chunk).desc.home].push_back(p);
+		std::map<device_id, partial> dev_result;
+		for(const auto& [dev, parts] : by_dev) dev_result[dev] = parts.size() == 1 ? parts[0] : emit_reduce(dev.worker, dev, parts);
+
+		std::map<int, std::vector<partial>> by_worker;
+		for(const auto& [dev, res] : dev_result) by_worker[dev.worker].push_back(res);
+		std::map<int, partial> worker_result;
+		for(const auto& [w, res] : by_worker) worker_result[w] = res.size() == 1 ? res[0] : emit_reduce(w, chunk(res[0].chunk).desc.home, res);
+
+		const device_id root{0, 0};
+		std::vector<int64_t> final_inputs, final_deps;
+		for(const auto& [w, res] : worker_result) {
+			if(w == 0) {
+				final_inputs.push_back(res.chunk);
+				final_deps.push_back(res.producer);
+				continue;
+			}
+			const int64_t landing = new_temp(b, root, type);
+			temps.push_back(landing);
+			const int64_t create = emit_create(0, root, landing, fill_kind::none, reduce_op::plus);
+			touch(landing, create);
+			final_inputs.push_back(landing);
+			final_deps.push_back(transfer(res.chunk, landing, b, {res.producer}, {create}));
+		}
+		const int64_t fin = new_temp(b, root, type);
+		temps.push_back(fin);
+		const int64_t fin_create = emit_create(0, root, fin, fill_kind::none, reduce_op::plus);
+		touch(fin, fin_create);
+		final_deps.push_back(fin_create);
+		task r;
+		r.worker = 0;
+		r.resource = root;
+		r.kind = task_kind::reduce;
+		r.op = op;
+		r.inputs = final_inputs;
+		r.output = fin;
+		r.deps = std::move(final_deps);
+		const int64_t fin_id = emit(std::move(r));
+		for(const auto in : final_inputs) touch(in, fin_id);
+		touch(fin, fin_id);
+
+		h.index.query(b, cand);
+		for(const int t : cand) {
+			const auto& target = h.chunks[static_cast<size_t>(t)];
+			transfer(fin, target.id, intersect(target.region, b), {fin_id}, {});
+		}
+		for(const int64_t id : temps) {
+			const auto& m = chunk(id);
+			task d;
+			d.worker = m.desc.home.worker;
+			d.resource = m.desc.home;
+			d.kind = task_kind::del;
+			d.deps = temp_users_.at(id);
+			d.chunk = id;
+			emit(std::move(d));
+			temp_users_.erase(id);
+		}
+	}
+	return {first, next_task_};
+}
+
+} // namespace mtb

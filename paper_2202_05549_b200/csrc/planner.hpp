@@ -1,0 +1,96 @@
+// The driver: turns array/launch/delete requests into per-worker task DAGs.
+//
+// Task sequence, ids, kinds, chunk bindings, regions, tags and reduce input order are those
+// of the reference driver (proj/src/planner.cpp:30-520) for the same request sequence; only
+// the dependency lists differ, and only in region mode (see deps.hpp). Planning cost is
+// O(S log C) per launch (indexed chunk queries, sweep-based overlap checks) rather than the
+// reference's O(S^2 + S*C), so many launches can be planned ahead of GPU execution.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <unordered_map>
+#include <vector>
+
+#include "deps.hpp"
+#include "plan.hpp"
+#include "registry.hpp"
+
+namespace mtb {
+
+struct planner_config {
+	int workers = 1;
+	int devices_per_worker = 1;
+	bool suppress_conflict_deps = false;
+	bool compat_deps = false;
+	bool retain_plan = true; // keep every emitted task for mt_plan_export
+};
+
+struct launch_arg {
+	enum kind_t { int_k, float_k, array_k } kind = array_k;
+	int64_t i = 0;
+	double f = 0.0;
+	int64_t array = -1;
+};
+
+struct array_rec {
+	int64_t id = -1;
+	box domain;
+	dtype type = dtype::f32;
+	std::vector<chunk_desc> chunks; // ascending id
+	chunk_index index;
+};
+
+struct chunk_meta {
+	chunk_desc desc;
+	dtype type = dtype::f32;
+	bool temp = false;
+};
+
+class planner {
+  public:
+	explicit planner(const planner_config& cfg);
+
+	const std::vector<device_id>& devices() const { return devices_; }
+	const planner_config& config() const { return cfg_; }
+
+	const array_rec& create_array(const box& domain, dtype type, std::vector<chunk_desc> chunks, fill_kind fill);
+	void delete_array(int64_t id);
+	std::pair<int64_t, int64_t> launch(const std::string& kernel, const box& grid, const point& block, const std::vector<superblock>& work,
+	    const std::vector<launch_arg>& args, const annotation& ann);
+
+	std::vector<task> take_pending();
+	// context-local kernels shadow the global registry (the reference registers synthesized
+	// gather kernels per scenario, scenario.cpp:368-389)
+	void add_local_kernel(kernel_entry e);
+	const kernel_entry* find_kernel(const std::string& id) const;
+	const array_rec& array(int64_t id) const;
+	const chunk_meta& chunk(int64_t id) const;
+	const std::vector<task>& plan() const { return plan_; }
+	int64_t next_id() const { return next_task_; }
+	int worker_of(int64_t task) const { return task_worker_[static_cast<size_t>(task)]; }
+
+  private:
+	planner_config cfg_;
+	std::vector<device_id> devices_;
+	dep_tracker deps_;
+	std::map<int64_t, std::unique_ptr<array_rec>> arrays_;
+	int64_t next_array_ = 0;
+	int64_t next_chunk_ = 0;
+	int64_t next_task_ = 0;
+	std::unordered_map<int64_t, chunk_meta> chunks_;
+	std::vector<int> task_worker_;
+	std::vector<task> plan_, pending_;
+	std::map<std::pair<int, int>, uint64_t> tags_;
+	std::unordered_map<int64_t, std::vector<int64_t>> temp_users_;
+	std::vector<std::unique_ptr<kernel_entry>> local_kernels_;
+
+	int64_t emit(task&& t);
+	int64_t new_temp(const box& region, device_id home, dtype type);
+	void touch(int64_t temp, int64_t t) { temp_users_[temp].push_back(t); }
+	void record(int64_t chunk, int64_t t, bool write, const box& region, bool check_filled, std::vector<int64_t>& out);
+	int64_t transfer(int64_t src, int64_t dst, const box& region, std::vector<int64_t> src_deps, std::vector<int64_t> dst_deps);
+	int64_t emit_create(int worker, device_id dev, int64_t chunk, fill_kind fill, reduce_op op);
+};
+
+} // namespace mtb
