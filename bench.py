@@ -1,0 +1,314 @@
+#!/usr/bin/env python
+"""Benchmark: 2D 5-point heat stencil (f32) over annotated, chunked distributed arrays.
+
+Workload (BASELINE.json configs[1]): a 65536 x 65536 f32 grid, row-block stencil
+distribution (halo [1, 0]) over N GPUs, one distributed `heat2d` launch per step:
+planning (annotation -> regions -> tasks) + executor + halo exchange + kernel. Inputs are
+resident in HBM (2 x 16 GiB, far larger than the 126 MB L2, so no flush is needed).
+
+Reports (one JSON line, rank 0):
+  value     cell-updates/s over K timed steps, CUDA events (all streams joined), max over ranks
+  e2e       same metric through the public API with HOST buffers: per step, upload the grid
+            from pinned memory (mt_array_write), run `e2e_iters` heat iterations, read the
+            grid back (mt_array_read); wall clock around the synchronous calls
+  roofline  heat2d kernel: 8 algorithmic bytes per cell update / its average duration (CUDA
+            events on the launching stream) vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the reference CPU executor (oracle/_ref, the unmodified reference compiled from
+            its sources) running the same kernel on a bounded row sample, all host threads
+
+`--impl reference` times the reference CPU executor as the main arm (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "stencil cell-updates/s + matmul TFLOP/s at 1/2/4/8 B200; % roofline; vs CPU ref"
+ANN = "global [i, j] => read in[i-1:i+1, j-1:j+1], write out[i,j]"
+ALPHA = 0.1
+BYTES_PER_CELL = 8  # one f32 read + one f32 write per cell update
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def barrier_max(value: float, ws: int) -> float:
+    if ws == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def setup_heat(ctx, rows, cols, n_parts, block=(16, 16)):
+    from paper_2202_05549_b200 import Arr
+    devs = ctx.devices
+    dist = lambda: ctx.dist.stencil([rows, cols], [rows // n_parts, cols], [1, 0], devs)  # noqa: E731
+    a = ctx.create_array([rows, cols], "f32", dist(), 0)
+    b = ctx.create_array([rows, cols], "f32", dist(), 0)
+    work = ctx.dist.block_work([rows, cols], list(block), [rows // n_parts, cols], devs)
+    ctx.launch("ramp2d_f32", [rows, cols], list(block), work, [rows, cols, 1000, 0.0, 1.0, Arr(a)], "global [i, j] => write out[i,j]")
+    ctx.flush()
+    return a, b, work
+
+
+def cpu_reference_rate(rows, cols, iters, devices) -> tuple[float, float]:
+    """Reference CPU executor (oracle/_ref) on a rows x cols sample: (cell-updates/s, seconds)."""
+    import oracle
+    from paper_2202_05549_b200 import Arr
+    ctx = oracle.reference_context(workers=1, devices=devices, execute=True)
+    a, b, work = setup_heat(ctx, rows, cols, devices)
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN)
+        ctx.flush()
+        a, b = b, a
+    ctx.synchronize()
+    dt = time.perf_counter() - t0
+    ctx.close()
+    return rows * cols * iters / dt, dt
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    try:
+        import oracle
+        threads = oracle.reference().host_threads() if hasattr(oracle.reference(), "host_threads") else (os.cpu_count() or 1)
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"reference CPU executor not loadable: {e}"}))
+        return
+    devices = max(1, min(threads, 64))
+    rows = max(devices, args.ref_rows // devices * devices)
+    cols = args.cols
+    # warmup + timed: each step = one heat iteration over the sample
+    cpu_reference_rate(rows, cols, max(1, args.warmup), devices)
+    rate, dt = cpu_reference_rate(rows, cols, args.steps, devices)
+    sample = f"{rows}x{cols} rows sample of the {args.rows}x{args.cols} grid, {devices} chunks (stencil_dist halo [1,0]), 1 worker x {devices} device threads"
+    print(json.dumps({
+        "metric": METRIC, "impl": "reference", "value": rate, "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (ramp2d_f32 pattern)",
+        "config": {"workload": "heat2d 2D 5-point stencil f32, row-block stencil distribution", "rows": rows, "cols": cols, "iterations_per_step": 1},
+        "cpu_baseline": {"value": rate, "unit": "cell-updates/s", "cores": devices, "kind": "reference", "sample": sample},
+        "e2e": {"value": rate, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    rows, cols = args.rows, args.cols
+    n_parts = 1  # this process's share; multi-process sharding is per-rank below
+    if ws > 1:
+        rows = args.rows  # weak scaling: every rank owns a full-size shard of its own
+    ctx = mb.context(workers=1, devices=1, num_gpus=1)
+    a, b, work = setup_heat(ctx, rows, cols, n_parts)
+    ctx.synchronize()
+
+    def step():
+        nonlocal a, b
+        ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN)
+        ctx.flush()
+        a, b = b, a
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    stats0 = ctx.exec_stats()
+    ctx.profile_kernels(True)
+    k0, ms0 = ctx.kernel_time("heat2d")
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    ctx.mark(0)
+    for _ in range(args.steps):
+        step()
+    ctx.mark(1)
+    elapsed = ctx.elapsed_ms()
+    ctx.synchronize()
+    clocks = sampler.stop()
+    ctx.profile_kernels(False)
+    k1, ms1 = ctx.kernel_time("heat2d")
+    stats1 = ctx.exec_stats()
+    elapsed = barrier_max(elapsed, ws)
+    cells = rows * cols * args.steps * ws
+    value = cells / (elapsed / 1e3)
+    kern_ms = (ms1 - ms0) / max(1, k1 - k0)
+    achieved = BYTES_PER_CELL * rows * cols / (kern_ms / 1e3) / 1e9
+    peak, peak_kind = peaks()
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if args.e2e_runs > 0:
+        host_in = torch.empty((rows, cols), dtype=torch.float32, pin_memory=True)
+        host_out = torch.empty((rows, cols), dtype=torch.float32, pin_memory=True)
+        hin = host_in.numpy()
+        hout = host_out.numpy()
+        ctx.lib.check(ctx.lib.array_read(ctx.h, a, hin.ctypes.data, hin.nbytes))
+        times = []
+        for run in range(args.e2e_runs + 1):
+            t0 = time.perf_counter()
+            ctx.lib.check(ctx.lib.array_write(ctx.h, a, hin.ctypes.data, hin.nbytes))
+            for _ in range(args.e2e_iters):
+                step()
+            ctx.lib.check(ctx.lib.array_read(ctx.h, a, hout.ctypes.data, hout.nbytes))
+            dt = time.perf_counter() - t0
+            if run > 0:  # first run is warm-up
+                times.append(dt)
+        dt = barrier_max(max(times), ws) if times else float("nan")
+        e2e = {"value": rows * cols * args.e2e_iters * ws / (sum(times) / len(times)), "unit": "cell-updates/s",
+               "h2d_bytes_per_step": rows * cols * 4, "d2h_bytes_per_step": rows * cols * 4, "iterations_per_step": args.e2e_iters,
+               "steps": len(times), "worst_step_s": dt,
+               "note": "step = upload grid from pinned host memory + e2e iterations + read grid back, via mt_array_write/mt_launch/mt_array_read"}
+        del host_in, host_out
+
+    cpu = None
+    if rank == 0 and args.cpu_baseline:
+        try:
+            import oracle
+            threads = oracle.reference().host_threads()
+            devices = max(1, min(threads, 64))
+            rrows = max(devices, args.ref_rows // devices * devices)
+            rate, dt = cpu_reference_rate(rrows, cols, args.ref_iters, devices)
+            cpu = {"value": rate, "unit": "cell-updates/s", "cores": devices, "kind": "reference",
+                   "sample": f"{rrows}x{cols} rows x {args.ref_iters} iterations ({dt:.1f} s), {devices} chunks, 1 worker x {devices} device threads"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "cell-updates/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (ramp2d_f32 pattern generated on device)",
+            "config": {"workload": f"heat2d 2D 5-point stencil f32 {rows}x{cols} per GPU, row-block stencil distribution halo [1,0]",
+                       "rows": rows, "cols": cols, "alpha": ALPHA, "parallelism": f"dp{ws} (row blocks)", "l2": "inputs (2 x 16 GiB) >> L2, no flush"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "kernel": "heat2d_vec_kernel", "kernel_ms": kern_ms, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": BYTES_PER_CELL * rows * cols},
+            "clocks": clocks,
+            "gpu_launches": int(stats1.get("kernels", 0) - stats0.get("kernels", 0)),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    ctx.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--rows", type=int, default=65536)
+    p.add_argument("--cols", type=int, default=65536)
+    p.add_argument("--e2e-iters", type=int, default=100)
+    p.add_argument("--e2e-runs", type=int, default=2)
+    p.add_argument("--ref-rows", type=int, default=512)
+    p.add_argument("--ref-iters", type=int, default=6)
+    p.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = p.parse_args()
+    if args.impl == "reference":
+        if args.ref_rows == 512:
+            args.ref_rows = 128
+        run_reference_arm(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

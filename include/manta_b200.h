@@ -158,7 +158,18 @@ typedef struct mt_config {
 	uint64_t device_capacity;       /* bytes per device the chunk store may use (0 = 90% of free HBM) */
 	uint64_t host_capacity;         /* pinned-host spill tier bytes (0 = no spill tier)  */
 	uint64_t staging_threshold;     /* reference throttle; informational on the GPU path */
+	int32_t record_accesses;        /* keep (task, chunk, region, write) records for mt_plan_accesses */
+	int32_t pad_;
 } mt_config;
+
+/* One planned chunk access (a create counts as a write of the whole chunk). */
+typedef struct mt_access {
+	int64_t task;
+	int64_t chunk;
+	mt_rect region;
+	int32_t write;
+	int32_t pad_;
+} mt_access;
 
 typedef struct mt_ctx mt_ctx;
 typedef struct mt_exec mt_exec;
@@ -205,6 +216,9 @@ int mt_array_check_replicas(mt_ctx* ctx, int64_t array_id, int32_t* coherent);
 int mt_plan_export(mt_ctx* ctx, int64_t first, int64_t last, mt_task* tasks, int64_t task_cap, int64_t* ntasks, int64_t* pool, int64_t pool_cap,
     int64_t* npool, mt_arg_binding* args, int64_t args_cap, int64_t* nargs);
 int64_t mt_plan_size(mt_ctx* ctx);
+/* access records of non-temporary chunks in emission order (needs cfg.record_accesses);
+ * used to check that the dependency DAG orders every pair of conflicting accesses */
+int mt_plan_accesses(mt_ctx* ctx, mt_access* out, int64_t cap, int64_t* n_out);
 /* chunk_meta (planner.hpp:41-45): temp flag, dtype, descriptor */
 int mt_chunk_meta(mt_ctx* ctx, int64_t chunk, mt_chunk_desc* desc, int32_t* dtype, int32_t* temp);
 /* executor attached to a context (NULL when cfg.execute == 0) */
@@ -226,6 +240,13 @@ int mt_exec_report_json(mt_exec* ex, char* buf, int64_t cap, int64_t* len);
 int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n);
 /* cudaStream_t of the most recent execute task (for event timing on the launching stream) */
 void* mt_exec_last_stream(mt_exec* ex);
+/* device timing: mark(0) / mark(1) complete when all work enqueued before them has
+ * completed on every GPU; elapsed = max over GPUs of mark1 - mark0 */
+int mt_exec_mark(mt_exec* ex, int32_t slot);
+int mt_exec_elapsed_ms(mt_exec* ex, double* ms);
+/* per-kernel CUDA-event timing on the launching stream (count, total ms since enabled) */
+int mt_exec_profile(mt_exec* ex, int32_t on);
+int mt_exec_kernel_time(mt_exec* ex, const char* kernel, int64_t* count, double* total_ms);
 
 /* ---- kernel plugin API (kernels.hpp:56-105) ------------------------------------------ */
 /* View of one chunk as seen by a kernel: element (g0,g1,g2) lives at

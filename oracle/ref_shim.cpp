@@ -651,6 +651,8 @@ int mr_sync(mt_ctx* ctx) {
 int mr_array_read(mt_ctx* ctx, int64_t id, void* host, uint64_t bytes) {
 	return guarded([&] {
 		if(!ctx->has_exec) throw validation_error("context does not execute");
+		ctx->exec.rt->submit(ctx->drv->take_pending());
+		ctx->exec.rt->synchronize();
 		const auto& h = ctx->drv->registry().get(id);
 		const uint64_t need = static_cast<uint64_t>(h.domain.volume()) * dtype_size(h.type);
 		if(bytes < need) throw validation_error("host buffer too small");
@@ -666,6 +668,9 @@ int mr_array_write(mt_ctx*, int64_t, const void*, uint64_t) { return fail(MT_EVA
 
 int mr_array_check_replicas(mt_ctx* ctx, int64_t id, int32_t* coherent) {
 	return guarded([&] {
+		if(!ctx->has_exec) throw validation_error("context does not execute");
+		ctx->exec.rt->submit(ctx->drv->take_pending());
+		ctx->exec.rt->synchronize();
 		const auto& h = ctx->drv->registry().get(id);
 		const auto& chunks = h.distribution.chunks;
 		*coherent = 1;

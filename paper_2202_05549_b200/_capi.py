@@ -90,7 +90,12 @@ class Config(C.Structure):
         ("compat_deps", C.c_int32), ("execute", C.c_int32), ("num_gpus", C.c_int32),
         ("streams_per_device", C.c_int32), ("oracle_mode", C.c_int32),
         ("device_capacity", C.c_uint64), ("host_capacity", C.c_uint64), ("staging_threshold", C.c_uint64),
+        ("record_accesses", C.c_int32), ("pad_", C.c_int32),
     ]
+
+
+class Access(C.Structure):
+    _fields_ = [("task", C.c_int64), ("chunk", C.c_int64), ("region", Rect), ("write", C.c_int32), ("pad_", C.c_int32)]
 
 
 class View(C.Structure):
@@ -136,6 +141,7 @@ _SIGS = {
     "plan_export": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, P(Task), C.c_int64, P(C.c_int64), P(C.c_int64), C.c_int64, P(C.c_int64),
                               P(ArgBinding), C.c_int64, P(C.c_int64)]),
     "plan_size": (C.c_int64, [C.c_void_p]),
+    "plan_accesses": (C.c_int, [C.c_void_p, P(Access), C.c_int64, P(C.c_int64)]),
     "chunk_meta": (C.c_int, [C.c_void_p, C.c_int64, P(ChunkDesc), P(C.c_int32), P(C.c_int32)]),
     "ctx_exec": (C.c_void_p, [C.c_void_p]),
     "exec_create": (C.c_int, [P(Config), P(C.c_void_p)]),
@@ -147,6 +153,10 @@ _SIGS = {
     "exec_report_json": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, P(C.c_int64)]),
     "exec_stats": (C.c_int, [C.c_void_p, P(C.c_uint64), C.c_int32]),
     "exec_last_stream": (C.c_void_p, [C.c_void_p]),
+    "exec_mark": (C.c_int, [C.c_void_p, C.c_int32]),
+    "exec_elapsed_ms": (C.c_int, [C.c_void_p, P(C.c_double)]),
+    "exec_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+    "exec_kernel_time": (C.c_int, [C.c_void_p, C.c_char_p, P(C.c_int64), P(C.c_double)]),
     "kernel_register": (C.c_int, [C.c_char_p, P(ParamSpec), C.c_int32, LAUNCHER]),
     "kernel_count": (C.c_int, []),
     "ctx_kernel_register": (C.c_int, [C.c_void_p, C.c_char_p, P(ParamSpec), C.c_int32, C.c_void_p, C.c_void_p]),
@@ -159,7 +169,7 @@ _SIGS = {
 }
 # entry points the oracle shim may lack
 _OPTIONAL = {"exec_stats", "exec_last_stream", "kernel_info", "host_threads", "ctx_kernel_register", "fuzz_scenario_json", "scenario_plan",
-             "scenario_run"}
+             "scenario_run", "plan_accesses", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
 
 
 class MantaError(RuntimeError):

@@ -172,7 +172,7 @@ class Context:
     """driver + executor over one library (product `mt_` or oracle shim `mr_`)."""
 
     def __init__(self, lib: capi.Lib, workers=1, devices=1, execute=True, compat_deps=False, suppress_conflict_deps=False,
-                 num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0):
+                 num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0, record_accesses=False):
         self.lib = lib
         self.dist = Distributions(lib)
         cfg = capi.Config()
@@ -185,6 +185,7 @@ class Context:
         cfg.device_capacity = device_capacity
         cfg.host_capacity = host_capacity
         cfg.staging_threshold = staging_threshold
+        cfg.record_accesses = int(record_accesses)
         h = C.c_void_p()
         lib.check(lib.ctx_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -304,6 +305,14 @@ class Context:
     def plan(self, first=0, last=None) -> list[dict]:
         return self.export_plan(first, last).dicts()
 
+    def accesses(self) -> list[tuple]:
+        """(task, chunk, (lo, hi), write) for every planned access of a non-temporary chunk."""
+        n = C.c_int64(0)
+        self.lib.check(self.lib.plan_accesses(self.h, None, 0, C.byref(n)))
+        buf = (capi.Access * max(1, n.value))()
+        self.lib.check(self.lib.plan_accesses(self.h, buf, n.value, C.byref(n)))
+        return [(a.task, a.chunk, a.region.box(), bool(a.write)) for a in buf[: n.value]]
+
     def chunk_meta(self, chunk: int):
         desc = capi.ChunkDesc()
         dt, tmp = C.c_int32(0), C.c_int32(0)
@@ -318,6 +327,31 @@ class Context:
         self.lib.check(self.lib.exec_stats(ex, out, 7))
         keys = ["tasks", "kernels", "copies", "bytes_copied", "bytes_sent", "bytes_received", "peak_device_bytes"]
         return dict(zip(keys, [int(v) for v in out]))
+
+    # -- device timing (bench) ------------------------------------------------------
+    def _ex(self):
+        ex = self.lib.ctx_exec(self.h)
+        if not ex:
+            raise ValidationError("context does not execute")
+        return ex
+
+    def mark(self, slot: int):
+        """Device event completing when all work enqueued so far has completed (0=start, 1=stop)."""
+        self.flush()
+        self.lib.check(self.lib.exec_mark(self._ex(), slot))
+
+    def elapsed_ms(self) -> float:
+        v = C.c_double(0)
+        self.lib.check(self.lib.exec_elapsed_ms(self._ex(), C.byref(v)))
+        return v.value
+
+    def profile_kernels(self, on=True):
+        self.lib.check(self.lib.exec_profile(self._ex(), int(on)))
+
+    def kernel_time(self, kernel: str) -> tuple[int, float]:
+        n, ms = C.c_int64(0), C.c_double(0)
+        self.lib.check(self.lib.exec_kernel_time(self._ex(), kernel.encode(), C.byref(n), C.byref(ms)))
+        return n.value, ms.value
 
     def last_stream(self) -> int:
         ex = self.lib.ctx_exec(self.h)

@@ -274,6 +274,7 @@ int mt_ctx_create(const mt_config* cfg, mt_ctx** out) {
 		pc.devices_per_worker = cfg->devices_per_worker;
 		pc.suppress_conflict_deps = cfg->suppress_conflict_deps != 0;
 		pc.compat_deps = cfg->compat_deps != 0;
+		pc.record_accesses = cfg->record_accesses != 0;
 		ctx->plan = std::make_unique<planner>(pc);
 		if(cfg->execute) {
 			ctx->exec = std::make_unique<mt_exec>();
@@ -409,6 +410,21 @@ int mt_plan_export(mt_ctx* ctx, int64_t first, int64_t last, mt_task* tasks, int
 
 int64_t mt_plan_size(mt_ctx* ctx) { return static_cast<int64_t>(ctx->plan->plan().size()); }
 
+int mt_plan_accesses(mt_ctx* ctx, mt_access* out, int64_t cap, int64_t* n_out) {
+	return guarded([&] {
+		const auto& a = ctx->plan->accesses();
+		*n_out = static_cast<int64_t>(a.size());
+		for(size_t i = 0; i < a.size() && static_cast<int64_t>(i) < cap; ++i) {
+			mt_access r{};
+			r.task = a[i].task;
+			r.chunk = a[i].chunk;
+			r.region = from_box(a[i].region);
+			r.write = a[i].write ? 1 : 0;
+			out[i] = r;
+		}
+	});
+}
+
 int mt_chunk_meta(mt_ctx* ctx, int64_t chunk, mt_chunk_desc* desc, int32_t* dt, int32_t* temp) {
 	return guarded([&] {
 		const auto& m = ctx->plan->chunk(chunk);
@@ -481,6 +497,22 @@ int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n) {
 }
 
 void* mt_exec_last_stream(mt_exec* ex) { return ex->ex->last_exec_stream(); }
+
+int mt_exec_mark(mt_exec* ex, int32_t slot) {
+	return guarded([&] { ex->ex->mark(slot); });
+}
+
+int mt_exec_elapsed_ms(mt_exec* ex, double* ms) {
+	return guarded([&] { *ms = ex->ex->elapsed_ms(); });
+}
+
+int mt_exec_profile(mt_exec* ex, int32_t on) {
+	return guarded([&] { ex->ex->set_profile(on != 0); });
+}
+
+int mt_exec_kernel_time(mt_exec* ex, const char* kernel, int64_t* count, double* total_ms) {
+	return guarded([&] { ex->ex->kernel_time(kernel, count, total_ms); });
+}
 
 namespace {
 kernel_entry make_entry(const char* id, const mt_param_spec* params, int32_t nparams, mt_launcher_fn launcher, const void* user) {

@@ -265,6 +265,8 @@ executor::executor(const executor_config& cfg) : cfg_(cfg) {
 		check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
 		G.capacity = cfg.device_capacity ? cfg.device_capacity : static_cast<uint64_t>(static_cast<double>(free_b) * 0.9);
 		check_cuda(cudaStreamCreateWithFlags(&G.service, cudaStreamNonBlocking), "cudaStreamCreate");
+		check_cuda(cudaStreamCreateWithFlags(&G.timing, cudaStreamNonBlocking), "cudaStreamCreate");
+		for(auto& m : G.marks) check_cuda(cudaEventCreate(&m), "cudaEventCreate");
 	}
 	free_events_.resize(static_cast<size_t>(ng));
 	for(int a = 0; a < ng; ++a) {
@@ -323,6 +325,9 @@ executor::~executor() {
 		cudaSetDevice(G.ordinal);
 		cudaDeviceSynchronize();
 		if(G.service) cudaStreamDestroy(G.service);
+		if(G.timing) cudaStreamDestroy(G.timing);
+		for(auto m : G.marks)
+			if(m) cudaEventDestroy(m);
 		if(G.pool) cudaMemPoolDestroy(G.pool);
 	}
 }
@@ -498,7 +503,17 @@ void executor::run_execute(const task& t) {
 	c.scalars_float = sf.data();
 	c.views = views.data();
 	c.user = k.user;
+	cudaEvent_t kt0 = nullptr, kt1 = nullptr;
+	if(profile_) {
+		check_cuda(cudaEventCreate(&kt0), "cudaEventCreate");
+		check_cuda(cudaEventCreate(&kt1), "cudaEventCreate");
+		check_cuda(cudaEventRecord(kt0, s), "cudaEventRecord");
+	}
 	const int rc = k.launcher(&c, s);
+	if(profile_) {
+		check_cuda(cudaEventRecord(kt1, s), "cudaEventRecord");
+		ktimes_[k.id].pending.emplace_back(kt0, kt1);
+	}
 	if(rc != 0) throw execution_error("kernel \"" + k.id + "\" launcher failed with code " + std::to_string(rc));
 	check_cuda(cudaGetLastError(), ("kernel \"" + k.id + "\" launch").c_str());
 	++ctr_.kernels;
@@ -583,6 +598,47 @@ void executor::run_reduce(const task& t) {
 	if(!ins.empty()) device_reduce(out.ptr, ins.data(), static_cast<int>(ins.size()), static_cast<uint64_t>(out.region.volume()), out.type, t.op, s);
 	++ctr_.kernels;
 	finish(t, s);
+}
+
+void executor::mark(int slot) {
+	if(slot < 0 || slot > 1) throw validation_error("mark slot must be 0 or 1");
+	for(auto& G : gpus_) {
+		check_cuda(cudaSetDevice(G.ordinal), "cudaSetDevice");
+		for(const auto& [s, tail] : tail_) {
+			const auto it = done_.find(tail);
+			if(it == done_.end() || it->second.gpu != G.ordinal) continue;
+			check_cuda(cudaStreamWaitEvent(G.timing, it->second.ev, 0), "cudaStreamWaitEvent");
+		}
+		check_cuda(cudaEventRecord(G.marks[slot], G.timing), "cudaEventRecord");
+	}
+}
+
+double executor::elapsed_ms() {
+	double worst = 0.0;
+	for(auto& G : gpus_) {
+		check_cuda(cudaSetDevice(G.ordinal), "cudaSetDevice");
+		check_cuda(cudaEventSynchronize(G.marks[1]), "cudaEventSynchronize");
+		float ms = 0.f;
+		check_cuda(cudaEventElapsedTime(&ms, G.marks[0], G.marks[1]), "cudaEventElapsedTime");
+		worst = std::max(worst, static_cast<double>(ms));
+	}
+	return worst;
+}
+
+void executor::kernel_time(const std::string& kernel, int64_t* count, double* total_ms) {
+	auto& kt = ktimes_[kernel];
+	for(auto& [a, b] : kt.pending) {
+		check_cuda(cudaEventSynchronize(b), "cudaEventSynchronize");
+		float ms = 0.f;
+		check_cuda(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+		kt.total_ms += ms;
+		kt.count += 1;
+		cudaEventDestroy(a);
+		cudaEventDestroy(b);
+	}
+	kt.pending.clear();
+	*count = kt.count;
+	*total_ms = kt.total_ms;
 }
 
 void executor::sync() {

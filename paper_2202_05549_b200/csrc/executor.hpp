@@ -74,6 +74,16 @@ class executor {
 	cudaStream_t last_exec_stream() const { return last_exec_stream_; }
 	int gpu_of(device_id d) const;
 
+	// Device-side timing. mark(0)/mark(1) record, on every GPU, an event that completes when
+	// all work enqueued so far (every stream) has completed; elapsed_ms() is the max over
+	// GPUs of mark(1) - mark(0).
+	void mark(int slot);
+	double elapsed_ms();
+	// Per-kernel event timing on the launching stream (bench roofline): when enabled every
+	// execute task's launcher call is bracketed by timing events.
+	void set_profile(bool on) { profile_ = on; }
+	void kernel_time(const std::string& kernel, int64_t* count, double* total_ms);
+
   private:
 	struct buffer {
 		void* ptr = nullptr;
@@ -95,6 +105,13 @@ class executor {
 		uint64_t used = 0;
 		uint64_t capacity = 0;
 		cudaStream_t service = nullptr; // message-buffer releases
+		cudaStream_t timing = nullptr;
+		cudaEvent_t marks[2] = {nullptr, nullptr};
+	};
+	struct kernel_timing {
+		std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+		int64_t count = 0;
+		double total_ms = 0.0;
 	};
 	struct done_ev {
 		cudaEvent_t ev = nullptr;
@@ -119,7 +136,8 @@ class executor {
 	int64_t last_id_ = -1;
 	exec_counters ctr_;
 	cudaStream_t last_exec_stream_ = nullptr;
-	std::vector<std::string> kinds_seen_;
+	bool profile_ = false;
+	std::map<std::string, kernel_timing> ktimes_;
 
 	ldev& dev(device_id d);
 	cudaEvent_t take_event(int gpu);

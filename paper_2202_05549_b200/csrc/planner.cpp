@@ -87,6 +87,7 @@ void planner::record(int64_t c, int64_t t, bool write, const box& region, bool c
 	else
 		deps_.read(c, t, region, d);
 	if(!cfg_.suppress_conflict_deps) out.insert(out.end(), d.begin(), d.end());
+	if(cfg_.record_accesses) accesses_.push_back({t, c, region, write});
 }
 
 // copy within a worker, or a tagged send/recv pair across workers (planner.cpp:72-120)
@@ -167,6 +168,7 @@ const array_rec& planner::create_array(const box& domain, dtype type, std::vecto
 		deps_.add_chunk(c.id, c.region);
 		const int64_t id = emit_create(c.home.worker, c.home, c.id, fill, reduce_op::plus);
 		deps_.mark_created(c.id, id, fill != fill_kind::none);
+		if(cfg_.record_accesses) accesses_.push_back({id, c.id, c.region, true});
 	}
 	return a;
 }

@@ -24,6 +24,7 @@ struct planner_config {
 	bool suppress_conflict_deps = false;
 	bool compat_deps = false;
 	bool retain_plan = true; // keep every emitted task for mt_plan_export
+	bool record_accesses = false;
 };
 
 struct launch_arg {
@@ -69,6 +70,12 @@ class planner {
 	const std::vector<task>& plan() const { return plan_; }
 	int64_t next_id() const { return next_task_; }
 	int worker_of(int64_t task) const { return task_worker_[static_cast<size_t>(task)]; }
+	struct access_rec {
+		int64_t task, chunk;
+		box region;
+		bool write;
+	};
+	const std::vector<access_rec>& accesses() const { return accesses_; }
 
   private:
 	planner_config cfg_;
@@ -84,6 +91,7 @@ class planner {
 	std::map<std::pair<int, int>, uint64_t> tags_;
 	std::unordered_map<int64_t, std::vector<int64_t>> temp_users_;
 	std::vector<std::unique_ptr<kernel_entry>> local_kernels_;
+	std::vector<access_rec> accesses_;
 
 	int64_t emit(task&& t);
 	int64_t new_temp(const box& region, device_id home, dtype type);
