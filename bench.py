@@ -47,6 +47,22 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel_file: str, rows: int, cols: int):
+    """dram read+write bytes per launch from the newest committed `ncu --set full` capture of
+    this kernel (profiles/round*/<kernel_file>), when it was taken on the same grid."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "round*", kernel_file))):
+        try:
+            with open(path) as f:
+                s = json.load(f)
+        except Exception:
+            continue
+        if s.get("algorithmic_bytes_per_launch") == BYTES_PER_CELL * rows * cols:
+            best = (s["traffic_bytes_per_launch"], os.path.relpath(path, ROOT))
+    return best
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -266,6 +282,7 @@ def run_b200(args):
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "cell-updates/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
+    traffic = ncu_traffic("heat2d_ncu_summary.json", rows, cols)
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -273,7 +290,8 @@ def run_b200(args):
             "data": "synthetic (ramp2d_f32 pattern generated on device)",
             "config": {"workload": f"heat2d 2D 5-point stencil f32 {rows}x{cols} per GPU, row-block stencil distribution halo [1,0]",
                        "rows": rows, "cols": cols, "alpha": ALPHA, "parallelism": f"dp{ws} (row blocks)", "l2": "inputs (2 x 16 GiB) >> L2, no flush"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic[0] if traffic else None, "traffic_source": traffic[1] if traffic else None,
                          "kernel": "heat2d_vec_kernel", "kernel_ms": kern_ms, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": BYTES_PER_CELL * rows * cols},
             "clocks": clocks,
