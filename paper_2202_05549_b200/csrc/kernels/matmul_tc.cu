@@ -1,8 +1,363 @@
-// Dense contraction kernels on the 5th-generation tensor cores (tcgen05 / TMEM / TMA).
+// Dense contraction on the 5th-generation tensor cores: C (f32) = A (bf16) x Bt^T (bf16).
+//
+// BASELINE config C3 (dense matmul with tiled distribution). The reference's `matmul`
+// (kernels.cpp:167-193) is a scalar f32 loop; this is the tensor-core contraction the
+// north_star asks for, registered as kernel `matmul_nt_bf16`:
+//   params  (m, n, k : i64, C : f32[2] writable, A : bf16[2], Bt : bf16[2])
+//   annot.  global [i, j] => write C[i,j], read A[i,:], read Bt[j,:]
+//   C[i,j] = sum_l A[i,l] * Bt[j,l]   (products exact in f32, f32 accumulation)
+// Both operands are K-major (Bt is B transposed), the layout UMMA consumes natively.
+//
+// Kernel structure (persistent, one CTA per SM, 192 threads, 6 warps):
+//   warp 0   TMA producer: 128x64 A and 256x64 Bt bf16 boxes (128B swizzle) into a 4-stage
+//            smem ring, completion counted on `full` mbarriers (expect_tx)
+//   warp 1   TMEM allocator + MMA issuer: one elected lane issues tcgen05.mma.cta_group::1
+//            .kind::f16, M=128 N=256 K=16, 4 per stage, accumulating in TMEM; tcgen05.commit
+//            frees the smem stage (`empty`) and, after the last K block, signals `tmem_full`
+//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 (each warp its 32 TMEM lanes = rows), f32
+//            stores to C with edge masking, then arrive `tmem_empty`
+// TMEM holds two 128x256 f32 accumulators (512 columns), so the epilogue of tile t overlaps
+// the MMAs of tile t+1. Tiles are rasterised in groups of 16 M-blocks so the ~148 tiles in
+// flight share A/B K-slices through L2.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../executor.hpp"
 #include "../registry.hpp"
+#include "common.cuh"
 
 namespace mtb {
+namespace tc {
 
-void register_matmul_kernels(kernel_table&) {}
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4, UMMA_K = 16;
+constexpr int NUM_THREADS = 192;
+constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;  // 32 KB
+constexpr uint32_t STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr uint32_t TMEM_COLS = 512;                // two 256-column f32 accumulators
+constexpr int GROUP_M = 16;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+
+struct gemm_args {
+	float* c;
+	int64_t ldc;       // elements
+	int64_t m, n, k;   // problem (rows of C, cols of C, reduction)
+	int64_t a_row0;    // A tensor-map row of output row 0
+	int64_t b_row0;    // Bt tensor-map row of output col 0
+	int m_blocks, n_blocks, k_blocks;
+};
+
+// ---- PTX wrappers -------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+	asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+	asm volatile(
+	    "{\n\t.reg .pred P1;\n\t"
+	    "WAIT_%=:\n\t"
+	    "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+	    "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+	    "r"(parity)
+	    : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+	asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+	asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t x, int32_t y) {
+	asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+	    "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+	    : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+	asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+	asm volatile(
+	    "{\n\t.reg .pred p;\n\t"
+	    "setp.ne.b32 p, %4, 0;\n\t"
+	    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+	    "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// K-major operand, 128-byte swizzle: 8-row atoms of 1024 B (SBO), version 1, layout type 2
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+	uint64_t d = 0;
+	d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+	d |= static_cast<uint64_t>(1) << 16;            // LBO (unused for swizzled K-major)
+	d |= static_cast<uint64_t>(1024 >> 4) << 32;    // SBO
+	d |= static_cast<uint64_t>(1) << 46;            // descriptor version (sm_100)
+	d |= static_cast<uint64_t>(2) << 61;            // SWIZZLE_128B
+	return d;
+}
+
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major, M=128, N=256
+__host__ __device__ constexpr uint32_t instr_desc() {
+	return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+	asm volatile(
+	    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%"
+	    "28,%29,%30,%31}, [%32];"
+	    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+	    "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+	    "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+	    : "r"(taddr));
+	asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tile_coords(int t, const gemm_args& p, int& mb, int& nb) {
+	const int group = GROUP_M * p.n_blocks;
+	const int g = t / group;
+	const int first_m = g * GROUP_M;
+	const int rows = min(GROUP_M, p.m_blocks - first_m);
+	const int r = t % group;
+	mb = first_m + r % rows;
+	nb = r / rows;
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_bf16_nt_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, gemm_args p) {
+	extern __shared__ uint8_t smem_raw[];
+	uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+	uint8_t* a_smem = smem;
+	uint8_t* b_smem = smem + STAGES * A_STAGE_BYTES;
+	uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+	uint64_t* full = bars;
+	uint64_t* empty = bars + STAGES;
+	uint64_t* tmem_full = bars + 2 * STAGES;
+	uint64_t* tmem_empty = bars + 2 * STAGES + 2;
+	uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+	const int warp = threadIdx.x / 32;
+	const int lane = threadIdx.x % 32;
+	const int num_tiles = p.m_blocks * p.n_blocks;
+
+	if(warp == 0 && lane == 0) {
+		for(int s = 0; s < STAGES; ++s) {
+			mbar_init(&full[s], 1);
+			mbar_init(&empty[s], 1);
+		}
+		for(int a = 0; a < 2; ++a) {
+			mbar_init(&tmem_full[a], 1);
+			mbar_init(&tmem_empty[a], 4);
+		}
+		asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+		asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
+		asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
+	}
+	if(warp == 1) {
+		asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(TMEM_COLS) : "memory");
+		asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+	}
+	tc_fence_before();
+	__syncthreads();
+	tc_fence_after();
+	const uint32_t tmem_base = *tmem_slot;
+
+	if(warp == 0) {
+		if(lane == 0) {
+			// ---- TMA producer ----
+			int stage = 0;
+			uint32_t phase = 0;
+			for(int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+				int mb, nb;
+				tile_coords(t, p, mb, nb);
+				const int32_t arow = static_cast<int32_t>(p.a_row0 + static_cast<int64_t>(mb) * BM);
+				const int32_t brow = static_cast<int32_t>(p.b_row0 + static_cast<int64_t>(nb) * BN);
+				for(int kb = 0; kb < p.k_blocks; ++kb) {
+					mbar_wait(&empty[stage], phase ^ 1);
+					mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+					tma_load_2d(a_smem + stage * A_STAGE_BYTES, &tmap_a, &full[stage], kb * BK, arow);
+					tma_load_2d(b_smem + stage * B_STAGE_BYTES, &tmap_b, &full[stage], kb * BK, brow);
+					if(++stage == STAGES) {
+						stage = 0;
+						phase ^= 1;
+					}
+				}
+			}
+		}
+	} else if(warp == 1) {
+		if(lane == 0) {
+			// ---- MMA issuer ----
+			constexpr uint32_t idesc = instr_desc();
+			int stage = 0;
+			uint32_t phase = 0;
+			int local = 0;
+			for(int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+				const int acc = local & 1;
+				mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
+				tc_fence_after();
+				const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+				for(int kb = 0; kb < p.k_blocks; ++kb) {
+					mbar_wait(&full[stage], phase);
+					tc_fence_after();
+					const uint32_t a0 = smem_u32(a_smem + stage * A_STAGE_BYTES);
+					const uint32_t b0 = smem_u32(b_smem + stage * B_STAGE_BYTES);
+#pragma unroll
+					for(int k = 0; k < BK / UMMA_K; ++k)
+						tc_mma(d, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+					tc_commit(&empty[stage]);
+					if(++stage == STAGES) {
+						stage = 0;
+						phase ^= 1;
+					}
+				}
+				tc_commit(&tmem_full[acc]);
+			}
+		}
+	} else {
+		// ---- epilogue: warps 2..5, TMEM lanes 32*(warp%4) .. +31 ----
+		const int quarter = warp & 3;
+		int local = 0;
+		for(int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+			int mb, nb;
+			tile_coords(t, p, mb, nb);
+			const int acc = local & 1;
+			mbar_wait(&tmem_full[acc], (local >> 1) & 1);
+			tc_fence_after();
+			const int64_t row = static_cast<int64_t>(mb) * BM + quarter * 32 + lane;
+			const bool row_ok = row < p.m;
+			float* crow = p.c + row * p.ldc;
+			const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+			for(int c = 0; c < BN; c += 32) {
+				uint32_t r[32];
+				tmem_ld32(taddr + static_cast<uint32_t>(c), r);
+				const int64_t col0 = static_cast<int64_t>(nb) * BN + c;
+				if(!row_ok) continue;
+				if(col0 + 32 <= p.n && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0)) {
+#pragma unroll
+					for(int v = 0; v < 8; ++v) {
+						float4 f = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]), __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+						*reinterpret_cast<float4*>(crow + col0 + 4 * v) = f;
+					}
+				} else {
+					for(int v = 0; v < 32; ++v)
+						if(col0 + v < p.n) crow[col0 + v] = __uint_as_float(r[v]);
+				}
+			}
+			tc_fence_before();
+			__syncwarp();
+			if(lane == 0) mbar_arrive(&tmem_empty[acc]);
+		}
+	}
+	__syncthreads();
+	if(warp == 1) {
+		tc_fence_after();
+		asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
+	}
+}
+
+// ---- host side -------------------------------------------------------------------------------
+
+using encode_fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+encode_fn get_encode() {
+	static encode_fn fn = nullptr;
+	static std::once_flag once;
+	std::call_once(once, [] {
+		void* p = nullptr;
+		cudaDriverEntryPointQueryResult q{};
+		if(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+			fn = reinterpret_cast<encode_fn>(p);
+	});
+	return fn;
+}
+
+// 2D bf16 K-major operand: `rows` x `cols` (cols contiguous), row pitch `ld` elements
+bool make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_rows) {
+	encode_fn enc = get_encode();
+	if(!enc) return false;
+	const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+	const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+	const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), box_rows};
+	const cuuint32_t estride[2] = {1, 1};
+	return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+	           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
+	       == CUDA_SUCCESS;
+}
+
+int num_sms() {
+	int dev = 0, sms = 148;
+	cudaGetDevice(&dev);
+	cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+	return sms;
+}
+
+// a: rows [a_row0, a_row0 + m) of an (a_rows x k) matrix; bt likewise for n.
+int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const void* bt, int64_t b_rows, int64_t ldb, int64_t b_row0, float* c,
+    int64_t ldc, int64_t m, int64_t n, int64_t k, cudaStream_t s) {
+	if(m <= 0 || n <= 0) return 0;
+	if(k <= 0) return 5;
+	if((lda * 2) % 16 || (ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(a) % 16) || (reinterpret_cast<uintptr_t>(bt) % 16)) return 6;
+	CUtensorMap ma, mb;
+	if(!make_map(&ma, a, a_rows, k, lda, BM) || !make_map(&mb, bt, b_rows, k, ldb, BN)) return 7;
+	gemm_args p{};
+	p.c = c;
+	p.ldc = ldc;
+	p.m = m;
+	p.n = n;
+	p.k = k;
+	p.a_row0 = a_row0;
+	p.b_row0 = b_row0;
+	p.m_blocks = static_cast<int>((m + BM - 1) / BM);
+	p.n_blocks = static_cast<int>((n + BN - 1) / BN);
+	p.k_blocks = static_cast<int>((k + BK - 1) / BK);
+	kern::ensure_smem(gemm_bf16_nt_kernel, static_cast<int>(SMEM_BYTES));
+	const int tiles = p.m_blocks * p.n_blocks;
+	const int grid = std::min(tiles, num_sms());
+	gemm_bf16_nt_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+	return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+} // namespace tc
+
+int launch_matmul_nt_bf16(const mt_launch_ctx* c, void* stream) {
+	const int64_t m = c->scalars_int[0], n = c->scalars_int[1], k = c->scalars_int[2];
+	const int64_t r0 = c->threads_lo[0], r1 = std::min(c->threads_hi[0], m);
+	const int64_t c0 = c->threads_lo[1], c1 = std::min(c->threads_hi[1], n);
+	if(r0 >= r1 || c0 >= c1) return 0;
+	const mt_view& vc = c->views[3];
+	const mt_view& va = c->views[4];
+	const mt_view& vb = c->views[5];
+	if(!vc.base || !va.base || !vb.base) return 2;
+	if(va.offset[1] != 0 || vb.offset[1] != 0 || va.extent[1] < k || vb.extent[1] < k) return 3; // whole K rows staged
+	float* cp = static_cast<float*>(vc.base) + (r0 - vc.offset[0]) * vc.stride[0] + (c0 - vc.offset[1]) * vc.stride[1];
+	return tc::run_gemm(va.base, va.extent[0], va.stride[0], r0 - va.offset[0], vb.base, vb.extent[0], vb.stride[0], c0 - vb.offset[0], cp, vc.stride[0],
+	    r1 - r0, c1 - c0, k, static_cast<cudaStream_t>(stream));
+}
+
+void register_matmul_kernels(kernel_table& t) {
+	t.add({"matmul_nt_bf16",
+	    {param_sig{"m", false, dtype::i64, 0, false}, param_sig{"n", false, dtype::i64, 0, false}, param_sig{"k", false, dtype::i64, 0, false},
+	        param_sig{"C", true, dtype::f32, 2, true}, param_sig{"A", true, dtype::bf16, 2, false}, param_sig{"Bt", true, dtype::bf16, 2, false}},
+	    launch_matmul_nt_bf16});
+}
 
 } // namespace mtb
+
+// direct entry for tests and the bench's contraction line (device pointers, row-major)
+extern "C" int mt_gemm_bf16_nt(const void* a, const void* bt, float* c, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, void* stream) {
+	return mtb::tc::run_gemm(a, m, lda, 0, bt, n, ldb, 0, c, ldc, m, n, k, static_cast<cudaStream_t>(stream));
+}

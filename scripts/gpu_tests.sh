@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -30
+python -c "import __graft_entry__ as g; g.smoke()"

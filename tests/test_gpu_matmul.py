@@ -1,0 +1,80 @@
+"""tcgen05 bf16 contraction (csrc/kernels/matmul_tc.cu) against an fp64 reference of the same
+bf16 inputs. Tolerance (north_star: <= 1e-3 for contractions): every element of C within
+1e-3 relative of the fp64 result (inputs are non-negative, so there is no cancellation and
+the elementwise relative error is meaningful)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2202_05549_b200 as mb
+from paper_2202_05549_b200 import Arr
+
+pytestmark = pytest.mark.gpu
+REL = 1e-3
+
+
+def _gemm_fn():
+    fn = mb.lib().dll.mt_gemm_bf16_nt
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]
+    return fn
+
+
+def pattern(rows, cols, mod, off):
+    i = np.arange(rows, dtype=np.int64)[:, None]
+    j = np.arange(cols, dtype=np.int64)[None, :]
+    return ((i * 31 + j * 17 + off) % mod).astype(np.float32) / mod
+
+
+def to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    """round-to-nearest-even f32 -> bf16 bit patterns"""
+    u = x.astype(np.float32).view(np.uint32)
+    r = ((u >> 16) & 1) + 0x7FFF
+    return ((u + r) >> 16).astype(np.uint16)
+
+
+def from_bf16_bits(b: np.ndarray) -> np.ndarray:
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (300, 520, 136), (1024, 768, 1000), (2048, 2048, 4096)])
+def test_gemm_matches_fp64(m, n, k):
+    import torch
+    a = to_bf16_bits(pattern(m, k, 1000, 7))
+    bt = to_bf16_bits(pattern(n, k, 997, 3))
+    da = torch.from_numpy(a.view(np.int16)).cuda()
+    db = torch.from_numpy(bt.view(np.int16)).cuda()
+    dc = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+    rc = _gemm_fn()(da.data_ptr(), db.data_ptr(), dc.data_ptr(), m, n, k, k, k, n, torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    got = dc.cpu().numpy().astype(np.float64)
+    want = from_bf16_bits(a).astype(np.float64) @ from_bf16_bits(bt).astype(np.float64).T
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+    assert np.isfinite(got).all()
+    assert rel.max() <= REL, rel.max()
+
+
+def test_matmul_nt_bf16_through_the_planner():
+    """C tiled over a 2x2 device grid; A row panels and Bt column panels are assembled into
+    per-device temporaries by the planner (replicated-input transfers, planner.cpp:324-347)."""
+    m, n, k = 512, 768, 320
+    a = to_bf16_bits(pattern(m, k, 1000, 7))
+    bt = to_bf16_bits(pattern(n, k, 997, 3))
+    with mb.context(workers=2, devices=2, num_gpus=1) as ctx:
+        devs = ctx.devices
+        A = ctx.create_array([m, k], "bf16", ctx.dist.row([m, k], 128, devs), 0)
+        B = ctx.create_array([n, k], "bf16", ctx.dist.row([n, k], 192, devs), 0)
+        Cm = ctx.create_array([m, n], "f32", ctx.dist.tile([m, n], [256, 384], devs), 0)
+        ctx.write(A, a)
+        ctx.write(B, bt)
+        work = ctx.dist.block_work([m, n], [16, 16], [256, 384], devs)
+        ctx.launch("matmul_nt_bf16", [m, n], [16, 16], work, [m, n, k, Arr(Cm), Arr(A), Arr(B)],
+                   "global [i, j] => write C[i,j], read A[i,:], read Bt[j,:]")
+        got = ctx.read(Cm).astype(np.float64)
+        kinds = [t["kind"] for t in ctx.plan()]
+    want = from_bf16_bits(a).astype(np.float64) @ from_bf16_bits(bt).astype(np.float64).T
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+    assert rel.max() <= REL
+    assert kinds.count("execute") == 4 and kinds.count("send") > 0
