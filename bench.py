@@ -162,6 +162,66 @@ def cpu_reference_rate(rows, cols, iters, devices) -> tuple[float, float]:
     return rows * cols * iters / dt, dt
 
 
+def bf16_ramp_row(i, n, mod):
+    """host restatement of ramp2d_bf16 for row i (f32 ramp, round-to-nearest-even to bf16)"""
+    import numpy as np
+    j = np.arange(n, dtype=np.int64)
+    v = (((i * 31 + j * 17 + 7) % mod).astype(np.float64) / mod).astype(np.float32)
+    u = v.view(np.uint32).astype(np.uint64)
+    u = ((u + (((u >> 16) & 1) + 0x7FFF)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def run_contraction(ctx, n, steps, warmup):
+    """BASELINE config C3 on one GPU: C (f32) = A (bf16) x Bt^T (bf16), n^3, through the planner
+    (one superblock per GPU) and the tcgen05 kernel; TFLOP/s from device events."""
+    from paper_2202_05549_b200 import Arr
+    dev = ctx.devices
+    A = ctx.create_array([n, n], "bf16", ctx.dist.single([n, n], dev[0]), 0)
+    B = ctx.create_array([n, n], "bf16", ctx.dist.single([n, n], dev[0]), 0)
+    Cm = ctx.create_array([n, n], "f32", ctx.dist.single([n, n], dev[0]), 0)
+    w = ctx.dist.block_work([n, n], [16, 16], [n, n], dev)
+    ctx.launch("ramp2d_bf16", [n, n], [16, 16], w, [n, n, 1000, 0.0, 1.0, Arr(A)], "global [i, j] => write out[i,j]")
+    ctx.launch("ramp2d_bf16", [n, n], [16, 16], w, [n, n, 997, 0.0, 1.0, Arr(B)], "global [i, j] => write out[i,j]")
+    ann = "global [i, j] => write C[i,j], read A[i,:], read Bt[j,:]"
+
+    def step():
+        ctx.launch("matmul_nt_bf16", [n, n], [16, 16], w, [n, n, n, Arr(Cm), Arr(A), Arr(B)], ann)
+        ctx.flush()
+
+    for _ in range(warmup):
+        step()
+    ctx.synchronize()
+    k0, ms0 = ctx.kernel_time("matmul_nt_bf16")
+    ctx.profile_kernels(True)
+    ctx.mark(0)
+    for _ in range(steps):
+        step()
+    ctx.mark(1)
+    elapsed = ctx.elapsed_ms()
+    ctx.synchronize()
+    ctx.profile_kernels(False)
+    k1, ms1 = ctx.kernel_time("matmul_nt_bf16")
+    # spot check 16 elements against an fp64 host dot product of the same bf16 inputs
+    import numpy as np
+    c = ctx.read(Cm)
+    rng = np.random.default_rng(0)
+    worst = 0.0
+    for _ in range(16):
+        i, j = int(rng.integers(n)), int(rng.integers(n))
+        want = float(bf16_ramp_row(i, n, 1000) @ bf16_ramp_row(j, n, 997))
+        worst = max(worst, abs(float(c[i, j]) - want) / max(abs(want), 1e-30))
+    del c
+    for a in (A, B, Cm):
+        ctx.delete_array(a)
+    ctx.synchronize()
+    flop = 2.0 * n ** 3
+    kern_ms = (ms1 - ms0) / max(1, k1 - k0)
+    return {"workload": f"matmul_nt_bf16 {n}^3 (C f32 = A bf16 x Bt^T bf16), 1 superblock", "value": flop * steps / (elapsed / 1e3) / 1e12,
+            "unit": "TFLOP/s", "steps": steps, "ms_per_step": elapsed / steps, "kernel_ms": kern_ms,
+            "max_rel_err_16_samples_vs_fp64": worst}
+
+
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -282,6 +342,19 @@ def run_b200(args):
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "cell-updates/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
+    contraction = None
+    if args.matmul_n > 0:
+        contraction = run_contraction(ctx, args.matmul_n, args.matmul_steps, 2)
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                pk = json.load(f)
+            tpeak, tburst = float(pk["bf16_tflops_sustained"]), float(pk["bf16_tflops"])
+        except Exception:
+            tpeak, tburst = 1400.0, 1590.0
+        kach = 2.0 * args.matmul_n ** 3 / (contraction["kernel_ms"] / 1e3) / 1e12
+        contraction["roofline"] = {"bound": "tensor", "achieved": kach, "peak": tpeak, "unit": "TFLOP/s", "frac": kach / tpeak,
+                                   "peak_kind": "measured sustained (cuBLAS bf16, 4 s loop)", "frac_of_burst": kach / tburst,
+                                   "kernel": "gemm_bf16_nt_kernel (tcgen05.mma cta_group::1 M128 N256, TMA, TMEM)"}
     traffic = ncu_traffic("heat2d_ncu_summary.json", rows, cols)
     if rank == 0:
         out = {
@@ -298,6 +371,7 @@ def run_b200(args):
             "gpu_launches": int(stats1.get("kernels", 0) - stats0.get("kernels", 0)),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "contraction": contraction,
         }
         print(json.dumps(out))
     ctx.close()
@@ -319,6 +393,8 @@ def main():
     p.add_argument("--ref-rows", type=int, default=512)
     p.add_argument("--ref-iters", type=int, default=6)
     p.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    p.add_argument("--matmul-n", type=int, default=32768, help="C3 contraction size (0 to skip)")
+    p.add_argument("--matmul-steps", type=int, default=5)
     args = p.parse_args()
     if args.impl == "reference":
         if args.ref_rows == 512:
