@@ -159,7 +159,7 @@ typedef struct mt_config {
 	uint64_t host_capacity;         /* pinned-host spill tier bytes (0 = no spill tier)  */
 	uint64_t staging_threshold;     /* reference throttle; informational on the GPU path */
 	int32_t record_accesses;        /* keep (task, chunk, region, write) records for mt_plan_accesses */
-	int32_t pad_;
+	int32_t lookahead_tasks;        /* spill tier: tasks buffered ahead for Belady eviction (0 = 512) */
 } mt_config;
 
 /* One planned chunk access (a create counts as a write of the whole chunk). */
@@ -236,7 +236,7 @@ int mt_exec_write_chunk(mt_exec* ex, int64_t chunk, const void* src, uint64_t by
 int mt_exec_report_json(mt_exec* ex, char* buf, int64_t cap, int64_t* len);
 
 /* counters: tasks, device launches, copies, bytes copied, bytes sent, bytes received, peak
- * device bytes (first n of them) */
+ * device bytes, evictions, spill bytes D2H, spill bytes H2D (first n of them) */
 int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n);
 /* cudaStream_t of the most recent execute task (for event timing on the launching stream) */
 void* mt_exec_last_stream(mt_exec* ex);

@@ -90,7 +90,7 @@ class Config(C.Structure):
         ("compat_deps", C.c_int32), ("execute", C.c_int32), ("num_gpus", C.c_int32),
         ("streams_per_device", C.c_int32), ("oracle_mode", C.c_int32),
         ("device_capacity", C.c_uint64), ("host_capacity", C.c_uint64), ("staging_threshold", C.c_uint64),
-        ("record_accesses", C.c_int32), ("pad_", C.c_int32),
+        ("record_accesses", C.c_int32), ("lookahead_tasks", C.c_int32),
     ]
 
 

@@ -172,7 +172,8 @@ class Context:
     """driver + executor over one library (product `mt_` or oracle shim `mr_`)."""
 
     def __init__(self, lib: capi.Lib, workers=1, devices=1, execute=True, compat_deps=False, suppress_conflict_deps=False,
-                 num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0, record_accesses=False):
+                 num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0, record_accesses=False,
+                 lookahead_tasks=0):
         self.lib = lib
         self.dist = Distributions(lib)
         cfg = capi.Config()
@@ -186,6 +187,7 @@ class Context:
         cfg.host_capacity = host_capacity
         cfg.staging_threshold = staging_threshold
         cfg.record_accesses = int(record_accesses)
+        cfg.lookahead_tasks = int(lookahead_tasks)
         h = C.c_void_p()
         lib.check(lib.ctx_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -323,9 +325,10 @@ class Context:
         ex = self.lib.ctx_exec(self.h)
         if not ex or not self.lib.has("exec_stats"):
             return {}
-        out = (C.c_uint64 * 7)()
-        self.lib.check(self.lib.exec_stats(ex, out, 7))
-        keys = ["tasks", "kernels", "copies", "bytes_copied", "bytes_sent", "bytes_received", "peak_device_bytes"]
+        keys = ["tasks", "kernels", "copies", "bytes_copied", "bytes_sent", "bytes_received", "peak_device_bytes", "evictions",
+                "spill_bytes_d2h", "spill_bytes_h2d", "dead_drops", "dead_skips"]
+        out = (C.c_uint64 * len(keys))()
+        self.lib.check(self.lib.exec_stats(ex, out, len(keys)))
         return dict(zip(keys, [int(v) for v in out]))
 
     # -- device timing (bench) ------------------------------------------------------

@@ -196,6 +196,8 @@ executor_config exec_cfg(const mt_config& c) {
 	e.num_gpus = c.num_gpus;
 	e.streams_per_device = c.streams_per_device > 0 ? c.streams_per_device : 4;
 	e.device_capacity = c.device_capacity;
+	e.host_capacity = c.host_capacity;
+	e.lookahead = c.lookahead_tasks > 0 ? c.lookahead_tasks : 512;
 	return e;
 }
 
@@ -491,7 +493,8 @@ int mt_exec_report_json(mt_exec* ex, char* buf, int64_t cap, int64_t* len) {
 int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n) {
 	return guarded([&] {
 		const auto& c = ex->ex->counters();
-		const uint64_t v[] = {c.tasks, c.kernels, c.copies, c.bytes_copied, c.bytes_sent, c.bytes_received, c.peak_device_bytes};
+		const uint64_t v[] = {c.tasks, c.kernels, c.copies, c.bytes_copied, c.bytes_sent, c.bytes_received, c.peak_device_bytes, c.evictions,
+		    c.bytes_device_to_host, c.bytes_host_to_device, c.dead_drops, c.dead_skips};
 		for(int32_t i = 0; i < n && i < static_cast<int32_t>(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
 	});
 }

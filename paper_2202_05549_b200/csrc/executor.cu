@@ -1,5 +1,7 @@
 #include "executor.hpp"
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <sstream>
@@ -266,8 +268,11 @@ executor::executor(const executor_config& cfg) : cfg_(cfg) {
 		G.capacity = cfg.device_capacity ? cfg.device_capacity : static_cast<uint64_t>(static_cast<double>(free_b) * 0.9);
 		check_cuda(cudaStreamCreateWithFlags(&G.service, cudaStreamNonBlocking), "cudaStreamCreate");
 		check_cuda(cudaStreamCreateWithFlags(&G.timing, cudaStreamNonBlocking), "cudaStreamCreate");
+		check_cuda(cudaStreamCreateWithFlags(&G.h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+		check_cuda(cudaStreamCreateWithFlags(&G.d2h, cudaStreamNonBlocking), "cudaStreamCreate");
 		for(auto& m : G.marks) check_cuda(cudaEventCreate(&m), "cudaEventCreate");
 	}
+	spill_ = cfg.host_capacity > 0;
 	free_events_.resize(static_cast<size_t>(ng));
 	for(int a = 0; a < ng; ++a) {
 		for(int b = 0; b < ng; ++b) {
@@ -312,8 +317,10 @@ executor::~executor() {
 	}
 	for(auto& [id, b] : bufs_) {
 		cudaSetDevice(b.gpu);
-		cudaFree(b.ptr); // pool memory: cudaFree is legal on stream-ordered allocations
+		if(b.ptr) cudaFree(b.ptr); // pool memory: cudaFree is legal on stream-ordered allocations
+		if(b.host) cudaFreeHost(b.host);
 	}
+	for(auto& [sz, blk] : host_free_) cudaFreeHost(blk.first);
 	for(auto& [id, d] : done_) cudaEventDestroy(d.ev);
 	for(auto& pool : free_events_)
 		for(auto ev : pool) cudaEventDestroy(ev);
@@ -326,6 +333,8 @@ executor::~executor() {
 		cudaDeviceSynchronize();
 		if(G.service) cudaStreamDestroy(G.service);
 		if(G.timing) cudaStreamDestroy(G.timing);
+		if(G.h2d) cudaStreamDestroy(G.h2d);
+		if(G.d2h) cudaStreamDestroy(G.d2h);
 		for(auto m : G.marks)
 			if(m) cudaEventDestroy(m);
 		if(G.pool) cudaMemPoolDestroy(G.pool);
@@ -367,6 +376,8 @@ void executor::wait_deps(const task& t, cudaStream_t s) {
 		if(it == done_.end() || it->second.stream == s) continue;
 		check_cuda(cudaStreamWaitEvent(s, it->second.ev, 0), "cudaStreamWaitEvent");
 	}
+	for(auto ev : stage_waits_) check_cuda(cudaStreamWaitEvent(s, ev, 0), "cudaStreamWaitEvent");
+	stage_waits_.clear();
 }
 
 cudaStream_t executor::pick_compute(const task& t, ldev& L) {
@@ -414,14 +425,346 @@ void executor::submit(const std::vector<task>& tasks) {
 		if(t.id <= last_id_) throw validation_error("tasks must be submitted in ascending id order");
 		last_id_ = t.id;
 		if(cfg_.local_workers >= 0 && (t.worker < cfg_.first_worker || t.worker >= cfg_.first_worker + cfg_.local_workers)) continue;
-		switch(t.kind) {
-		case task_kind::create: run_create(t); break;
-		case task_kind::del: run_delete(t); break;
-		case task_kind::execute: run_execute(t); break;
-		case task_kind::copy: run_copy(t); break;
-		case task_kind::send: run_send(t); break;
-		case task_kind::recv: run_recv(t); break;
-		case task_kind::reduce: run_reduce(t); break;
+		if(spill_)
+			queue_.push_back(t);
+		else
+			issue(t);
+	}
+	if(spill_) drain(false);
+}
+
+void executor::drain(bool all) {
+	while(!queue_.empty() && (all || static_cast<int>(queue_.size()) > cfg_.lookahead)) {
+		task t = std::move(queue_.front());
+		queue_.pop_front();
+		issue(t);
+	}
+}
+
+void executor::issue(const task& t) {
+	if(spill_) stage(t);
+	switch(t.kind) {
+	case task_kind::create: run_create(t); break;
+	case task_kind::del: run_delete(t); break;
+	case task_kind::execute: run_execute(t); break;
+	case task_kind::copy: run_copy(t); break;
+	case task_kind::send: run_send(t); break;
+	case task_kind::recv: run_recv(t); break;
+	case task_kind::reduce: run_reduce(t); break;
+	}
+	if(spill_) note_use(t);
+}
+
+// ---- spill tier -------------------------------------------------------------------------------
+//
+// The reference stages every task through an LRU memory manager with unconditional write-back
+// (memory.cpp:161-186, 245-377), which on a cyclic stencil sweep evicts exactly the chunk the
+// next iteration needs first and moves 2.0-2.4x the minimum bytes. Here every
+// decision is taken when a task is issued, with `lookahead` later tasks already known:
+//   * victims are resident chunks the current task does not use, furthest next use first
+//     (Belady/MIN over the lookahead window), clean ones (valid host copy) before dirty ones,
+//     least recently used last;
+//   * eviction = D2H on the GPU's d2h stream after every task that touched the chunk (only when
+//     the host copy is stale: dirty tracking) + cudaFreeAsync; restoration = allocation on the
+//     h2d stream after the latest eviction's free + H2D, and the using task waits on it;
+//   * all of it is stream-ordered, so H2D, D2H and kernels overlap (full-duplex PCIe).
+
+void executor::used_chunks(const task& t, std::vector<std::pair<int64_t, bool>>& out) const {
+	out.clear();
+	switch(t.kind) {
+	case task_kind::create: break;
+	case task_kind::del: out.emplace_back(t.chunk, true); break;
+	case task_kind::execute:
+		for(size_t i = 0; i < t.args.size(); ++i) {
+			if(t.args[i].kind != arg_kind::chunk) continue;
+			const bool w = t.kern && i < t.kern->params.size() && t.kern->params[i].writable;
+			out.emplace_back(t.args[i].chunk, w);
+		}
+		break;
+	case task_kind::copy:
+		out.emplace_back(t.src, false);
+		out.emplace_back(t.dst, true);
+		break;
+	case task_kind::send: out.emplace_back(t.chunk, false); break;
+	case task_kind::recv: out.emplace_back(t.chunk, true); break;
+	case task_kind::reduce:
+		for(const auto c : t.inputs) out.emplace_back(c, false);
+		out.emplace_back(t.output, true);
+		break;
+	}
+}
+
+void executor::accesses_of(const task& t, std::vector<access_t>& out) const {
+	out.clear();
+	const auto full = [&](int64_t c) {
+		const auto it = bufs_.find(c);
+		return it == bufs_.end() ? box() : it->second.region;
+	};
+	switch(t.kind) {
+	case task_kind::create: out.push_back({t.chunk, t.region, false, true, false}); break;
+	case task_kind::del: out.push_back({t.chunk, full(t.chunk), false, false, true}); break;
+	case task_kind::execute:
+		for(size_t i = 0; i < t.args.size(); ++i) {
+			const auto& a = t.args[i];
+			if(a.kind != arg_kind::chunk) continue;
+			const box whole = full(a.chunk);
+			const bool known = a.access != 0 && whole.rank() == a.region.rank();
+			const box r = known ? intersect(a.region, whole) : whole;
+			const bool dense = t.kern && t.kern->dense_writes;
+			const bool overwrite = known && (a.access & 2) && !(a.access & 1) && dense;
+			out.push_back({a.chunk, r, !overwrite, overwrite, false});
+		}
+		break;
+	case task_kind::copy:
+		out.push_back({t.src, t.src_region, true, false, false});
+		out.push_back({t.dst, t.dst_region, false, true, false});
+		break;
+	case task_kind::send: out.push_back({t.chunk, t.region, true, false, false}); break;
+	case task_kind::recv: out.push_back({t.chunk, t.region, false, true, false}); break;
+	case task_kind::reduce:
+		for(const auto c : t.inputs) out.push_back({c, full(c), true, false, false});
+		out.push_back({t.output, full(t.output), false, true, false});
+		break;
+	}
+}
+
+bool executor::dead_ahead(int64_t chunk, const task* first) const {
+	const auto it = bufs_.find(chunk);
+	if(it == bufs_.end()) return false;
+	std::vector<box> live{it->second.region};
+	std::vector<access_t> accs;
+	const auto step = [&](const task& t) -> int {
+		accesses_of(t, accs);
+		for(const auto& a : accs)
+			if(a.chunk == chunk && a.kill) return 1;
+		for(const auto& a : accs) {
+			if(a.chunk != chunk || !a.read || a.region.is_empty()) continue;
+			for(const auto& l : live)
+				if(overlaps(l, a.region)) return -1;
+		}
+		for(const auto& a : accs) {
+			if(a.chunk != chunk || !a.overwrite || a.region.is_empty()) continue;
+			std::vector<box> next;
+			for(const auto& l : live) {
+				if(!overlaps(l, a.region)) {
+					next.push_back(l);
+					continue;
+				}
+				box rest = l; // l minus a.region, slab by slab
+				for(int k = 0; k < rest.rank(); ++k) {
+					if(rest.lo[k] < a.region.lo[k]) {
+						box piece = rest;
+						piece.hi[k] = a.region.lo[k];
+						next.push_back(piece);
+						rest.lo[k] = a.region.lo[k];
+					}
+					if(a.region.hi[k] < rest.hi[k]) {
+						box piece = rest;
+						piece.lo[k] = a.region.hi[k];
+						next.push_back(piece);
+						rest.hi[k] = a.region.hi[k];
+					}
+				}
+			}
+			live.swap(next);
+		}
+		return live.empty() ? 1 : 0;
+	};
+	if(first) {
+		const int r = step(*first);
+		if(r != 0) return r > 0;
+	}
+	for(const auto& t : queue_) {
+		const int r = step(t);
+		if(r != 0) return r > 0;
+	}
+	return false; // unknown beyond the window: keep the data
+}
+
+// An allocation under memory pressure reuses memory freed by an eviction kFreeLag evictions
+// back rather than the one just issued, so the H2D of a restore overlaps the D2H of the
+// eviction that made room for it (full-duplex PCIe); the device keeps kFreeLag chunks of
+// physical headroom above the logical capacity.
+constexpr size_t kFreeLag = 2;
+
+cudaEvent_t executor::alloc_event(int gpu) const {
+	const auto& G = gpus_[static_cast<size_t>(gpu)];
+	if(G.frees.size() <= kFreeLag) return nullptr;
+	return G.frees[G.frees.size() - 1 - kFreeLag];
+}
+
+void executor::alloc_wait(int gpu, cudaStream_t s) {
+	if(cudaEvent_t e = alloc_event(gpu)) check_cuda(cudaStreamWaitEvent(s, e, 0), "cudaStreamWaitEvent");
+}
+
+void* executor::host_alloc(uint64_t bytes, int gpu) {
+	auto it = host_free_.find(bytes);
+	if(it != host_free_.end()) {
+		auto [p, ev] = it->second;
+		host_free_.erase(it);
+		// the block's previous owner may still be read by an in-flight H2D: D2H waits for it
+		if(ev) {
+			check_cuda(cudaStreamWaitEvent(gpus_[static_cast<size_t>(gpu)].d2h, ev, 0), "cudaStreamWaitEvent");
+			cudaEventDestroy(ev);
+		}
+		return p;
+	}
+	if(host_used_ + bytes > cfg_.host_capacity)
+		throw execution_error("host tier exhausted: " + std::to_string(host_used_ + bytes) + " bytes needed, capacity " + std::to_string(cfg_.host_capacity));
+	void* p = nullptr;
+	check_cuda(cudaHostAlloc(&p, bytes, cudaHostAllocPortable), "cudaHostAlloc");
+	host_used_ += bytes;
+	return p;
+}
+
+void executor::host_release(void* p, uint64_t bytes, cudaEvent_t after) { host_free_.emplace(bytes, std::make_pair(p, after)); }
+
+void executor::evict(int64_t chunk) {
+	buffer& b = buf(chunk);
+	auto& G = gpus_[static_cast<size_t>(b.gpu)];
+	check_cuda(cudaSetDevice(b.gpu), "cudaSetDevice");
+	for(const auto u : b.users) {
+		const auto it = done_.find(u);
+		if(it != done_.end()) check_cuda(cudaStreamWaitEvent(G.d2h, it->second.ev, 0), "cudaStreamWaitEvent");
+	}
+	if(b.restored) check_cuda(cudaStreamWaitEvent(G.d2h, b.restored, 0), "cudaStreamWaitEvent");
+	if(!b.host_valid && dead_ahead(chunk, nullptr)) {
+		++ctr_.dead_drops; // overwritten before it is read again: no write-back
+	} else if(!b.host_valid) {
+		if(!b.host) b.host = host_alloc(b.bytes, b.gpu);
+		check_cuda(cudaMemcpyAsync(b.host, b.ptr, b.bytes, cudaMemcpyDeviceToHost, G.d2h), "cudaMemcpyAsync D2H (evict)");
+		b.host_valid = true;
+		ctr_.bytes_device_to_host += b.bytes;
+	}
+	check_cuda(cudaFreeAsync(b.ptr, G.d2h), "cudaFreeAsync");
+	if(!b.evicted) check_cuda(cudaEventCreateWithFlags(&b.evicted, cudaEventDisableTiming), "cudaEventCreate");
+	check_cuda(cudaEventRecord(b.evicted, G.d2h), "cudaEventRecord");
+	cudaEvent_t fe = take_event(b.gpu);
+	check_cuda(cudaEventRecord(fe, G.d2h), "cudaEventRecord");
+	G.frees.push_back(fe);
+	while(G.frees.size() > 4 * kFreeLag) {
+		free_events_[static_cast<size_t>(b.gpu)].push_back(G.frees.front());
+		G.frees.pop_front();
+	}
+	b.ptr = nullptr;
+	b.users.clear();
+	G.used -= b.bytes;
+	++ctr_.evictions;
+}
+
+void executor::ensure_room(int gpu, uint64_t bytes, const std::vector<int64_t>& pinned) {
+	auto& G = gpus_[static_cast<size_t>(gpu)];
+	if(bytes > G.capacity)
+		throw execution_error("a chunk of " + std::to_string(bytes) + " bytes can never fit the device capacity " + std::to_string(G.capacity));
+	if(G.used + bytes <= G.capacity) return;
+	// next READ of every chunk within the lookahead window (queue_ holds the future tasks): a
+	// chunk that is only overwritten ahead does not need its data kept (Belady on reads)
+	std::unordered_map<int64_t, size_t> next;
+	std::vector<access_t> accs;
+	for(size_t i = 0; i < queue_.size(); ++i) {
+		accesses_of(queue_[i], accs);
+		for(const auto& a : accs)
+			if(a.read) next.emplace(a.chunk, i);
+	}
+	while(G.used + bytes > G.capacity) {
+		int64_t victim = -1;
+		size_t v_next = 0;
+		bool v_clean = false;
+		uint64_t v_last = 0;
+		for(auto& [id, b] : bufs_) {
+			if(b.gpu != gpu || !b.ptr || std::find(pinned.begin(), pinned.end(), id) != pinned.end()) continue;
+			// data that is overwritten before it is read again is worth nothing: never-needed,
+			// and free to drop (no write-back)
+			const bool dead = !b.host_valid && dead_ahead(id, nullptr);
+			const auto it = next.find(id);
+			const size_t nu = dead || it == next.end() ? SIZE_MAX : it->second;
+			const bool free_drop = dead || b.host_valid;
+			const bool better = victim < 0 || nu > v_next || (nu == v_next && free_drop && !v_clean)
+			                    || (nu == v_next && free_drop == v_clean && b.last_use < v_last);
+			if(better) {
+				victim = id;
+				v_next = nu;
+				v_clean = free_drop;
+				v_last = b.last_use;
+			}
+		}
+		if(victim < 0)
+			throw execution_error("device " + std::to_string(gpu) + ": task footprint exceeds capacity " + std::to_string(G.capacity)
+			                      + " with every resident chunk in use");
+		if(std::getenv("MTB_SPILL_TRACE"))
+			std::fprintf(stderr, "[spill] evict chunk %ld next_read %ld clean %d queue %zu used %lu cap %lu\n", static_cast<long>(victim),
+			    v_next == SIZE_MAX ? -1L : static_cast<long>(v_next), v_clean ? 1 : 0, queue_.size(), static_cast<unsigned long>(G.used),
+			    static_cast<unsigned long>(G.capacity));
+		evict(victim);
+	}
+}
+
+void executor::restore(int64_t chunk, const std::vector<int64_t>& pinned, const task& current) {
+	buffer& b = buf(chunk);
+	ensure_room(b.gpu, b.bytes, pinned);
+	auto& G = gpus_[static_cast<size_t>(b.gpu)];
+	check_cuda(cudaSetDevice(b.gpu), "cudaSetDevice");
+	alloc_wait(b.gpu, G.h2d);
+	check_cuda(cudaMallocFromPoolAsync(&b.ptr, b.bytes, G.pool, G.h2d), "cudaMallocFromPoolAsync (restore)");
+	const bool needed = b.host_valid && !dead_ahead(chunk, &current);
+	if(std::getenv("MTB_SPILL_TRACE"))
+		std::fprintf(stderr, "[spill] restore chunk %ld for task %ld (%s) copy %d\n", static_cast<long>(chunk), static_cast<long>(current.id),
+		    task_kind_name(current.kind), needed ? 1 : 0);
+	if(!needed) {
+		// contents are overwritten before they are read: allocate only
+		G.used += b.bytes;
+		ctr_.peak_device_bytes = std::max(ctr_.peak_device_bytes, G.used);
+		if(!b.restored) check_cuda(cudaEventCreateWithFlags(&b.restored, cudaEventDisableTiming), "cudaEventCreate");
+		check_cuda(cudaEventRecord(b.restored, G.h2d), "cudaEventRecord");
+		++ctr_.dead_skips;
+		return;
+	}
+	if(b.evicted) check_cuda(cudaStreamWaitEvent(G.h2d, b.evicted, 0), "cudaStreamWaitEvent"); // its own write-back first
+	check_cuda(cudaMemcpyAsync(b.ptr, b.host, b.bytes, cudaMemcpyHostToDevice, G.h2d), "cudaMemcpyAsync H2D (restore)");
+	if(!b.restored) check_cuda(cudaEventCreateWithFlags(&b.restored, cudaEventDisableTiming), "cudaEventCreate");
+	check_cuda(cudaEventRecord(b.restored, G.h2d), "cudaEventRecord");
+	G.used += b.bytes;
+	ctr_.peak_device_bytes = std::max(ctr_.peak_device_bytes, G.used);
+	ctr_.bytes_host_to_device += b.bytes;
+}
+
+void executor::stage(const task& t) {
+	std::vector<std::pair<int64_t, bool>> uses;
+	used_chunks(t, uses);
+	std::vector<int64_t> pinned;
+	for(const auto& [c, w] : uses) pinned.push_back(c);
+	for(const auto& [c, w] : uses) {
+		buffer& b = buf(c);
+		if(!b.ptr) restore(c, pinned, t);
+		if(b.restored) stage_waits_.push_back(b.restored);
+	}
+	if(t.kind == task_kind::create) {
+		const uint64_t bytes = static_cast<uint64_t>(t.region.volume()) * dtype_size(t.type);
+		ensure_room(gpu_of(t.home), bytes, pinned);
+		if(cudaEvent_t e = alloc_event(gpu_of(t.home))) stage_waits_.push_back(e);
+	}
+}
+
+void executor::note_use(const task& t) {
+	std::vector<std::pair<int64_t, bool>> uses;
+	used_chunks(t, uses);
+	if(t.kind == task_kind::create) uses.emplace_back(t.chunk, true);
+	++clock_;
+	for(const auto& [c, w] : uses) {
+		const auto it = bufs_.find(c);
+		if(it == bufs_.end()) continue; // deleted by this task
+		buffer& b = it->second;
+		b.users.push_back(t.id);
+		b.last_use = clock_;
+		if(w) b.host_valid = false;
+		if(b.users.size() > 64) {
+			std::vector<int64_t> keep;
+			for(const auto u : b.users) {
+				const auto d = done_.find(u);
+				if(d != done_.end() && cudaEventQuery(d->second.ev) != cudaSuccess) keep.push_back(u);
+			}
+			cudaGetLastError();
+			b.users.swap(keep);
 		}
 	}
 }
@@ -452,8 +795,19 @@ void executor::run_delete(const task& t) {
 	ldev& L = dev(b.home);
 	cudaStream_t s = pick_compute(t, L);
 	wait_deps(t, s);
-	check_cuda(cudaFreeAsync(b.ptr, s), "cudaFreeAsync");
-	gpus_[static_cast<size_t>(b.gpu)].used -= b.bytes;
+	if(b.ptr) {
+		check_cuda(cudaFreeAsync(b.ptr, s), "cudaFreeAsync");
+		gpus_[static_cast<size_t>(b.gpu)].used -= b.bytes;
+	}
+	if(b.host) {
+		// the pinned block is reusable once every earlier use of the chunk is done
+		cudaEvent_t after = nullptr;
+		check_cuda(cudaEventCreateWithFlags(&after, cudaEventDisableTiming), "cudaEventCreate");
+		check_cuda(cudaEventRecord(after, s), "cudaEventRecord");
+		host_release(b.host, b.bytes, after);
+	}
+	if(b.restored) cudaEventDestroy(b.restored);
+	if(b.evicted) cudaEventDestroy(b.evicted);
 	bufs_.erase(t.chunk);
 	finish(t, s);
 }
@@ -602,12 +956,20 @@ void executor::run_reduce(const task& t) {
 
 void executor::mark(int slot) {
 	if(slot < 0 || slot > 1) throw validation_error("mark slot must be 0 or 1");
+	drain(true);
 	for(auto& G : gpus_) {
 		check_cuda(cudaSetDevice(G.ordinal), "cudaSetDevice");
 		for(const auto& [s, tail] : tail_) {
 			const auto it = done_.find(tail);
 			if(it == done_.end() || it->second.gpu != G.ordinal) continue;
 			check_cuda(cudaStreamWaitEvent(G.timing, it->second.ev, 0), "cudaStreamWaitEvent");
+		}
+		// spill-tier transfers are not tasks: join their streams explicitly
+		for(cudaStream_t s : {G.h2d, G.d2h}) {
+			cudaEvent_t e = take_event(G.ordinal);
+			check_cuda(cudaEventRecord(e, s), "cudaEventRecord");
+			check_cuda(cudaStreamWaitEvent(G.timing, e, 0), "cudaStreamWaitEvent");
+			free_events_[static_cast<size_t>(G.ordinal)].push_back(e);
 		}
 		check_cuda(cudaEventRecord(G.marks[slot], G.timing), "cudaEventRecord");
 	}
@@ -642,6 +1004,7 @@ void executor::kernel_time(const std::string& kernel, int64_t* count, double* to
 }
 
 void executor::sync() {
+	drain(true);
 	std::string err;
 	for(auto& G : gpus_) {
 		cudaSetDevice(G.ordinal);
@@ -656,25 +1019,34 @@ void executor::sync() {
 }
 
 void executor::download(int64_t chunk, void* host, const box& host_box, const box& region) {
+	drain(true);
 	const buffer& b = buf(chunk);
 	if(!encloses(b.region, region) || !encloses(host_box, region)) throw validation_error("download region outside the chunk or the host box");
 	check_cuda(cudaSetDevice(b.gpu), "cudaSetDevice");
 	cudaStream_t s = gpus_[static_cast<size_t>(b.gpu)].service;
 	check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
-	copy_box(b.ptr, b.region, b.gpu, host, host_box, -1, region, dtype_size(b.type), s);
+	if(b.ptr)
+		copy_box(b.ptr, b.region, b.gpu, host, host_box, -1, region, dtype_size(b.type), s);
+	else
+		copy_box(b.host, b.region, -1, host, host_box, -1, region, dtype_size(b.type), s); // evicted: host copy is current
 	check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-	ctr_.bytes_device_to_host += static_cast<uint64_t>(region.volume()) * dtype_size(b.type);
 }
 
 void executor::upload(int64_t chunk, const void* host, const box& host_box) {
-	const buffer& b = buf(chunk);
+	drain(true);
+	buffer& b = buf(chunk);
 	if(!encloses(host_box, b.region)) throw validation_error("upload: chunk outside the host box");
 	check_cuda(cudaSetDevice(b.gpu), "cudaSetDevice");
 	cudaStream_t s = gpus_[static_cast<size_t>(b.gpu)].service;
 	check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
-	copy_box(host, host_box, -1, b.ptr, b.region, b.gpu, b.region, dtype_size(b.type), s);
+	if(b.ptr) {
+		copy_box(host, host_box, -1, b.ptr, b.region, b.gpu, b.region, dtype_size(b.type), s);
+		b.host_valid = false;
+	} else {
+		copy_box(host, host_box, -1, b.host, b.region, -1, b.region, dtype_size(b.type), s);
+		b.host_valid = true;
+	}
 	check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-	ctr_.bytes_host_to_device += b.bytes;
 }
 
 std::string executor::report_json() const {

@@ -19,6 +19,7 @@
 
 #include <cuda_runtime.h>
 
+#include <deque>
 #include <map>
 #include <string>
 #include <tuple>
@@ -36,6 +37,8 @@ struct executor_config {
 	int num_gpus = 0;            // 0: all visible
 	int streams_per_device = 4;
 	uint64_t device_capacity = 0; // 0: 90% of free memory at start
+	uint64_t host_capacity = 0;   // pinned-host spill tier; 0 disables spilling
+	int lookahead = 512;          // spill tier: tasks held back so eviction can see future uses
 	int first_worker = 0;         // workers [first, first+local) execute here (multi-process)
 	int local_workers = -1;       // -1: all workers
 };
@@ -51,6 +54,8 @@ struct exec_counters {
 	uint64_t evictions = 0;
 	uint64_t bytes_device_to_host = 0;
 	uint64_t bytes_host_to_device = 0;
+	uint64_t dead_drops = 0; // evictions that skipped the write-back (data dead ahead)
+	uint64_t dead_skips = 0; // restores that skipped the H2D (data overwritten before read)
 };
 
 class executor {
@@ -86,12 +91,19 @@ class executor {
 
   private:
 	struct buffer {
-		void* ptr = nullptr;
+		void* ptr = nullptr; // device copy (null while evicted)
 		uint64_t bytes = 0;
 		box region;
 		dtype type = dtype::f32;
 		device_id home;
 		int gpu = 0;
+		// spill tier
+		void* host = nullptr;     // pinned host copy
+		bool host_valid = false;  // host copy equals the device contents
+		std::vector<int64_t> users; // tasks that touched the device copy since it became resident
+		cudaEvent_t restored = nullptr; // completes when the last H2D restore has landed
+		cudaEvent_t evicted = nullptr;  // completes when the last eviction's D2H has landed
+		uint64_t last_use = 0;
 	};
 	struct ldev {
 		int gpu = 0;
@@ -106,6 +118,8 @@ class executor {
 		uint64_t capacity = 0;
 		cudaStream_t service = nullptr; // message-buffer releases
 		cudaStream_t timing = nullptr;
+		cudaStream_t h2d = nullptr, d2h = nullptr; // spill tier
+		std::deque<cudaEvent_t> frees;             // one event per eviction (after its D2H + free), oldest first
 		cudaEvent_t marks[2] = {nullptr, nullptr};
 	};
 	struct kernel_timing {
@@ -146,6 +160,37 @@ class executor {
 	void finish(const task& t, cudaStream_t s);
 	void retire_completed();
 	buffer& buf(int64_t chunk);
+
+	// spill tier (active when cfg.host_capacity > 0)
+	bool spill_ = false;
+	std::deque<task> queue_;
+	std::vector<cudaEvent_t> stage_waits_;
+	std::multimap<uint64_t, std::pair<void*, cudaEvent_t>> host_free_; // size -> (block, reusable-after event)
+	uint64_t host_used_ = 0;
+	uint64_t clock_ = 0;
+	void issue(const task& t);
+	void drain(bool all);
+	void used_chunks(const task& t, std::vector<std::pair<int64_t, bool>>& out) const;
+	struct access_t {
+		int64_t chunk;
+		box region;
+		bool read;      // may read `region` (anything not a definite overwrite counts)
+		bool overwrite; // definitely writes every cell of `region`
+		bool kill;      // delete
+	};
+	void accesses_of(const task& t, std::vector<access_t>& out) const;
+	// true when, in `first` (optional) followed by the queued tasks, every cell of the chunk
+	// is overwritten (or the chunk deleted) before any of it is read
+	bool dead_ahead(int64_t chunk, const task* first) const;
+	void stage(const task& t);
+	void note_use(const task& t);
+	void ensure_room(int gpu, uint64_t bytes, const std::vector<int64_t>& pinned);
+	void evict(int64_t chunk);
+	void restore(int64_t chunk, const std::vector<int64_t>& pinned, const task& current);
+	void* host_alloc(uint64_t bytes, int gpu);
+	void host_release(void* p, uint64_t bytes, cudaEvent_t after);
+	void alloc_wait(int gpu, cudaStream_t s);
+	cudaEvent_t alloc_event(int gpu) const;
 
 	void run_create(const task& t);
 	void run_delete(const task& t);

@@ -22,6 +22,10 @@ struct arg_bind {
 	int64_t i = 0;
 	double f = 0.0;
 	int64_t chunk = -1;
+	// access of a chunk argument as the planner inferred it (executor data-liveness analysis;
+	// unknown for plans that arrive through mt_exec_submit)
+	box region;
+	int8_t access = 0; // bit 0: reads, bit 1: writes; 0 = unknown
 };
 
 // One task; the fields a kind does not use stay default. See include/manta_b200.h mt_task.

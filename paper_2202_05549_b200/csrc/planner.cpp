@@ -363,6 +363,8 @@ std::pair<int64_t, int64_t> planner::launch(const std::string& kernel, const box
 				exec_deps.push_back(create);
 				binds[i].kind = arg_kind::chunk;
 				binds[i].chunk = part;
+				binds[i].region = b;
+				binds[i].access = 3;
 				sb_partials.emplace_back(bp.access_index, part);
 				continue;
 			}
@@ -374,6 +376,8 @@ std::pair<int64_t, int64_t> planner::launch(const std::string& kernel, const box
 				const int64_t cid = h.chunks[static_cast<size_t>(enc)].id;
 				binds[i].kind = arg_kind::chunk;
 				binds[i].chunk = cid;
+				binds[i].region = region;
+				binds[i].access = static_cast<int8_t>((mode.reads() ? 1 : 0) | (mode.writes() ? 2 : 0));
 				recs.push_back({cid, mode.writes(), mode.reads(), region});
 				if(mode.writes()) writes.push_back({bp.access_index, region, cid, false});
 				continue;
@@ -397,6 +401,8 @@ std::pair<int64_t, int64_t> planner::launch(const std::string& kernel, const box
 			}
 			binds[i].kind = arg_kind::chunk;
 			binds[i].chunk = temp;
+			binds[i].region = region;
+			binds[i].access = static_cast<int8_t>((mode.reads() ? 1 : 0) | (mode.writes() ? 2 : 0));
 			if(mode.writes())
 				writes.push_back({bp.access_index, region, temp, true});
 			else

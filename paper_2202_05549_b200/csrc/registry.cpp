@@ -39,6 +39,13 @@ const kernel_entry& kernel_table::at(int index) const {
 	return *entries_[static_cast<size_t>(index)];
 }
 
+void kernel_table::set_dense_writes(const std::string& id) {
+	std::lock_guard<std::mutex> lock(mu_);
+	const auto it = by_name_.find(id);
+	if(it == by_name_.end()) throw validation_error("unknown kernel \"" + id + "\"");
+	entries_[static_cast<size_t>(it->second)]->dense_writes = true;
+}
+
 int kernel_table::size() const {
 	std::lock_guard<std::mutex> lock(mu_);
 	return static_cast<int>(entries_.size());

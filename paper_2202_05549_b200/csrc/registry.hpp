@@ -26,6 +26,9 @@ struct kernel_entry {
 	std::vector<param_sig> params;
 	mt_launcher_fn launcher = nullptr;
 	const void* user = nullptr; // passed to the launcher as mt_launch_ctx::user
+	// every cell of a declared `write` region (inside the array domain) is written by the
+	// kernel; lets the spill tier skip restoring data that is about to be overwritten
+	bool dense_writes = false;
 };
 
 class kernel_table {
@@ -36,6 +39,7 @@ class kernel_table {
 	int find(const std::string& id) const; // -1 when absent
 	const kernel_entry& at(int index) const;
 	int size() const;
+	void set_dense_writes(const std::string& id); // see kernel_entry::dense_writes
 
   private:
 	kernel_table();
