@@ -137,6 +137,168 @@ __global__ void kmeans_update_i32_kernel(range r, int64_t k, int64_t d, dview po
 		if(acc[k * d + c]) atomicAdd(reinterpret_cast<unsigned long long*>(at1<int64_t>(counts, c)), acc[k * d + c]);
 }
 
+// Up to ~110K bins: two u16 counters per u32 shared word (65536 bins = 128 KB). A half that
+// wraps past 0xFFFF is detected from the atomic's old value and its 65536 moved to the global
+// partial (for the low half the carry that leaked into the high half is taken back).
+constexpr int kHistPairMaxBins = 110000;
+
+__global__ void histogram_pair_kernel(const int32_t* x, int64_t n_local, int64_t bins, unsigned long long* hist) {
+	extern __shared__ uint32_t w[];
+	const int64_t words = (bins + 1) / 2;
+	for(int64_t b = threadIdx.x; b < words; b += blockDim.x) w[b] = 0;
+	__syncthreads();
+	const auto add = [&](int32_t v) {
+		if(static_cast<uint64_t>(v) >= static_cast<uint64_t>(bins)) return;
+		const uint32_t sh = (v & 1) * 16;
+		const uint32_t old = atomicAdd(&w[v >> 1], 1u << sh);
+		if(((old >> sh) & 0xFFFFu) == 0xFFFFu) {
+			if(sh == 0) atomicSub(&w[v >> 1], 1u << 16);
+			atomicAdd(hist + v, 65536ull);
+		}
+	};
+	const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+	const int64_t nvec = n_local / 4;
+	const int4* xv = reinterpret_cast<const int4*>(x);
+	for(int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nvec; t += stride) {
+		const int4 v = __ldcs(xv + t);
+		add(v.x);
+		add(v.y);
+		add(v.z);
+		add(v.w);
+	}
+	for(int64_t t = nvec * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n_local; t += stride) add(x[t]);
+	__syncthreads();
+	for(int64_t b = threadIdx.x; b < words; b += blockDim.x) {
+		const uint32_t v = w[b];
+		if(v & 0xFFFFu) atomicAdd(hist + 2 * b, static_cast<unsigned long long>(v & 0xFFFFu));
+		if((v >> 16) && 2 * b + 1 < bins) atomicAdd(hist + 2 * b + 1, static_cast<unsigned long long>(v >> 16));
+	}
+}
+
+// k-means assignment, fast path: when every |coordinate| < 8192 (checked on the fly: the
+// block checks its centroid table, each thread its points) a squared distance over d <= 16
+// dimensions fits in u32 exactly, so the int64 reference arithmetic becomes one IADD + one
+// IMAD per (point, centroid, dimension). Two points per thread share every centroid load
+// (broadcast LDS.128 from shared memory). Points outside the range take the int64 path.
+constexpr int kKmPts = 2;
+
+__global__ void __launch_bounds__(256) kmeans_assign_fast_kernel(const int32_t* __restrict__ points, int64_t pld, int64_t n_local, int k, int d,
+    const int32_t* __restrict__ cents, int64_t cld, int32_t* __restrict__ assign) {
+	extern __shared__ int4 cs4[]; // k rows of 16 i32 (padded to 16 columns)
+	int32_t* cs = reinterpret_cast<int32_t*>(cs4);
+	int big = 0;
+	for(int e = threadIdx.x; e < k * 16; e += blockDim.x) {
+		const int c = e / 16, q = e % 16;
+		const int32_t v = q < d ? cents[static_cast<int64_t>(c) * cld + q] : 0;
+		cs[e] = v;
+		big |= (v >= 8192 || v <= -8192);
+	}
+	const int cent_big = __syncthreads_or(big);
+	const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * kKmPts;
+	for(int64_t base = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kKmPts; base < n_local; base += stride) {
+		int32_t p[kKmPts][16];
+		bool ok = !cent_big;
+#pragma unroll
+		for(int j = 0; j < kKmPts; ++j) {
+			const int64_t i = base + j;
+#pragma unroll
+			for(int q = 0; q < 16; ++q) {
+				const int32_t v = (i < n_local && q < d) ? points[i * pld + q] : 0;
+				p[j][q] = v;
+				ok &= (v < 8192 && v > -8192);
+			}
+		}
+		uint32_t best[kKmPts];
+		int bi[kKmPts];
+#pragma unroll
+		for(int j = 0; j < kKmPts; ++j) {
+			best[j] = 0xFFFFFFFFu;
+			bi[j] = 0;
+		}
+		if(ok) {
+			for(int c = 0; c < k; ++c) {
+				const int4* crow = cs4 + c * 4;
+				int32_t cv[16];
+#pragma unroll
+				for(int v4 = 0; v4 < 4; ++v4) {
+					const int4 t = crow[v4];
+					cv[4 * v4] = t.x;
+					cv[4 * v4 + 1] = t.y;
+					cv[4 * v4 + 2] = t.z;
+					cv[4 * v4 + 3] = t.w;
+				}
+#pragma unroll
+				for(int j = 0; j < kKmPts; ++j) {
+					uint32_t dist = 0;
+#pragma unroll
+					for(int q = 0; q < 16; ++q) {
+						const int32_t df = p[j][q] - cv[q];
+						dist += static_cast<uint32_t>(df * df);
+					}
+					if(dist < best[j]) {
+						best[j] = dist;
+						bi[j] = c;
+					}
+				}
+			}
+		} else {
+			// exact int64 path (reference arithmetic, kernels.cpp:283-292)
+#pragma unroll
+			for(int j = 0; j < kKmPts; ++j) {
+				int64_t b64 = INT64_MAX;
+				for(int c = 0; c < k; ++c) {
+					int64_t dist = 0;
+#pragma unroll
+					for(int q = 0; q < 16; ++q) {
+						const int64_t df = static_cast<int64_t>(p[j][q]) - cs[c * 16 + q]; // padded columns are 0 - 0
+						dist += df * df;
+					}
+					if(dist < b64) {
+						b64 = dist;
+						bi[j] = c;
+					}
+				}
+			}
+		}
+#pragma unroll
+		for(int j = 0; j < kKmPts; ++j)
+			if(base + j < n_local) assign[base + j] = bi[j];
+	}
+}
+
+// k-means update: per-CTA shared sums as (lo, hi) u32 pairs — one u32 atomic per value plus a
+// second only on carry or for negative values, i.e. an exact wrapping int64 sum — and u32
+// counts; flushed once per CTA with 64-bit global atomics.
+__global__ void kmeans_update_fast_kernel(const int32_t* __restrict__ points, int64_t pld, const int32_t* __restrict__ assign, int64_t n_local, int k,
+    int d, unsigned long long* sums, int64_t sld, unsigned long long* counts) {
+	extern __shared__ uint32_t sm[];
+	uint32_t* lo = sm;
+	uint32_t* hi = sm + k * d;
+	uint32_t* cnt = sm + 2 * k * d;
+	for(int e = threadIdx.x; e < 2 * k * d + k; e += blockDim.x) sm[e] = 0;
+	__syncthreads();
+	for(int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_local; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+		const int c = assign[i];
+		if(c < 0 || c >= k) continue; // outside the partial: the reference would fault; skip
+		for(int q = 0; q < d; ++q) {
+			const int32_t v = points[i * pld + q];
+			const uint32_t u = static_cast<uint32_t>(v);
+			const uint32_t old = atomicAdd(&lo[c * d + q], u);
+			const uint32_t carry = (old + u < old) ? 1u : 0u;
+			const uint32_t h = (v < 0 ? 0xFFFFFFFFu : 0u) + carry;
+			if(h) atomicAdd(&hi[c * d + q], h);
+		}
+		atomicAdd(&cnt[c], 1u);
+	}
+	__syncthreads();
+	for(int e = threadIdx.x; e < k * d; e += blockDim.x) {
+		const unsigned long long v = (static_cast<unsigned long long>(hi[e]) << 32) | lo[e];
+		if(v) atomicAdd(sums + static_cast<int64_t>(e / d) * sld + e % d, v);
+	}
+	for(int c = threadIdx.x; c < k; c += blockDim.x)
+		if(cnt[c]) atomicAdd(counts + c, static_cast<unsigned long long>(cnt[c]));
+}
+
 } // namespace kern
 
 int launch_histogram(const mt_launch_ctx* c, void* stream) {
@@ -159,6 +321,12 @@ int launch_histogram(const mt_launch_ctx* c, void* stream) {
 		int64_t blocks = (n_local / 4 + 511) / 512;
 		blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
 		histogram_smem_kernel<<<static_cast<unsigned>(blocks), 512, smem, s>>>(x, lo, n_local, bins, hist);
+	} else if(bins <= kHistPairMaxBins && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
+		const size_t smem = static_cast<size_t>((bins + 1) / 2) * sizeof(uint32_t);
+		ensure_smem(histogram_pair_kernel, static_cast<int>(((kHistPairMaxBins + 1) / 2) * 4));
+		int64_t blocks = (n_local / 4 + 1023) / 1024;
+		blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148));
+		histogram_pair_kernel<<<static_cast<unsigned>(blocks), 1024, smem, s>>>(x, n_local, bins, hist);
 	} else {
 		histogram_global_kernel<<<grid_1d(n_local, 256), 256, 0, s>>>(x, n_local, bins, hist);
 	}
@@ -172,6 +340,21 @@ int launch_kmeans_assign_i32(const mt_launch_ctx* c, void* stream) {
 	if(r.total <= 0) return 0;
 	const int64_t k = c->scalars_int[1], d = c->scalars_int[2];
 	const auto s = static_cast<cudaStream_t>(stream);
+	const mt_view& va = c->views[3];
+	const mt_view& vp = c->views[4];
+	const mt_view& vc = c->views[5];
+	const size_t fast_smem = static_cast<size_t>(k) * 16 * sizeof(int32_t);
+	const bool fast = d >= 1 && d <= 16 && fast_smem <= 200 * 1024 && vp.stride[1] == 1 && vc.stride[1] == 1 && va.stride[0] == 1 && vc.offset[0] == 0
+	                  && vc.offset[1] == 0 && vp.offset[1] == 0 && vc.extent[0] >= k;
+	if(fast) {
+		ensure_smem(kmeans_assign_fast_kernel, 200 * 1024);
+		const int32_t* pts = static_cast<const int32_t*>(vp.base) + (r.lo[0] - vp.offset[0]) * vp.stride[0];
+		int32_t* asg = static_cast<int32_t*>(va.base) + (r.lo[0] - va.offset[0]);
+		const unsigned blocks = std::max<unsigned>(1, std::min<unsigned>(static_cast<unsigned>((r.total + 511) / 512), 148 * 8));
+		kmeans_assign_fast_kernel<<<blocks, 256, fast_smem, s>>>(pts, vp.stride[0], r.total, static_cast<int>(k), static_cast<int>(d),
+		    static_cast<const int32_t*>(vc.base), vc.stride[0], asg);
+		return cudaGetLastError() == cudaSuccess ? 0 : 1;
+	}
 	const size_t smem = static_cast<size_t>(k * d) * sizeof(int32_t);
 	if(smem <= static_cast<size_t>(kKmMaxSmem) && d <= 16) {
 		kmeans_assign_i32_kernel<<<grid_1d(r.total, 256), 256, smem, s>>>(r, k, d, make_view(c->views[3]), make_view(c->views[4]), make_view(c->views[5]));
@@ -189,6 +372,22 @@ int launch_kmeans_update_i32(const mt_launch_ctx* c, void* stream) {
 	const int64_t d = c->scalars_int[1];
 	const mt_view& vs = c->views[4];
 	const int64_t k = vs.extent[0];
+	{
+		const mt_view& vp = c->views[2];
+		const mt_view& va = c->views[3];
+		const mt_view& vn = c->views[5];
+		const size_t smem = static_cast<size_t>(2 * k * d + k) * 4;
+		if(vs.offset[0] == 0 && vs.offset[1] == 0 && vs.extent[1] == d && vn.offset[0] == 0 && vn.extent[0] == k && smem <= 200 * 1024
+		    && vp.stride[1] == 1 && vp.offset[1] == 0 && va.stride[0] == 1) {
+			ensure_smem(kmeans_update_fast_kernel, 200 * 1024);
+			const int32_t* pts = static_cast<const int32_t*>(vp.base) + (r.lo[0] - vp.offset[0]) * vp.stride[0];
+			const int32_t* asg = static_cast<const int32_t*>(va.base) + (r.lo[0] - va.offset[0]);
+			const unsigned blocks = std::max<unsigned>(1, std::min<unsigned>(static_cast<unsigned>((r.total + 255) / 256), 148 * 4));
+			kmeans_update_fast_kernel<<<blocks, 512, smem, static_cast<cudaStream_t>(stream)>>>(pts, vp.stride[0], asg, r.total, static_cast<int>(k),
+			    static_cast<int>(d), static_cast<unsigned long long*>(vs.base), vs.stride[0], static_cast<unsigned long long*>(vn.base));
+			return cudaGetLastError() == cudaSuccess ? 0 : 1;
+		}
+	}
 	// shared-memory privatisation only when the partial starts at centroid 0 (whole table)
 	const bool smem_ok = vs.offset[0] == 0 && vs.offset[1] == 0 && vs.extent[1] == d && static_cast<size_t>(k * d + k) * 8 <= 96 * 1024;
 	const size_t smem = smem_ok ? static_cast<size_t>(k * d + k) * 8 : 0;

@@ -1,0 +1,83 @@
+"""C4 kernels at sizes beyond the golden vectors: histogram paths (shared u32, packed u16 pairs,
+global), k-means fast/exact paths, all bit-exact against the C oracle."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2202_05549_b200 as mb
+from paper_2202_05549_b200 import Arr
+
+pytestmark = pytest.mark.gpu
+I32 = C.POINTER(C.c_int32)
+I64 = C.POINTER(C.c_int64)
+
+
+@pytest.mark.parametrize("bins", [7, 256, 16384, 65536, 100000, 300000])
+def test_histogram_paths(okern, bins):
+    n = 3_000_017
+    with mb.context(workers=1, devices=2, num_gpus=1) as ctx:
+        devs = ctx.devices
+        x = ctx.create_array([n], "i32", ctx.dist.row([n], 1_500_160, devs), 0)
+        h = ctx.create_array([bins], "i64", ctx.dist.replicated([bins], devs), 0)
+        w = ctx.dist.block_work([n], [128], [1_500_160], devs)
+        ctx.launch("hpattern1d", [n], [128], w, [n, bins, 99, Arr(x)], "global i => write out[i]")
+        ctx.launch("histogram", [n], [128], w, [n, bins, Arr(x), Arr(h)], "global i => read x[i], reduce(+) hist[:]")
+        got = ctx.read(h)
+    want = np.empty(bins, np.int64)
+    okern.oracle_histogram_hashed(C.c_int64(0), C.c_int64(n), C.c_int64(bins), C.c_int64(99), want.ctypes.data_as(I64))
+    assert np.array_equal(got, want)
+
+
+def test_histogram_u16_overflow():
+    """every element in one bin: the packed-u16 counters wrap many times"""
+    n, bins = 1 << 20, 65536
+    with mb.context(workers=1, devices=1, num_gpus=1) as ctx:
+        d = ctx.devices
+        x = ctx.create_array([n], "i32", ctx.dist.single([n], d[0]), 1)  # all ones -> bin 1
+        h = ctx.create_array([bins], "i64", ctx.dist.single([bins], d[0]), 0)
+        ctx.launch("histogram", [n], [128], ctx.dist.block_work([n], [128], [n], d), [n, bins, Arr(x), Arr(h)], "global i => read x[i], reduce(+) hist[:]")
+        got = ctx.read(h)
+    assert got[1] == n and got.sum() == n
+
+
+@pytest.mark.parametrize("mod", [1000, 20000])
+def test_kmeans_fast_and_exact_paths(okern, mod):
+    """mod 1000: all coordinates < 8192 (u32 fast path); mod 20000: int64 path."""
+    n, k, d = 50_000, 64, 16
+    with mb.context(workers=1, devices=2, num_gpus=1) as ctx:
+        devs = ctx.devices
+        pts = ctx.create_array([n, d], "i32", ctx.dist.row([n, d], 25_000, devs), 0)
+        asg = ctx.create_array([n], "i32", ctx.dist.row([n], 25_000, devs), 0)
+        cen = ctx.create_array([k, d], "i32", ctx.dist.replicated([k, d], devs), 0)
+        sums = ctx.create_array([k, d], "i64", ctx.dist.replicated([k, d], devs), 0)
+        cnts = ctx.create_array([k], "i64", ctx.dist.replicated([k], devs), 0)
+        ctx.launch("ipattern2d_i32", [n, d], [64, 16], ctx.dist.block_work([n, d], [64, 16], [25_024, d], devs), [n, d, mod, Arr(pts)],
+                   "global [i, j] => write out[i,j]")
+        wk = ctx.dist.block_work([k, d], [16, 16], [k, d], devs)
+        ctx.launch("ipattern2d_i32", [k, d], [16, 16], wk, [k, d, mod - 3, Arr(cen)], "global [i, j] => write out[i,j]")
+        w1 = ctx.dist.block_work([n], [64], [25_024], devs)
+        for _ in range(2):
+            ctx.launch("kmeans_assign_i32", [n], [64], w1, [n, k, d, Arr(asg), Arr(pts), Arr(cen)],
+                       "global i => write assign[i], read points[i,:], read centroids[:,:]")
+            ctx.launch("kmeans_update_i32", [n], [64], w1, [n, d, Arr(pts), Arr(asg), Arr(sums), Arr(cnts)],
+                       "global i => read points[i,:], read assign[i], reduce(+) sums[:,:], reduce(+) counts[:]")
+            ctx.launch("kmeans_finalize_i32", [k, d], [16, 16], wk, [k, d, Arr(cen), Arr(sums), Arr(cnts)],
+                       "global [i, j] => readwrite centroids[i,j], read sums[i,j], read counts[i]")
+        g_asg, g_cen, g_sums, g_cnts = ctx.read(asg), ctx.read(cen), ctx.read(sums), ctx.read(cnts)
+    p = np.empty((n, d), np.int32)
+    okern.oracle_ipattern2d_i32(C.c_int64(n), C.c_int64(d), C.c_int64(mod), p.ctypes.data_as(I32))
+    c = np.empty((k, d), np.int32)
+    okern.oracle_ipattern2d_i32(C.c_int64(k), C.c_int64(d), C.c_int64(mod - 3), c.ctypes.data_as(I32))
+    a = np.empty(n, np.int32)
+    s = np.empty((k, d), np.int64)
+    m = np.empty(k, np.int64)
+    for _ in range(2):
+        okern.oracle_kmeans_assign_i32(C.c_int64(n), C.c_int64(k), C.c_int64(d), p.ctypes.data_as(I32), c.ctypes.data_as(I32), a.ctypes.data_as(I32))
+        okern.oracle_kmeans_update_i32(C.c_int64(n), C.c_int64(k), C.c_int64(d), p.ctypes.data_as(I32), a.ctypes.data_as(I32), s.ctypes.data_as(I64),
+                                       m.ctypes.data_as(I64))
+        okern.oracle_kmeans_finalize_i32(C.c_int64(k), C.c_int64(d), s.ctypes.data_as(I64), m.ctypes.data_as(I64), c.ctypes.data_as(I32))
+    assert np.array_equal(g_asg, a)
+    assert np.array_equal(g_sums, s)
+    assert np.array_equal(g_cnts, m)
+    assert np.array_equal(g_cen, c)
