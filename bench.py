@@ -222,6 +222,145 @@ def run_contraction(ctx, n, steps, warmup):
             "max_rel_err_16_samples_vs_fp64": worst}
 
 
+def _timed(ctx, kernel, fn, steps):
+    fn()
+    ctx.synchronize()
+    ctx.profile_kernels(True)
+    k0, m0 = ctx.kernel_time(kernel)
+    ctx.mark(0)
+    for _ in range(steps):
+        fn()
+    ctx.mark(1)
+    ms = ctx.elapsed_ms()
+    ctx.synchronize()
+    ctx.profile_kernels(False)
+    k1, m1 = ctx.kernel_time(kernel)
+    return ms / steps, (m1 - m0) / max(1, k1 - k0)
+
+
+def run_c4(ctx, hist_n, km_n, steps, hbm, cpu):
+    """BASELINE config C4 on one GPU through the planner: histogram (reduce(+) into i64 bins)
+    and int32 k-means (d=16, k=256). Step times from device events (all streams joined)."""
+    from paper_2202_05549_b200 import Arr
+    dev = ctx.devices
+    out = {"histogram": [], "kmeans": None}
+    n = hist_n
+    for bins in (256, 65536):
+        x = ctx.create_array([n], "i32", ctx.dist.single([n], dev[0]), 0)
+        h = ctx.create_array([bins], "i64", ctx.dist.single([bins], dev[0]), 0)
+        w = ctx.dist.block_work([n], [256], [n], dev)
+        ctx.launch("hpattern1d", [n], [256], w, [n, bins, 12345, Arr(x)], "global i => write out[i]")
+
+        def step():
+            ctx.launch("histogram", [n], [256], w, [n, bins, Arr(x), Arr(h)], "global i => read x[i], reduce(+) hist[:]")
+            ctx.flush()
+
+        ms, _ = _timed(ctx, "histogram", step, steps)
+        ok = int(ctx.read(h).sum()) == n
+        gbs = 4.0 * n / (ms / 1e3) / 1e9
+        out["histogram"].append({"workload": f"histogram n={n} i32 -> {bins} i64 bins", "value": n / (ms / 1e3), "unit": "elements/s", "ms_per_step": ms,
+                                 "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                                              "note": "4 B/element; step time (plan + partial + reduce tree + copy-back) over device events"},
+                                 "total_count_check": ok})
+        ctx.delete_array(x)
+        ctx.delete_array(h)
+        ctx.synchronize()
+    n, k, d = km_n, 256, 16
+    pts = ctx.create_array([n, d], "i32", ctx.dist.single([n, d], dev[0]), 0)
+    asg = ctx.create_array([n], "i32", ctx.dist.single([n], dev[0]), 0)
+    cen = ctx.create_array([k, d], "i32", ctx.dist.single([k, d], dev[0]), 0)
+    sums = ctx.create_array([k, d], "i64", ctx.dist.single([k, d], dev[0]), 0)
+    cnts = ctx.create_array([k], "i64", ctx.dist.single([k], dev[0]), 0)
+    ctx.launch("ipattern2d_i32", [n, d], [256, 16], ctx.dist.block_work([n, d], [256, 16], [n, d], dev), [n, d, 1000, Arr(pts)],
+               "global [i, j] => write out[i,j]")
+    wk = ctx.dist.block_work([k, d], [16, 16], [k, d], dev)
+    ctx.launch("ipattern2d_i32", [k, d], [16, 16], wk, [k, d, 997, Arr(cen)], "global [i, j] => write out[i,j]")
+    w1 = ctx.dist.block_work([n], [256], [n], dev)
+
+    def assign():
+        ctx.launch("kmeans_assign_i32", [n], [256], w1, [n, k, d, Arr(asg), Arr(pts), Arr(cen)],
+                   "global i => write assign[i], read points[i,:], read centroids[:,:]")
+        ctx.flush()
+
+    def update():
+        ctx.launch("kmeans_update_i32", [n], [256], w1, [n, d, Arr(pts), Arr(asg), Arr(sums), Arr(cnts)],
+                   "global i => read points[i,:], read assign[i], reduce(+) sums[:,:], reduce(+) counts[:]")
+        ctx.flush()
+
+    a_ms, a_kms = _timed(ctx, "kmeans_assign_i32", assign, 2)
+    u_ms, u_kms = _timed(ctx, "kmeans_update_i32", update, steps)
+    ok = int(ctx.read(cnts).sum()) == n  # reduce(+) overwrites its destination each launch (planner.cpp:507-509)
+    for a in (pts, asg, cen, sums, cnts):
+        ctx.delete_array(a)
+    ctx.synchronize()
+    triples = float(n) * k * d
+    int_peak = 148 * 64 * 1.965e9  # (IADD3 alu + IMAD fma) pairs per clk per SM x SMs x max clock
+    ubytes = n * (d + 1) * 4
+    out["kmeans"] = {"workload": f"int32 k-means n={n} d={d} k={k}", "value": n / ((a_ms + u_ms) / 1e3), "unit": "points/s (assign + update)",
+                     "assign": {"ms": a_kms, "roofline": {"bound": "int32 alu", "achieved": triples / (a_kms / 1e3), "peak": int_peak,
+                                                           "unit": "(sub, mul-add) pairs/s", "frac": triples / (a_kms / 1e3) / int_peak,
+                                                           "peak_kind": "derived: 148 SM x 64 IADD+IMAD pairs/clk x 1.965 GHz"}},
+                     "update": {"ms": u_kms, "roofline": {"bound": "hbm", "achieved": ubytes / (u_kms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                                                           "frac": ubytes / (u_kms / 1e3) / 1e9 / hbm}},
+                     "count_check": ok}
+    if cpu:
+        import oracle
+        try:
+            out["cpu_baseline"] = cpu_c4(oracle)
+        except Exception as e:  # noqa: BLE001
+            out["cpu_baseline"] = {"unavailable": str(e)}
+    return out
+
+
+def cpu_c4(oracle):
+    """reference CPU executor (oracle/_ref) on bounded samples of the C4 workloads"""
+    from paper_2202_05549_b200 import Arr
+    threads = oracle.reference().host_threads()
+    dv = max(1, min(threads, 64))
+    res = {}
+    n, bins = 100_000_000, 256
+    ctx = oracle.reference_context(workers=1, devices=dv, execute=True)
+    devs = ctx.devices
+    per = (n + dv - 1) // dv
+    per = (per + 255) // 256 * 256
+    x = ctx.create_array([n], "i32", ctx.dist.row([n], per, devs), 0)
+    h = ctx.create_array([bins], "i64", ctx.dist.replicated([bins], devs), 0)
+    w = ctx.dist.block_work([n], [256], [per], devs)
+    ctx.launch("hpattern1d", [n], [256], w, [n, bins, 12345, Arr(x)], "global i => write out[i]")
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    ctx.launch("histogram", [n], [256], w, [n, bins, Arr(x), Arr(h)], "global i => read x[i], reduce(+) hist[:]")
+    ctx.synchronize()
+    dt = time.perf_counter() - t0
+    ctx.close()
+    res["histogram"] = {"value": n / dt, "unit": "elements/s", "cores": dv, "kind": "reference", "sample": f"n={n}, {bins} bins, {dt:.1f} s"}
+    n, k, d = 400_000, 256, 16
+    ctx = oracle.reference_context(workers=1, devices=dv, execute=True)
+    devs = ctx.devices
+    per = ((n + dv - 1) // dv + 255) // 256 * 256
+    pts = ctx.create_array([n, d], "i32", ctx.dist.row([n, d], per, devs), 0)
+    asg = ctx.create_array([n], "i32", ctx.dist.row([n], per, devs), 0)
+    cen = ctx.create_array([k, d], "i32", ctx.dist.replicated([k, d], devs), 0)
+    sums = ctx.create_array([k, d], "i64", ctx.dist.replicated([k, d], devs), 0)
+    cnts = ctx.create_array([k], "i64", ctx.dist.replicated([k], devs), 0)
+    ctx.launch("ipattern2d_i32", [n, d], [256, 16], ctx.dist.block_work([n, d], [256, 16], [per, d], devs), [n, d, 1000, Arr(pts)],
+               "global [i, j] => write out[i,j]")
+    ctx.launch("ipattern2d_i32", [k, d], [16, 16], ctx.dist.block_work([k, d], [16, 16], [k, d], devs), [k, d, 997, Arr(cen)],
+               "global [i, j] => write out[i,j]")
+    ctx.synchronize()
+    w1 = ctx.dist.block_work([n], [256], [per], devs)
+    t0 = time.perf_counter()
+    ctx.launch("kmeans_assign_i32", [n], [256], w1, [n, k, d, Arr(asg), Arr(pts), Arr(cen)],
+               "global i => write assign[i], read points[i,:], read centroids[:,:]")
+    ctx.launch("kmeans_update_i32", [n], [256], w1, [n, d, Arr(pts), Arr(asg), Arr(sums), Arr(cnts)],
+               "global i => read points[i,:], read assign[i], reduce(+) sums[:,:], reduce(+) counts[:]")
+    ctx.synchronize()
+    dt = time.perf_counter() - t0
+    ctx.close()
+    res["kmeans"] = {"value": n / dt, "unit": "points/s (assign + update)", "cores": dv, "kind": "reference", "sample": f"n={n}, k={k}, d={d}, {dt:.1f} s"}
+    return res
+
+
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -355,6 +494,14 @@ def run_b200(args):
         contraction["roofline"] = {"bound": "tensor", "achieved": kach, "peak": tpeak, "unit": "TFLOP/s", "frac": kach / tpeak,
                                    "peak_kind": "measured sustained (cuBLAS bf16, 4 s loop)", "frac_of_burst": kach / tburst,
                                    "kernel": "gemm_bf16_nt_kernel (tcgen05.mma cta_group::1 M128 N256, TMA, TMEM)"}
+    c4 = None
+    if args.c4:
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                hbm = float(json.load(f)["hbm_gbs"])
+        except Exception:
+            hbm = 6650.0
+        c4 = run_c4(ctx, args.hist_n, args.km_n, 5, hbm, rank == 0 and args.cpu_baseline)
     traffic = ncu_traffic("heat2d_ncu_summary.json", rows, cols)
     if rank == 0:
         out = {
@@ -372,6 +519,7 @@ def run_b200(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "contraction": contraction,
+            "reductions": c4,
         }
         print(json.dumps(out))
     ctx.close()
@@ -395,6 +543,9 @@ def main():
     p.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     p.add_argument("--matmul-n", type=int, default=32768, help="C3 contraction size (0 to skip)")
     p.add_argument("--matmul-steps", type=int, default=5)
+    p.add_argument("--no-c4", dest="c4", action="store_false", help="skip the histogram / k-means legs")
+    p.add_argument("--hist-n", type=int, default=4_000_000_000)
+    p.add_argument("--km-n", type=int, default=1_000_000_000)
     args = p.parse_args()
     if args.impl == "reference":
         if args.ref_rows == 512:
