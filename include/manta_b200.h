@@ -297,6 +297,10 @@ int mt_kernel_count(void);
 /* context-local kernel (shadows the global registry for this context's launches); the
  * launcher may be NULL for plan-only contexts */
 int mt_ctx_kernel_register(mt_ctx* ctx, const char* id, const mt_param_spec* params, int32_t nparams, mt_launcher_fn launcher, const void* user);
+/* context-local synthesized `gather` kernel for an annotation (scenario.cpp:276-389): one
+ * array parameter per access (element type + domain given in access order) and a device
+ * body that folds the thread's read regions into its write/reduce regions */
+int mt_ctx_gather_register(mt_ctx* ctx, const char* id, const char* annotation_text, int32_t naccess, const int32_t* dtypes, const mt_rect* domains);
 int mt_kernel_info(int32_t index, char* id, int32_t id_cap, mt_param_spec* params, int32_t cap, int32_t* nparams);
 
 #ifdef __cplusplus

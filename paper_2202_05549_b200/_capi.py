@@ -160,6 +160,7 @@ _SIGS = {
     "kernel_register": (C.c_int, [C.c_char_p, P(ParamSpec), C.c_int32, LAUNCHER]),
     "kernel_count": (C.c_int, []),
     "ctx_kernel_register": (C.c_int, [C.c_void_p, C.c_char_p, P(ParamSpec), C.c_int32, C.c_void_p, C.c_void_p]),
+    "ctx_gather_register": (C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int32, P(C.c_int32), P(Rect)]),
     "fuzz_scenario_json": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int64, P(C.c_int64)]),
     "scenario_plan": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(Task), C.c_int64, P(C.c_int64), P(C.c_int64),
                                 C.c_int64, P(C.c_int64), P(ArgBinding), C.c_int64, P(C.c_int64)]),
@@ -169,7 +170,7 @@ _SIGS = {
 }
 # entry points the oracle shim may lack
 _OPTIONAL = {"exec_stats", "exec_last_stream", "kernel_info", "host_threads", "ctx_kernel_register", "fuzz_scenario_json", "scenario_plan",
-             "scenario_run", "plan_accesses", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
+             "scenario_run", "plan_accesses", "ctx_gather_register", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
 
 
 class MantaError(RuntimeError):
@@ -201,7 +202,7 @@ class Lib:
     def __init__(self, path: str, prefix: str):
         self.path = path
         self.prefix = prefix
-        self.dll = C.CDLL(path, mode=C.RTLD_GLOBAL)
+        self.dll = C.CDLL(path)  # RTLD_LOCAL: product and oracle shim must never interpose
         for name, (res, args) in _SIGS.items():
             sym = prefix + name
             if not hasattr(self.dll, sym):

@@ -10,6 +10,11 @@
 
 using namespace mtb;
 
+namespace mtb {
+std::shared_ptr<void> make_gather_kernel(const std::string& annotation_text, const std::vector<dtype>& types, const std::vector<box>& domains,
+    kernel_entry& out);
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -214,6 +219,7 @@ struct mt_ctx {
 	std::unique_ptr<planner> plan;
 	std::unique_ptr<mt_exec> exec;
 	std::unordered_map<std::string, annotation> ann_cache;
+	std::vector<std::shared_ptr<void>> owned; // descriptors of context-local kernels
 };
 
 namespace {
@@ -535,6 +541,21 @@ kernel_entry make_entry(const char* id, const mt_param_spec* params, int32_t npa
 	return e;
 }
 } // namespace
+
+int mt_ctx_gather_register(mt_ctx* ctx, const char* id, const char* annotation_text, int32_t naccess, const int32_t* dtypes, const mt_rect* domains) {
+	return guarded([&] {
+		std::vector<dtype> types;
+		std::vector<box> doms;
+		for(int32_t i = 0; i < naccess; ++i) {
+			types.push_back(to_dtype(dtypes[i]));
+			doms.push_back(to_box(domains[i]));
+		}
+		kernel_entry e;
+		e.id = id;
+		ctx->owned.push_back(make_gather_kernel(annotation_text, types, doms, e));
+		ctx->plan->add_local_kernel(std::move(e));
+	});
+}
 
 int mt_ctx_kernel_register(mt_ctx* ctx, const char* id, const mt_param_spec* params, int32_t nparams, mt_launcher_fn launcher, const void* user) {
 	return guarded([&] { ctx->plan->add_local_kernel(make_entry(id, params, nparams, launcher, user)); });

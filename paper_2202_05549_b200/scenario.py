@@ -74,11 +74,23 @@ def gather_signature(sc: dict, annotation: str) -> list[tuple]:
 
 
 def register_gather_kernels(ctx: Context, sc: dict, launcher=None, user_for: Callable | None = None):
+    """register_gather_kernels (scenario.cpp:368-389): one context-local `gather@<launch index>`
+    kernel per gather launch, with the native GPU body (mt_ctx_gather_register)."""
     import ctypes as C
+    arrays = {a["name"]: a for a in sc.get("arrays", [])}
     for index, l in enumerate(sc.get("launches", [])):
         if l["kernel"] != "gather":
             continue
         sig = gather_signature(sc, l["annotation"])
+        if launcher is None and ctx.lib.has("ctx_gather_register"):
+            n = len(sig)
+            types = (C.c_int32 * max(1, n))(*[t for _, _, t, _, _ in sig])
+            doms = (capi.Rect * max(1, n))()
+            for i, (name, _, _, r, _) in enumerate(sig):
+                doms[i] = capi.Rect.make([0] * r, arrays[name]["domain"])
+            ctx.lib.check(ctx.lib.ctx_gather_register(ctx.h, f"gather@{index}".encode(), l["annotation"].encode(), n, types, doms))
+            _sig_cache[(ctx.lib.path, f"gather@{index}")] = sig
+            continue
         params = (capi.ParamSpec * max(1, len(sig)))()
         for i, (name, _, t, r, w) in enumerate(sig):
             params[i].name = name.encode()
