@@ -154,12 +154,15 @@ typedef struct mt_config {
 	int32_t execute;                /* 0: plan only (no GPU needed); 1: run on GPUs    */
 	int32_t num_gpus;               /* physical GPUs to map devices onto (0 = all)     */
 	int32_t streams_per_device;     /* compute streams per logical device (0 = 4)      */
-	int32_t oracle_mode;            /* shim only: 1 worker x 1 device semantics         */
+	int32_t single_worker;          /* 0: this process executes every worker; 1: only worker_rank
+	                                   (one process per GPU; every rank plans the full plan) */
 	uint64_t device_capacity;       /* bytes per device the chunk store may use (0 = 90% of free HBM) */
 	uint64_t host_capacity;         /* pinned-host spill tier bytes (0 = no spill tier)  */
 	uint64_t staging_threshold;     /* reference throttle; informational on the GPU path */
 	int32_t record_accesses;        /* keep (task, chunk, region, write) records for mt_plan_accesses */
 	int32_t lookahead_tasks;        /* spill tier: tasks buffered ahead for Belady eviction (0 = 512) */
+	int32_t worker_rank;            /* with single_worker: the worker this process executes */
+	int32_t gpu_base;               /* with single_worker: CUDA ordinal of this process's first GPU */
 } mt_config;
 
 /* One planned chunk access (a create counts as a write of the whole chunk). */
@@ -223,6 +226,14 @@ int mt_plan_accesses(mt_ctx* ctx, mt_access* out, int64_t cap, int64_t* n_out);
 int mt_chunk_meta(mt_ctx* ctx, int64_t chunk, mt_chunk_desc* desc, int32_t* dtype, int32_t* temp);
 /* executor attached to a context (NULL when cfg.execute == 0) */
 mt_exec* mt_ctx_exec(mt_ctx* ctx);
+
+/* ---- one process per worker (cfg.single_worker) -------------------------------------- */
+/* Every rank exports its IPC mailbox blob, the blobs are exchanged out of band (any
+ * all-gather, e.g. torch.distributed), then every rank imports all of them (rank order,
+ * equal sizes). Send/recv tasks between workers of different processes then move through
+ * GPU-driven NVLink rings with no host involvement. Barrier before destroying contexts. */
+int mt_ctx_peer_export(mt_ctx* ctx, void* buf, int64_t cap, int64_t* len);
+int mt_ctx_peer_import(mt_ctx* ctx, const void* blobs, int64_t blob_len, int32_t nblobs);
 
 /* ---- executor alone: drop-in for manta::system_runtime ------------------------------ */
 int mt_exec_create(const mt_config* cfg, mt_exec** out);

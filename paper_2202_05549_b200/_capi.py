@@ -88,9 +88,10 @@ class Config(C.Structure):
     _fields_ = [
         ("workers", C.c_int32), ("devices_per_worker", C.c_int32), ("suppress_conflict_deps", C.c_int32),
         ("compat_deps", C.c_int32), ("execute", C.c_int32), ("num_gpus", C.c_int32),
-        ("streams_per_device", C.c_int32), ("oracle_mode", C.c_int32),
+        ("streams_per_device", C.c_int32), ("single_worker", C.c_int32),
         ("device_capacity", C.c_uint64), ("host_capacity", C.c_uint64), ("staging_threshold", C.c_uint64),
         ("record_accesses", C.c_int32), ("lookahead_tasks", C.c_int32),
+        ("worker_rank", C.c_int32), ("gpu_base", C.c_int32),
     ]
 
 
@@ -161,6 +162,8 @@ _SIGS = {
     "kernel_count": (C.c_int, []),
     "ctx_kernel_register": (C.c_int, [C.c_void_p, C.c_char_p, P(ParamSpec), C.c_int32, C.c_void_p, C.c_void_p]),
     "ctx_gather_register": (C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int32, P(C.c_int32), P(Rect)]),
+    "ctx_peer_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, P(C.c_int64)]),
+    "ctx_peer_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),
     "fuzz_scenario_json": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int64, P(C.c_int64)]),
     "scenario_plan": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(Task), C.c_int64, P(C.c_int64), P(C.c_int64),
                                 C.c_int64, P(C.c_int64), P(ArgBinding), C.c_int64, P(C.c_int64)]),
@@ -170,7 +173,7 @@ _SIGS = {
 }
 # entry points the oracle shim may lack
 _OPTIONAL = {"exec_stats", "exec_last_stream", "kernel_info", "host_threads", "ctx_kernel_register", "fuzz_scenario_json", "scenario_plan",
-             "scenario_run", "plan_accesses", "ctx_gather_register", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
+             "scenario_run", "plan_accesses", "ctx_gather_register", "ctx_peer_export", "ctx_peer_import", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
 
 
 class MantaError(RuntimeError):

@@ -173,7 +173,7 @@ class Context:
 
     def __init__(self, lib: capi.Lib, workers=1, devices=1, execute=True, compat_deps=False, suppress_conflict_deps=False,
                  num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0, record_accesses=False,
-                 lookahead_tasks=0):
+                 lookahead_tasks=0, worker_rank=None, gpu_base=0):
         self.lib = lib
         self.dist = Distributions(lib)
         cfg = capi.Config()
@@ -188,6 +188,8 @@ class Context:
         cfg.staging_threshold = staging_threshold
         cfg.record_accesses = int(record_accesses)
         cfg.lookahead_tasks = int(lookahead_tasks)
+        if worker_rank is not None:  # one process per worker
+            cfg.single_worker, cfg.worker_rank, cfg.gpu_base = 1, int(worker_rank), int(gpu_base)
         h = C.c_void_p()
         lib.check(lib.ctx_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -330,6 +332,29 @@ class Context:
         out = (C.c_uint64 * len(keys))()
         self.lib.check(self.lib.exec_stats(ex, out, len(keys)))
         return dict(zip(keys, [int(v) for v in out]))
+
+    # -- one process per worker ------------------------------------------------------
+    def peer_export(self) -> bytes:
+        n = C.c_int64(0)
+        self.lib.check(self.lib.ctx_peer_export(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        self.lib.check(self.lib.ctx_peer_export(self.h, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def peer_import(self, blobs: Sequence[bytes]):
+        size = len(blobs[0])
+        if any(len(b) != size for b in blobs):
+            raise ValidationError("mailbox blobs differ in size")
+        data = b"".join(blobs)
+        self.lib.check(self.lib.ctx_peer_import(self.h, data, size, len(blobs)))
+
+    def connect_peers(self, group=None):
+        """Exchange mailboxes with every rank of the torch.distributed group and map them."""
+        import torch.distributed as dist
+        mine = self.peer_export()
+        blobs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(blobs, mine, group=group)
+        self.peer_import(blobs)
 
     # -- device timing (bench) ------------------------------------------------------
     def _ex(self):

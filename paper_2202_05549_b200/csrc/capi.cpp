@@ -203,6 +203,15 @@ executor_config exec_cfg(const mt_config& c) {
 	e.device_capacity = c.device_capacity;
 	e.host_capacity = c.host_capacity;
 	e.lookahead = c.lookahead_tasks > 0 ? c.lookahead_tasks : 512;
+	if(c.single_worker) {
+		// one process per worker: this process executes worker_rank only, on GPU ordinal
+		// gpu_base (+ device index); every rank plans the identical full plan
+		if(c.worker_rank < 0 || c.worker_rank >= c.workers) throw validation_error("worker_rank outside the configured workers");
+		e.first_worker = c.worker_rank;
+		e.local_workers = 1;
+		e.gpu_base = c.gpu_base;
+		if(e.num_gpus == 0) e.num_gpus = c.devices_per_worker;
+	}
 	return e;
 }
 
@@ -212,6 +221,7 @@ struct mt_exec {
 	std::unique_ptr<executor> ex;
 	// chunk geometry for host transfers (from create tasks)
 	std::unordered_map<int64_t, std::pair<box, dtype>> chunk_geom;
+	std::vector<uint8_t> peer_blob;
 };
 
 struct mt_ctx {
@@ -360,7 +370,8 @@ int mt_array_read(mt_ctx* ctx, int64_t id, void* host, uint64_t bytes) {
 		e.ex->sync();
 		const array_rec& a = ctx->plan->array(id);
 		if(bytes < static_cast<uint64_t>(a.domain.volume()) * dtype_size(a.type)) throw validation_error("host buffer too small");
-		for(const auto& c : a.chunks) e.ex->download(c.id, host, a.domain, c.region);
+		for(const auto& c : a.chunks)
+			if(e.ex->has_chunk(c.id)) e.ex->download(c.id, host, a.domain, c.region); // single_worker: local chunks only
 	});
 }
 
@@ -385,7 +396,7 @@ int mt_array_check_replicas(mt_ctx* ctx, int64_t id, int32_t* coherent) {
 		for(size_t i = 0; i < a.chunks.size() && *coherent; ++i) {
 			for(size_t j = i + 1; j < a.chunks.size() && *coherent; ++j) {
 				const box ov = intersect(a.chunks[i].region, a.chunks[j].region);
-				if(ov.is_empty()) continue;
+				if(ov.is_empty() || !e.ex->has_chunk(a.chunks[i].id) || !e.ex->has_chunk(a.chunks[j].id)) continue;
 				std::vector<char> x(static_cast<size_t>(ov.volume()) * elem), y(x.size());
 				e.ex->download(a.chunks[i].id, x.data(), ov, ov);
 				e.ex->download(a.chunks[j].id, y.data(), ov, ov);
@@ -506,6 +517,25 @@ int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n) {
 }
 
 void* mt_exec_last_stream(mt_exec* ex) { return ex->ex->last_exec_stream(); }
+
+int mt_ctx_peer_export(mt_ctx* ctx, void* buf, int64_t cap, int64_t* len) {
+	return guarded([&] {
+		mt_exec& e = need_exec(ctx);
+		if(e.peer_blob.empty()) e.peer_blob = e.ex->peer_export();
+		*len = static_cast<int64_t>(e.peer_blob.size());
+		if(buf && cap >= *len) std::memcpy(buf, e.peer_blob.data(), e.peer_blob.size());
+	});
+}
+
+int mt_ctx_peer_import(mt_ctx* ctx, const void* blobs, int64_t blob_len, int32_t nblobs) {
+	return guarded([&] {
+		mt_exec& e = need_exec(ctx);
+		std::vector<std::vector<uint8_t>> v;
+		const auto* p = static_cast<const uint8_t*>(blobs);
+		for(int32_t i = 0; i < nblobs; ++i) v.emplace_back(p + i * blob_len, p + (i + 1) * blob_len);
+		e.ex->peer_import(v);
+	});
+}
 
 int mt_exec_mark(mt_exec* ex, int32_t slot) {
 	return guarded([&] { ex->ex->mark(slot); });

@@ -254,12 +254,12 @@ executor::executor(const executor_config& cfg) : cfg_(cfg) {
 	gpus_.resize(static_cast<size_t>(ng));
 	for(int g = 0; g < ng; ++g) {
 		auto& G = gpus_[static_cast<size_t>(g)];
-		G.ordinal = g;
-		check_cuda(cudaSetDevice(g), "cudaSetDevice");
+		G.ordinal = cfg.gpu_base + g;
+		check_cuda(cudaSetDevice(G.ordinal), "cudaSetDevice");
 		cudaMemPoolProps props{};
 		props.allocType = cudaMemAllocationTypePinned;
 		props.location.type = cudaMemLocationTypeDevice;
-		props.location.id = g;
+		props.location.id = G.ordinal;
 		check_cuda(cudaMemPoolCreate(&G.pool, &props), "cudaMemPoolCreate");
 		uint64_t threshold = std::numeric_limits<uint64_t>::max();
 		check_cuda(cudaMemPoolSetAttribute(G.pool, cudaMemPoolAttrReleaseThreshold, &threshold), "cudaMemPoolSetAttribute");
@@ -278,16 +278,16 @@ executor::executor(const executor_config& cfg) : cfg_(cfg) {
 		for(int b = 0; b < ng; ++b) {
 			if(a == b) continue;
 			int can = 0;
-			cudaDeviceCanAccessPeer(&can, a, b);
+			cudaDeviceCanAccessPeer(&can, ord(a), ord(b));
 			if(!can) continue;
-			cudaSetDevice(a);
-			const cudaError_t pe = cudaDeviceEnablePeerAccess(b, 0);
+			cudaSetDevice(ord(a));
+			const cudaError_t pe = cudaDeviceEnablePeerAccess(ord(b), 0);
 			if(pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) check_cuda(pe, "cudaDeviceEnablePeerAccess");
 			cudaGetLastError();
 			// let kernels on `a` dereference chunks allocated from b's pool
 			cudaMemAccessDesc d{};
 			d.location.type = cudaMemLocationTypeDevice;
-			d.location.id = a;
+			d.location.id = ord(a);
 			d.flags = cudaMemAccessFlagsProtReadWrite;
 			check_cuda(cudaMemPoolSetAccess(gpus_[static_cast<size_t>(b)].pool, &d, 1), "cudaMemPoolSetAccess");
 		}
@@ -302,10 +302,11 @@ executor::executor(const executor_config& cfg) : cfg_(cfg) {
 			const int global_index = local && cfg.local_workers >= 0 ? (w - cfg.first_worker) * nd + d : w * nd + d;
 			L.gpu = global_index % ng;
 			if(!local) continue;
-			check_cuda(cudaSetDevice(L.gpu), "cudaSetDevice");
+			check_cuda(cudaSetDevice(ord(L.gpu)), "cudaSetDevice");
 			L.compute.resize(static_cast<size_t>(k));
 			for(auto& s : L.compute) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
 			check_cuda(cudaStreamCreateWithFlags(&L.copy, cudaStreamNonBlocking), "cudaStreamCreate");
+			check_cuda(cudaStreamCreateWithFlags(&L.recv, cudaStreamNonBlocking), "cudaStreamCreate");
 		}
 	}
 }
@@ -315,8 +316,11 @@ executor::~executor() {
 		cudaSetDevice(G.ordinal);
 		cudaDeviceSynchronize();
 	}
+	// peers must have stopped writing into our mailbox (callers barrier before teardown)
+	for(void* p : opened_) cudaIpcCloseMemHandle(p);
+	if(mbox_) cudaFree(mbox_);
 	for(auto& [id, b] : bufs_) {
-		cudaSetDevice(b.gpu);
+		cudaSetDevice(ord(b.gpu));
 		if(b.ptr) cudaFree(b.ptr); // pool memory: cudaFree is legal on stream-ordered allocations
 		if(b.host) cudaFreeHost(b.host);
 	}
@@ -327,6 +331,7 @@ executor::~executor() {
 	for(auto& L : ldevs_) {
 		for(auto s : L.compute) cudaStreamDestroy(s);
 		if(L.copy) cudaStreamDestroy(L.copy);
+		if(L.recv) cudaStreamDestroy(L.recv);
 	}
 	for(auto& G : gpus_) {
 		cudaSetDevice(G.ordinal);
@@ -348,7 +353,7 @@ executor::ldev& executor::dev(device_id d) {
 		throw validation_error("task routed to unknown device " + to_string(d));
 	auto& L = ldevs_[static_cast<size_t>(d.worker * cfg_.devices_per_worker + d.device)];
 	if(L.compute.empty()) throw validation_error("device " + to_string(d) + " is not executed by this process");
-	check_cuda(cudaSetDevice(L.gpu), "cudaSetDevice");
+	check_cuda(cudaSetDevice(ord(L.gpu)), "cudaSetDevice");
 	return L;
 }
 
@@ -400,6 +405,7 @@ cudaStream_t executor::pick_compute(const task& t, ldev& L) {
 void executor::finish(const task& t, cudaStream_t s) {
 	int cur = 0;
 	cudaGetDevice(&cur);
+	cur -= cfg_.gpu_base; // ordinal -> executor GPU index
 	cudaEvent_t ev = take_event(cur);
 	check_cuda(cudaEventRecord(ev, s), "cudaEventRecord");
 	done_[t.id] = {ev, s, cur};
@@ -622,7 +628,7 @@ void executor::host_release(void* p, uint64_t bytes, cudaEvent_t after) { host_f
 void executor::evict(int64_t chunk) {
 	buffer& b = buf(chunk);
 	auto& G = gpus_[static_cast<size_t>(b.gpu)];
-	check_cuda(cudaSetDevice(b.gpu), "cudaSetDevice");
+	check_cuda(cudaSetDevice(ord(b.gpu)), "cudaSetDevice");
 	for(const auto u : b.users) {
 		const auto it = done_.find(u);
 		if(it != done_.end()) check_cuda(cudaStreamWaitEvent(G.d2h, it->second.ev, 0), "cudaStreamWaitEvent");
@@ -703,7 +709,7 @@ void executor::restore(int64_t chunk, const std::vector<int64_t>& pinned, const 
 	buffer& b = buf(chunk);
 	ensure_room(b.gpu, b.bytes, pinned);
 	auto& G = gpus_[static_cast<size_t>(b.gpu)];
-	check_cuda(cudaSetDevice(b.gpu), "cudaSetDevice");
+	check_cuda(cudaSetDevice(ord(b.gpu)), "cudaSetDevice");
 	alloc_wait(b.gpu, G.h2d);
 	check_cuda(cudaMallocFromPoolAsync(&b.ptr, b.bytes, G.pool, G.h2d), "cudaMallocFromPoolAsync (restore)");
 	const bool needed = b.host_valid && !dead_ahead(chunk, &current);
@@ -882,13 +888,14 @@ void executor::run_copy(const task& t) {
 	ldev& L = dev(t.resource);
 	cudaStream_t s = L.copy;
 	wait_deps(t, s);
-	copy_box(src.ptr, src.region, src.gpu, dst.ptr, dst.region, dst.gpu, t.dst_region, dtype_size(src.type), s);
+	copy_box(src.ptr, src.region, ord(src.gpu), dst.ptr, dst.region, ord(dst.gpu), t.dst_region, dtype_size(src.type), s);
 	++ctr_.copies;
 	ctr_.bytes_copied += static_cast<uint64_t>(t.dst_region.volume()) * dtype_size(src.type);
 	finish(t, s);
 }
 
 void executor::run_send(const task& t) {
+	if(remote_worker(t.peer)) return remote_send(t);
 	const buffer& src = buf(t.chunk);
 	ldev& L = dev(t.resource);
 	cudaStream_t s = L.copy;
@@ -898,7 +905,7 @@ void executor::run_send(const task& t) {
 	m.bytes = static_cast<uint64_t>(t.region.volume()) * dtype_size(src.type);
 	m.gpu = L.gpu;
 	check_cuda(cudaMallocFromPoolAsync(&m.ptr, m.bytes, G.pool, s), "cudaMallocFromPoolAsync");
-	copy_box(src.ptr, src.region, src.gpu, m.ptr, t.region, L.gpu, t.region, dtype_size(src.type), s);
+	copy_box(src.ptr, src.region, ord(src.gpu), m.ptr, t.region, ord(L.gpu), t.region, dtype_size(src.type), s);
 	m.ready = take_event(L.gpu);
 	check_cuda(cudaEventRecord(m.ready, s), "cudaEventRecord");
 	const auto key = std::make_tuple(t.worker, t.peer, t.tag);
@@ -909,6 +916,7 @@ void executor::run_send(const task& t) {
 }
 
 void executor::run_recv(const task& t) {
+	if(remote_worker(t.peer)) return remote_recv(t);
 	const auto key = std::make_tuple(t.peer, t.worker, t.tag);
 	const auto it = mailbox_.find(key);
 	if(it == mailbox_.end())
@@ -923,15 +931,15 @@ void executor::run_recv(const task& t) {
 	check_cuda(cudaStreamWaitEvent(s, m.ready, 0), "cudaStreamWaitEvent");
 	if(m.bytes != static_cast<uint64_t>(t.region.volume()) * dtype_size(dst.type))
 		throw execution_error("received payload size does not match the destination region");
-	copy_box(m.ptr, t.region, m.gpu, dst.ptr, dst.region, dst.gpu, t.region, dtype_size(dst.type), s);
+	copy_box(m.ptr, t.region, ord(m.gpu), dst.ptr, dst.region, ord(dst.gpu), t.region, dtype_size(dst.type), s);
 	// release the message buffer on its own device once the unpack is done
 	cudaEvent_t unpacked = take_event(L.gpu);
 	check_cuda(cudaEventRecord(unpacked, s), "cudaEventRecord");
 	auto& G = gpus_[static_cast<size_t>(m.gpu)];
-	check_cuda(cudaSetDevice(m.gpu), "cudaSetDevice");
+	check_cuda(cudaSetDevice(ord(m.gpu)), "cudaSetDevice");
 	check_cuda(cudaStreamWaitEvent(G.service, unpacked, 0), "cudaStreamWaitEvent");
 	check_cuda(cudaFreeAsync(m.ptr, G.service), "cudaFreeAsync");
-	check_cuda(cudaSetDevice(L.gpu), "cudaSetDevice");
+	check_cuda(cudaSetDevice(ord(L.gpu)), "cudaSetDevice");
 	free_events_[static_cast<size_t>(m.gpu)].push_back(m.ready);
 	free_events_[static_cast<size_t>(L.gpu)].push_back(unpacked);
 	ctr_.bytes_received += m.bytes;
@@ -1022,11 +1030,11 @@ void executor::download(int64_t chunk, void* host, const box& host_box, const bo
 	drain(true);
 	const buffer& b = buf(chunk);
 	if(!encloses(b.region, region) || !encloses(host_box, region)) throw validation_error("download region outside the chunk or the host box");
-	check_cuda(cudaSetDevice(b.gpu), "cudaSetDevice");
+	check_cuda(cudaSetDevice(ord(b.gpu)), "cudaSetDevice");
 	cudaStream_t s = gpus_[static_cast<size_t>(b.gpu)].service;
 	check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
 	if(b.ptr)
-		copy_box(b.ptr, b.region, b.gpu, host, host_box, -1, region, dtype_size(b.type), s);
+		copy_box(b.ptr, b.region, ord(b.gpu), host, host_box, -1, region, dtype_size(b.type), s);
 	else
 		copy_box(b.host, b.region, -1, host, host_box, -1, region, dtype_size(b.type), s); // evicted: host copy is current
 	check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
@@ -1036,17 +1044,163 @@ void executor::upload(int64_t chunk, const void* host, const box& host_box) {
 	drain(true);
 	buffer& b = buf(chunk);
 	if(!encloses(host_box, b.region)) throw validation_error("upload: chunk outside the host box");
-	check_cuda(cudaSetDevice(b.gpu), "cudaSetDevice");
+	check_cuda(cudaSetDevice(ord(b.gpu)), "cudaSetDevice");
 	cudaStream_t s = gpus_[static_cast<size_t>(b.gpu)].service;
 	check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
 	if(b.ptr) {
-		copy_box(host, host_box, -1, b.ptr, b.region, b.gpu, b.region, dtype_size(b.type), s);
+		copy_box(host, host_box, -1, b.ptr, b.region, ord(b.gpu), b.region, dtype_size(b.type), s);
 		b.host_valid = false;
 	} else {
 		copy_box(host, host_box, -1, b.host, b.region, -1, b.region, dtype_size(b.type), s);
 		b.host_valid = true;
 	}
 	check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
+// ---- inter-process send/recv (one process per worker) -------------------------------------
+//
+// A message of the planner's send/recv pair (planner.cpp:96-119) moves as segments of at most
+// kSlotBytes through a per-(src, dst) ring of kSlots slots that lives in the RECEIVER's
+// IPC-mapped mailbox. Per segment q (slot q % kSlots), entirely GPU-driven and stream-ordered:
+//   sender   (copy stream): wait consumed >= q+1-kSlots  ->  peer copy into the slot over
+//                           NVLink  ->  release-store ready[slot] = q+1 (system scope)
+//   receiver (recv stream): acquire-wait ready[slot] >= q+1  ->  copy slot into the chunk  ->
+//                           release-store the sender's consumed counter = q+1
+// Both sides derive the same segment sequence from the replicated plan (same regions, tags in
+// issue order), so no host round trip is needed. Sends and receives use different streams so a
+// sender spinning on a full ring never blocks the receive that would drain the peer's ring.
+
+namespace {
+
+__global__ void spin_until_geq(const uint64_t* flag, uint64_t value) {
+	uint64_t v = 0;
+	for(;;) {
+		asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+		if(v >= value) break;
+		__nanosleep(64);
+	}
+}
+
+__global__ void release_store(uint64_t* flag, uint64_t value) {
+	asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
+
+struct mbox_blob {
+	uint64_t magic;
+	int32_t rank, world, slots, pad;
+	uint64_t slot_bytes;
+	cudaIpcMemHandle_t handle;
+};
+constexpr uint64_t kMboxMagic = 0x6d616e7461623230ull; // "mantab20"
+
+uint64_t ring_off(int src) { return static_cast<uint64_t>(src) * executor::kSlots * executor::kSlotBytes; }
+uint64_t flag_off(int world, int src) { return static_cast<uint64_t>(world) * executor::kSlots * executor::kSlotBytes + static_cast<uint64_t>(src) * executor::kSlots * 8; }
+uint64_t cons_off(int world, int dst) { return flag_off(world, world) + static_cast<uint64_t>(dst) * 128; }
+uint64_t mbox_bytes(int world) { return cons_off(world, world); }
+
+} // namespace
+
+std::vector<uint8_t> executor::peer_export() {
+	if(cfg_.local_workers != 1 || cfg_.devices_per_worker != 1) throw validation_error("inter-process messaging needs one worker with one device per process");
+	if(mbox_) throw validation_error("mailbox already exported");
+	world_ = cfg_.workers;
+	my_rank_ = cfg_.first_worker;
+	check_cuda(cudaSetDevice(ord(0)), "cudaSetDevice");
+	const uint64_t bytes = mbox_bytes(world_);
+	check_cuda(cudaMalloc(&mbox_, bytes), "cudaMalloc (mailbox)");
+	check_cuda(cudaMemset(mbox_ + flag_off(world_, 0), 0, bytes - flag_off(world_, 0)), "cudaMemset (mailbox flags)");
+	check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+	mbox_blob b{};
+	b.magic = kMboxMagic;
+	b.rank = my_rank_;
+	b.world = world_;
+	b.slots = kSlots;
+	b.slot_bytes = kSlotBytes;
+	check_cuda(cudaIpcGetMemHandle(&b.handle, mbox_), "cudaIpcGetMemHandle");
+	std::vector<uint8_t> out(sizeof(b));
+	std::memcpy(out.data(), &b, sizeof(b));
+	return out;
+}
+
+void executor::peer_import(const std::vector<std::vector<uint8_t>>& blobs) {
+	if(!mbox_) throw validation_error("export the local mailbox first");
+	if(static_cast<int>(blobs.size()) != world_) throw validation_error("one mailbox blob per worker expected");
+	check_cuda(cudaSetDevice(ord(0)), "cudaSetDevice");
+	links_.assign(static_cast<size_t>(world_), peer_link{});
+	for(int p = 0; p < world_; ++p) {
+		mbox_blob b{};
+		if(blobs[static_cast<size_t>(p)].size() != sizeof(b)) throw validation_error("bad mailbox blob");
+		std::memcpy(&b, blobs[static_cast<size_t>(p)].data(), sizeof(b));
+		if(b.magic != kMboxMagic || b.rank != p || b.world != world_ || b.slots != kSlots || b.slot_bytes != kSlotBytes)
+			throw validation_error("mailbox blob " + std::to_string(p) + " does not match this configuration");
+		if(p == my_rank_) continue;
+		void* base = nullptr;
+		check_cuda(cudaIpcOpenMemHandle(&base, b.handle, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+		opened_.push_back(base);
+		char* peer = static_cast<char*>(base);
+		auto& l = links_[static_cast<size_t>(p)];
+		l.tx_ring = peer + ring_off(my_rank_);
+		l.tx_ready = reinterpret_cast<uint64_t*>(peer + flag_off(world_, my_rank_));
+		l.tx_consumed = reinterpret_cast<uint64_t*>(mbox_ + cons_off(world_, p));
+		l.rx_ring = mbox_ + ring_off(p);
+		l.rx_ready = reinterpret_cast<uint64_t*>(mbox_ + flag_off(world_, p));
+		l.rx_consumed = reinterpret_cast<uint64_t*>(peer + cons_off(world_, my_rank_));
+	}
+}
+
+void executor::remote_send(const task& t) {
+	if(links_.empty()) throw execution_error("send to worker " + std::to_string(t.peer) + " in another process before peer_import");
+	const buffer& src = buf(t.chunk);
+	ldev& L = dev(t.resource);
+	cudaStream_t s = L.copy;
+	wait_deps(t, s);
+	auto& link = links_.at(static_cast<size_t>(t.peer));
+	auto& G = gpus_[static_cast<size_t>(L.gpu)];
+	const size_t elem = dtype_size(src.type);
+	const uint64_t bytes = static_cast<uint64_t>(t.region.volume()) * elem;
+	// contiguous staging of the region (one copy when it is already contiguous in the chunk)
+	void* stage = nullptr;
+	check_cuda(cudaMallocFromPoolAsync(&stage, bytes, G.pool, s), "cudaMallocFromPoolAsync");
+	copy_box(src.ptr, src.region, ord(src.gpu), stage, t.region, ord(L.gpu), t.region, elem, s);
+	for(uint64_t off = 0; off < bytes; off += kSlotBytes) {
+		const uint64_t seg = std::min<uint64_t>(kSlotBytes, bytes - off);
+		const uint64_t q = link.tx_seq++;
+		const uint64_t slot = q % kSlots;
+		if(q >= static_cast<uint64_t>(kSlots)) spin_until_geq<<<1, 1, 0, s>>>(link.tx_consumed, q + 1 - kSlots);
+		check_cuda(cudaMemcpyAsync(link.tx_ring + slot * kSlotBytes, static_cast<char*>(stage) + off, seg, cudaMemcpyDefault, s), "cudaMemcpyAsync (send)");
+		release_store<<<1, 1, 0, s>>>(link.tx_ready + slot, q + 1);
+	}
+	check_cuda(cudaFreeAsync(stage, s), "cudaFreeAsync");
+	check_cuda(cudaGetLastError(), "send kernels");
+	ctr_.bytes_sent += bytes;
+	finish(t, s);
+}
+
+void executor::remote_recv(const task& t) {
+	if(links_.empty()) throw execution_error("receive from worker " + std::to_string(t.peer) + " in another process before peer_import");
+	const buffer& dst = buf(t.chunk);
+	ldev& L = dev(t.resource);
+	cudaStream_t s = L.recv;
+	wait_deps(t, s);
+	auto& link = links_.at(static_cast<size_t>(t.peer));
+	auto& G = gpus_[static_cast<size_t>(L.gpu)];
+	const size_t elem = dtype_size(dst.type);
+	const uint64_t bytes = static_cast<uint64_t>(t.region.volume()) * elem;
+	void* stage = nullptr;
+	check_cuda(cudaMallocFromPoolAsync(&stage, bytes, G.pool, s), "cudaMallocFromPoolAsync");
+	for(uint64_t off = 0; off < bytes; off += kSlotBytes) {
+		const uint64_t seg = std::min<uint64_t>(kSlotBytes, bytes - off);
+		const uint64_t q = link.rx_seq++;
+		const uint64_t slot = q % kSlots;
+		spin_until_geq<<<1, 1, 0, s>>>(link.rx_ready + slot, q + 1);
+		check_cuda(cudaMemcpyAsync(static_cast<char*>(stage) + off, link.rx_ring + slot * kSlotBytes, seg, cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync (recv)");
+		release_store<<<1, 1, 0, s>>>(link.rx_consumed, q + 1);
+	}
+	copy_box(stage, t.region, ord(L.gpu), dst.ptr, dst.region, ord(dst.gpu), t.region, elem, s);
+	check_cuda(cudaFreeAsync(stage, s), "cudaFreeAsync");
+	check_cuda(cudaGetLastError(), "recv kernels");
+	ctr_.bytes_received += bytes;
+	finish(t, s);
 }
 
 std::string executor::report_json() const {

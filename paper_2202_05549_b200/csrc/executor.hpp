@@ -40,6 +40,7 @@ struct executor_config {
 	uint64_t host_capacity = 0;   // pinned-host spill tier; 0 disables spilling
 	int lookahead = 512;          // spill tier: tasks held back so eviction can see future uses
 	int first_worker = 0;         // workers [first, first+local) execute here (multi-process)
+	int gpu_base = 0;             // first CUDA device ordinal this executor uses
 	int local_workers = -1;       // -1: all workers
 };
 
@@ -89,6 +90,15 @@ class executor {
 	void set_profile(bool on) { profile_ = on; }
 	void kernel_time(const std::string& kernel, int64_t* count, double* total_ms);
 
+	// One process per worker: GPU-driven point-to-point messaging for send/recv tasks whose
+	// peer worker runs in another process. Every rank exports one IPC-mapped mailbox (a ring of
+	// kSlots x kSlotBytes per source rank, ready flags, consumption counters); after the blobs
+	// are exchanged out of band (torch.distributed), each rank maps every peer's mailbox.
+	std::vector<uint8_t> peer_export();
+	void peer_import(const std::vector<std::vector<uint8_t>>& blobs);
+	static constexpr int kSlots = 4;
+	static constexpr uint64_t kSlotBytes = 16ull << 20;
+
   private:
 	struct buffer {
 		void* ptr = nullptr; // device copy (null while evicted)
@@ -109,8 +119,27 @@ class executor {
 		int gpu = 0;
 		std::vector<cudaStream_t> compute;
 		cudaStream_t copy = nullptr;
+		cudaStream_t recv = nullptr; // inter-process receives (never queued behind a spinning send)
 		size_t rr = 0;
 	};
+	struct peer_link {
+		char* tx_ring = nullptr;              // my ring inside the peer's mailbox
+		uint64_t* tx_ready = nullptr;         // ready flags for my segments (peer memory)
+		uint64_t* tx_consumed = nullptr;      // peer's consumption of my segments (my memory)
+		uint64_t tx_seq = 0;
+		char* rx_ring = nullptr;              // the peer's ring inside my mailbox
+		uint64_t* rx_ready = nullptr;         // its ready flags (my memory)
+		uint64_t* rx_consumed = nullptr;      // my consumption of its segments (peer memory)
+		uint64_t rx_seq = 0;
+	};
+	char* mbox_ = nullptr;
+	int world_ = 0;
+	int my_rank_ = -1;
+	std::vector<peer_link> links_;
+	std::vector<void*> opened_;
+	bool remote_worker(int w) const { return cfg_.local_workers >= 0 && (w < cfg_.first_worker || w >= cfg_.first_worker + cfg_.local_workers); }
+	void remote_send(const task& t);
+	void remote_recv(const task& t);
 	struct gpu_res {
 		int ordinal = 0;
 		cudaMemPool_t pool = nullptr;
@@ -154,6 +183,7 @@ class executor {
 	std::map<std::string, kernel_timing> ktimes_;
 
 	ldev& dev(device_id d);
+	int ord(int gpu_index) const { return gpus_[static_cast<size_t>(gpu_index)].ordinal; }
 	cudaEvent_t take_event(int gpu);
 	void wait_deps(const task& t, cudaStream_t s);
 	cudaStream_t pick_compute(const task& t, ldev& L);

@@ -1,0 +1,121 @@
+"""One process per worker on the GPU: every rank plans the full plan, executes only its own
+worker's tasks, and the cross-worker send/recv tasks (halo rows, reduce partials) move through
+the GPU-driven IPC mailbox rings. Two processes share the single test GPU (IPC works within a
+device; the spin-waits progress under time-slicing), so this checks correctness, not speed.
+The gathered result is compared bit-exact with the single-process run."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+HEAT = "global [i, j] => read in[i-1:i+1, j-1:j+1], write out[i,j]"
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _heat_rank(rank, world, port, rows, cols, iters, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+    ctx = mb.context(workers=world, devices=1, worker_rank=rank, gpu_base=0)
+    ctx.connect_peers()
+    devs = ctx.devices
+    dist_ = lambda: ctx.dist.stencil([rows, cols], [rows // world, cols], [1, 0], devs)  # noqa: E731
+    a = ctx.create_array([rows, cols], "f32", dist_(), 0)
+    b = ctx.create_array([rows, cols], "f32", dist_(), 0)
+    work = ctx.dist.block_work([rows, cols], [16, 16], [rows // world, cols], devs)
+    ctx.launch("ramp2d_f32", [rows, cols], [16, 16], work, [rows, cols, 1000, 0.0, 1.0, Arr(a)], "global [i, j] => write out[i,j]")
+    for _ in range(iters):
+        ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT)
+        ctx.flush()
+        a, b = b, a
+    ctx.synchronize()
+    out = ctx.read(a)  # local chunks only
+    lo = rank * rows // world
+    hi = (rank + 1) * rows // world
+    q.put((rank, out[lo:hi].copy(), ctx.exec_stats()))
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_two_process_heat_matches_single_process():
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+    rows, cols, iters, world = 256, 512, 4, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_heat_rank, args=(r, world, port, rows, cols, iters, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    got = np.concatenate([p[1] for p in parts])
+    assert all(p[2]["bytes_sent"] > 0 for p in parts)
+    with mb.context(workers=1, devices=world, num_gpus=1) as c:
+        devs = c.devices
+        a = c.create_array([rows, cols], "f32", c.dist.stencil([rows, cols], [rows // world, cols], [1, 0], devs), 0)
+        b = c.create_array([rows, cols], "f32", c.dist.stencil([rows, cols], [rows // world, cols], [1, 0], devs), 0)
+        w = c.dist.block_work([rows, cols], [16, 16], [rows // world, cols], devs)
+        c.launch("ramp2d_f32", [rows, cols], [16, 16], w, [rows, cols, 1000, 0.0, 1.0, Arr(a)], "global [i, j] => write out[i,j]")
+        for _ in range(iters):
+            c.launch("heat2d", [rows, cols], [16, 16], w, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT)
+            a, b = b, a
+        want = c.read(a)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def _hist_rank(rank, world, port, n, bins, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+    ctx = mb.context(workers=world, devices=1, worker_rank=rank, gpu_base=0)
+    ctx.connect_peers()
+    devs = ctx.devices
+    per = n // world
+    x = ctx.create_array([n], "i32", ctx.dist.row([n], per, devs), 0)
+    h = ctx.create_array([bins], "i64", ctx.dist.replicated([bins], devs), 0)
+    w = ctx.dist.block_work([n], [128], [per], devs)
+    ctx.launch("hpattern1d", [n], [128], w, [n, bins, 5, Arr(x)], "global i => write out[i]")
+    ctx.launch("histogram", [n], [128], w, [n, bins, Arr(x), Arr(h)], "global i => read x[i], reduce(+) hist[:]")
+    ctx.synchronize()
+    q.put((rank, ctx.read(h)))
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_two_process_reduce_tree(okern):
+    """partials travel to the root worker and the result back to every replica via the rings"""
+    import ctypes as C
+    n, bins, world = 1 << 20, 1000, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_hist_rank, args=(r, world, port, n, bins, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = np.empty(bins, np.int64)
+    okern.oracle_histogram_hashed(C.c_int64(0), C.c_int64(n), C.c_int64(bins), C.c_int64(5), want.ctypes.data_as(C.POINTER(C.c_int64)))
+    for _, h in res:
+        assert np.array_equal(h, want)
