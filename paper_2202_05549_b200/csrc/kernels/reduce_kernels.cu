@@ -139,18 +139,18 @@ __global__ void kmeans_update_i32_kernel(range r, int64_t k, int64_t d, dview po
 
 // Up to ~110K bins: two u16 counters per u32 shared word (65536 bins = 128 KB). A half that
 // wraps past 0xFFFF is detected from the atomic's old value and its 65536 moved to the global
-// partial (for the low half the carry that leaked into the high half is taken back).
+// partial (for the low half the carry that leaked into the high half is taken back). With
+// uniformly spread values the kernel is bound by shared-memory atomic throughput under random
+// bank conflicts, not by HBM.
 constexpr int kHistPairMaxBins = 110000;
 
-__global__ void histogram_pair_kernel(const int32_t* x, int64_t n_local, int64_t bins, unsigned long long* hist) {
+__global__ void __launch_bounds__(1024, 1) histogram_pair_kernel(const int32_t* x, int64_t n_local, int bins, unsigned long long* hist) {
 	extern __shared__ uint32_t w[];
-	const int64_t words = (bins + 1) / 2;
-	for(int64_t b = threadIdx.x; b < words; b += blockDim.x) w[b] = 0;
+	const int words = (bins + 1) / 2;
+	for(int b = threadIdx.x; b < words; b += blockDim.x) w[b] = 0;
 	__syncthreads();
-	const auto add = [&](int32_t v) {
-		if(static_cast<uint64_t>(v) >= static_cast<uint64_t>(bins)) return;
+	const auto fixup = [&](int32_t v, uint32_t old) {
 		const uint32_t sh = (v & 1) * 16;
-		const uint32_t old = atomicAdd(&w[v >> 1], 1u << sh);
 		if(((old >> sh) & 0xFFFFu) == 0xFFFFu) {
 			if(sh == 0) atomicSub(&w[v >> 1], 1u << 16);
 			atomicAdd(hist + v, 65536ull);
@@ -159,16 +159,37 @@ __global__ void histogram_pair_kernel(const int32_t* x, int64_t n_local, int64_t
 	const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
 	const int64_t nvec = n_local / 4;
 	const int4* xv = reinterpret_cast<const int4*>(x);
-	for(int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nvec; t += stride) {
-		const int4 v = __ldcs(xv + t);
-		add(v.x);
-		add(v.y);
-		add(v.z);
-		add(v.w);
+	// one CTA of 32 warps per SM: four 16-byte loads in flight per thread keep ~64 KB per SM
+	// outstanding, enough to cover HBM latency at full bandwidth
+	constexpr int U = 4;
+	int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+	for(; t + (U - 1) * stride < nvec; t += U * stride) {
+		int32_t v[4 * U];
+#pragma unroll
+		for(int u = 0; u < U; ++u) {
+			const int4 q = __ldcs(xv + t + u * stride);
+			v[4 * u] = q.x;
+			v[4 * u + 1] = q.y;
+			v[4 * u + 2] = q.z;
+			v[4 * u + 3] = q.w;
+		}
+#pragma unroll
+		for(int e = 0; e < 4 * U; ++e)
+			if(static_cast<uint32_t>(v[e]) < static_cast<uint32_t>(bins)) fixup(v[e], atomicAdd(&w[v[e] >> 1], 1u << ((v[e] & 1) * 16)));
 	}
-	for(int64_t t = nvec * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n_local; t += stride) add(x[t]);
+	for(; t < nvec; t += stride) {
+		const int4 q = __ldcs(xv + t);
+		const int32_t v[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+		for(int e = 0; e < 4; ++e)
+			if(static_cast<uint32_t>(v[e]) < static_cast<uint32_t>(bins)) fixup(v[e], atomicAdd(&w[v[e] >> 1], 1u << ((v[e] & 1) * 16)));
+	}
+	for(int64_t e = nvec * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_local; e += stride) {
+		const int32_t v = x[e];
+		if(static_cast<uint32_t>(v) < static_cast<uint32_t>(bins)) fixup(v, atomicAdd(&w[v >> 1], 1u << ((v & 1) * 16)));
+	}
 	__syncthreads();
-	for(int64_t b = threadIdx.x; b < words; b += blockDim.x) {
+	for(int b = threadIdx.x; b < words; b += blockDim.x) {
 		const uint32_t v = w[b];
 		if(v & 0xFFFFu) atomicAdd(hist + 2 * b, static_cast<unsigned long long>(v & 0xFFFFu));
 		if((v >> 16) && 2 * b + 1 < bins) atomicAdd(hist + 2 * b + 1, static_cast<unsigned long long>(v >> 16));
@@ -176,36 +197,54 @@ __global__ void histogram_pair_kernel(const int32_t* x, int64_t n_local, int64_t
 }
 
 // k-means assignment, fast path: when every |coordinate| < 8192 (checked on the fly: the
-// block checks its centroid table, each thread its points) a squared distance over d <= 16
-// dimensions fits in u32 exactly, so the int64 reference arithmetic becomes one IADD + one
-// IMAD per (point, centroid, dimension). Two points per thread share every centroid load
-// (broadcast LDS.128 from shared memory). Points outside the range take the int64 path.
-constexpr int kKmPts = 2;
+// block checks its centroid table, each thread its points) the squared distance over d <= 16
+// dimensions lies in [0, 2^32), so it is computed exactly in wrapping u32 arithmetic as
+// |x|^2 + |c|^2 - 2 x.c: the table holds -2c (and |c|^2 per row), so each (point, centroid)
+// costs 16 IMADs on the FMA pipe plus one IADD3 / compare / select on the ALU pipe (the
+// direct (x-c)^2 form costs 32 FMA-pipe ops, because ptxas moves the subtractions there too).
+// The exact distance makes the argmin (first minimum, strict '<') identical to the int64
+// reference (kernels.cpp:283-292). Four points per thread share each broadcast centroid load.
+// Points outside the range take the int64 path.
+constexpr int kKmPts = 4;
 
-__global__ void __launch_bounds__(256) kmeans_assign_fast_kernel(const int32_t* __restrict__ points, int64_t pld, int64_t n_local, int k, int d,
+__global__ void __launch_bounds__(256, 2) kmeans_assign_fast_kernel(const int32_t* __restrict__ points, int64_t pld, int64_t n_local, int k, int d,
     const int32_t* __restrict__ cents, int64_t cld, int32_t* __restrict__ assign) {
-	extern __shared__ int4 cs4[]; // k rows of 16 i32 (padded to 16 columns)
+	extern __shared__ int4 cs4[]; // k rows of 16 values -2c (padded to 16 columns), then k |c|^2
 	int32_t* cs = reinterpret_cast<int32_t*>(cs4);
+	uint32_t* cn = reinterpret_cast<uint32_t*>(cs + k * 16);
 	int big = 0;
 	for(int e = threadIdx.x; e < k * 16; e += blockDim.x) {
 		const int c = e / 16, q = e % 16;
 		const int32_t v = q < d ? cents[static_cast<int64_t>(c) * cld + q] : 0;
-		cs[e] = v;
-		big |= (v >= 8192 || v <= -8192);
+		const bool b = (v >= 8192 || v <= -8192);
+		big |= b;
+		cs[e] = b ? 0 : -2 * v;
 	}
 	const int cent_big = __syncthreads_or(big);
+	for(int c = threadIdx.x; c < k; c += blockDim.x) {
+		uint32_t s = 0;
+		for(int q = 0; q < 16; ++q) {
+			const uint32_t h = static_cast<uint32_t>(cs[c * 16 + q] / -2);
+			s += h * h;
+		}
+		cn[c] = s;
+	}
+	__syncthreads();
 	const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * kKmPts;
 	for(int64_t base = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kKmPts; base < n_local; base += stride) {
-		int32_t p[kKmPts][16];
+		uint32_t p[kKmPts][16];
+		uint32_t xx[kKmPts];
 		bool ok = !cent_big;
 #pragma unroll
 		for(int j = 0; j < kKmPts; ++j) {
 			const int64_t i = base + j;
+			xx[j] = 0;
 #pragma unroll
 			for(int q = 0; q < 16; ++q) {
 				const int32_t v = (i < n_local && q < d) ? points[i * pld + q] : 0;
-				p[j][q] = v;
+				p[j][q] = static_cast<uint32_t>(v);
 				ok &= (v < 8192 && v > -8192);
+				xx[j] += static_cast<uint32_t>(v) * static_cast<uint32_t>(v);
 			}
 		}
 		uint32_t best[kKmPts];
@@ -216,25 +255,25 @@ __global__ void __launch_bounds__(256) kmeans_assign_fast_kernel(const int32_t* 
 			bi[j] = 0;
 		}
 		if(ok) {
+#pragma unroll 1
 			for(int c = 0; c < k; ++c) {
 				const int4* crow = cs4 + c * 4;
-				int32_t cv[16];
+				uint32_t cv[16];
 #pragma unroll
 				for(int v4 = 0; v4 < 4; ++v4) {
 					const int4 t = crow[v4];
-					cv[4 * v4] = t.x;
-					cv[4 * v4 + 1] = t.y;
-					cv[4 * v4 + 2] = t.z;
-					cv[4 * v4 + 3] = t.w;
+					cv[4 * v4] = static_cast<uint32_t>(t.x);
+					cv[4 * v4 + 1] = static_cast<uint32_t>(t.y);
+					cv[4 * v4 + 2] = static_cast<uint32_t>(t.z);
+					cv[4 * v4 + 3] = static_cast<uint32_t>(t.w);
 				}
+				const uint32_t cc = cn[c];
 #pragma unroll
 				for(int j = 0; j < kKmPts; ++j) {
-					uint32_t dist = 0;
+					uint32_t m2 = 0; // -2 x.c (mod 2^32)
 #pragma unroll
-					for(int q = 0; q < 16; ++q) {
-						const int32_t df = p[j][q] - cv[q];
-						dist += static_cast<uint32_t>(df * df);
-					}
+					for(int q = 0; q < 16; ++q) m2 += p[j][q] * cv[q];
+					const uint32_t dist = xx[j] + cc + m2;
 					if(dist < best[j]) {
 						best[j] = dist;
 						bi[j] = c;
@@ -243,14 +282,14 @@ __global__ void __launch_bounds__(256) kmeans_assign_fast_kernel(const int32_t* 
 			}
 		} else {
 			// exact int64 path (reference arithmetic, kernels.cpp:283-292)
-#pragma unroll
+#pragma unroll 1
 			for(int j = 0; j < kKmPts; ++j) {
 				int64_t b64 = INT64_MAX;
+				const int64_t i = base + j;
 				for(int c = 0; c < k; ++c) {
 					int64_t dist = 0;
-#pragma unroll
-					for(int q = 0; q < 16; ++q) {
-						const int64_t df = static_cast<int64_t>(p[j][q]) - cs[c * 16 + q]; // padded columns are 0 - 0
+					for(int q = 0; q < d; ++q) {
+						const int64_t df = static_cast<int64_t>(i < n_local ? points[i * pld + q] : 0) - cents[static_cast<int64_t>(c) * cld + q];
 						dist += df * df;
 					}
 					if(dist < b64) {
@@ -266,34 +305,79 @@ __global__ void __launch_bounds__(256) kmeans_assign_fast_kernel(const int32_t* 
 	}
 }
 
-// k-means update: per-CTA shared sums as (lo, hi) u32 pairs — one u32 atomic per value plus a
-// second only on carry or for negative values, i.e. an exact wrapping int64 sum — and u32
-// counts; flushed once per CTA with 64-bit global atomics.
-__global__ void kmeans_update_fast_kernel(const int32_t* __restrict__ points, int64_t pld, const int32_t* __restrict__ assign, int64_t n_local, int k,
-    int d, unsigned long long* sums, int64_t sld, unsigned long long* counts) {
+// k-means update: a warp takes 32 points. Lane l counts point l (one shared atomic for 32
+// points), then the warp walks the 32 points in pairs, a half-warp per point and lane q adding
+// coordinate q, so one instruction covers two points x 16 dimensions with a coalesced 128-byte
+// load. Each half-warp owns its own copy of the per-CTA sum table, laid out so copy 0 lives in
+// banks 0-15 and copy 1 in banks 16-31 (row c of copy h at word 32c + 16h): the two points of
+// an instruction never collide in a bank. Each sum is an exact wrapping int64 held as signed
+// i32 words plus one shared wrap counter touched only when an i32 add overflows (detected from
+// the atomics' old values, checked once per group of 8), so a coordinate costs one shared
+// atomic. Points whose assignment lies outside the partial (the reference's bounds-checked view
+// would throw) and lanes past d go to a dummy row k / add 0, so the atomics need no predicates.
+// Flushed once per CTA with 64-bit global atomics.
+template <bool kContig>
+__global__ void __launch_bounds__(512, 2) kmeans_update_fast_kernel(const int32_t* __restrict__ points, int64_t pld, const int32_t* __restrict__ assign,
+    int64_t n_local, int k, int d, unsigned long long* sums, int64_t sld, unsigned long long* counts) {
 	extern __shared__ uint32_t sm[];
-	uint32_t* lo = sm;
-	uint32_t* hi = sm + k * d;
-	uint32_t* cnt = sm + 2 * k * d;
-	for(int e = threadIdx.x; e < 2 * k * d + k; e += blockDim.x) sm[e] = 0;
+	const int rows = k + 1;
+	uint32_t* lo = sm;                // rows x 32 words (two 16-word copies)
+	uint32_t* hi = sm + rows * 32;    // rows x 16 wrap counters
+	uint32_t* cnt = sm + rows * 48;   // rows counts
+	for(int e = threadIdx.x; e < rows * 49; e += blockDim.x) sm[e] = 0;
 	__syncthreads();
-	for(int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_local; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-		const int c = assign[i];
-		if(c < 0 || c >= k) continue; // outside the partial: the reference would fault; skip
-		for(int q = 0; q < d; ++q) {
-			const int32_t v = points[i * pld + q];
-			const uint32_t u = static_cast<uint32_t>(v);
-			const uint32_t old = atomicAdd(&lo[c * d + q], u);
-			const uint32_t carry = (old + u < old) ? 1u : 0u;
-			const uint32_t h = (v < 0 ? 0xFFFFFFFFu : 0u) + carry;
-			if(h) atomicAdd(&hi[c * d + q], h);
+	const int lane = threadIdx.x & 31;
+	const int q = lane & 15;
+	const int h = lane >> 4;
+	const int qc = q < d ? q : 0;
+	const int64_t step = kContig ? 16 : pld;
+	const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+	const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+	for(int64_t i0 = warp * 32; i0 < n_local; i0 += warps * 32) {
+		int cl;
+		int32_t v[16];
+		if(i0 + 32 <= n_local) {
+			cl = __ldcs(assign + i0 + lane);
+			const int32_t* pp = points + (i0 + h) * step + qc;
+#pragma unroll
+			for(int u = 0; u < 16; ++u) v[u] = __ldcs(pp + 2 * u * step);
+		} else {
+			cl = i0 + lane < n_local ? assign[i0 + lane] : k;
+#pragma unroll
+			for(int u = 0; u < 16; ++u) v[u] = i0 + 2 * u + h < n_local ? points[(i0 + 2 * u + h) * step + qc] : 0;
 		}
-		atomicAdd(&cnt[c], 1u);
+		if(static_cast<uint32_t>(cl) >= static_cast<uint32_t>(k)) cl = k;
+		atomicAdd(&cnt[cl], 1u);
+#pragma unroll
+		for(int g = 0; g < 16; g += 8) {
+			uint32_t old[8], uv[8];
+			int c[8];
+			uint32_t ovf = 0;
+#pragma unroll
+			for(int u = 0; u < 8; ++u) {
+				c[u] = __shfl_sync(0xFFFFFFFFu, cl, 2 * (g + u) + h);
+				uv[u] = q < d ? static_cast<uint32_t>(v[g + u]) : 0u;
+				old[u] = atomicAdd(&lo[c[u] * 32 + h * 16 + q], uv[u]);
+				const uint32_t nw = old[u] + uv[u];
+				ovf |= (old[u] ^ nw) & (uv[u] ^ nw);
+			}
+			if(static_cast<int32_t>(ovf) < 0) {
+#pragma unroll
+				for(int u = 0; u < 8; ++u) {
+					const uint32_t nw = old[u] + uv[u];
+					if(static_cast<int32_t>((old[u] ^ nw) & (uv[u] ^ nw)) < 0)
+						atomicAdd(&hi[c[u] * 16 + q], static_cast<int32_t>(uv[u]) < 0 ? 0xFFFFFFFFu : 1u);
+				}
+			}
+		}
 	}
 	__syncthreads();
-	for(int e = threadIdx.x; e < k * d; e += blockDim.x) {
-		const unsigned long long v = (static_cast<unsigned long long>(hi[e]) << 32) | lo[e];
-		if(v) atomicAdd(sums + static_cast<int64_t>(e / d) * sld + e % d, v);
+	for(int e = threadIdx.x; e < k * 16; e += blockDim.x) {
+		const int c = e / 16, qq = e % 16;
+		if(qq >= d) continue;
+		const int64_t v = static_cast<int64_t>(static_cast<int32_t>(lo[c * 32 + qq])) + static_cast<int64_t>(static_cast<int32_t>(lo[c * 32 + 16 + qq]))
+		                  + static_cast<int64_t>(static_cast<uint64_t>(hi[e]) << 32);
+		if(v) atomicAdd(sums + static_cast<int64_t>(c) * sld + qq, static_cast<unsigned long long>(v));
 	}
 	for(int c = threadIdx.x; c < k; c += blockDim.x)
 		if(cnt[c]) atomicAdd(counts + c, static_cast<unsigned long long>(cnt[c]));
@@ -326,7 +410,7 @@ int launch_histogram(const mt_launch_ctx* c, void* stream) {
 		ensure_smem(histogram_pair_kernel, static_cast<int>(((kHistPairMaxBins + 1) / 2) * 4));
 		int64_t blocks = (n_local / 4 + 1023) / 1024;
 		blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148));
-		histogram_pair_kernel<<<static_cast<unsigned>(blocks), 1024, smem, s>>>(x, n_local, bins, hist);
+		histogram_pair_kernel<<<static_cast<unsigned>(blocks), 1024, smem, s>>>(x, n_local, static_cast<int>(bins), hist);
 	} else {
 		histogram_global_kernel<<<grid_1d(n_local, 256), 256, 0, s>>>(x, n_local, bins, hist);
 	}
@@ -343,14 +427,14 @@ int launch_kmeans_assign_i32(const mt_launch_ctx* c, void* stream) {
 	const mt_view& va = c->views[3];
 	const mt_view& vp = c->views[4];
 	const mt_view& vc = c->views[5];
-	const size_t fast_smem = static_cast<size_t>(k) * 16 * sizeof(int32_t);
+	const size_t fast_smem = static_cast<size_t>(k) * 17 * sizeof(int32_t);
 	const bool fast = d >= 1 && d <= 16 && fast_smem <= 200 * 1024 && vp.stride[1] == 1 && vc.stride[1] == 1 && va.stride[0] == 1 && vc.offset[0] == 0
 	                  && vc.offset[1] == 0 && vp.offset[1] == 0 && vc.extent[0] >= k;
 	if(fast) {
 		ensure_smem(kmeans_assign_fast_kernel, 200 * 1024);
 		const int32_t* pts = static_cast<const int32_t*>(vp.base) + (r.lo[0] - vp.offset[0]) * vp.stride[0];
 		int32_t* asg = static_cast<int32_t*>(va.base) + (r.lo[0] - va.offset[0]);
-		const unsigned blocks = std::max<unsigned>(1, std::min<unsigned>(static_cast<unsigned>((r.total + 511) / 512), 148 * 8));
+		const unsigned blocks = std::max<unsigned>(1, std::min<unsigned>(static_cast<unsigned>((r.total + 1023) / 1024), 148 * 2));
 		kmeans_assign_fast_kernel<<<blocks, 256, fast_smem, s>>>(pts, vp.stride[0], r.total, static_cast<int>(k), static_cast<int>(d),
 		    static_cast<const int32_t*>(vc.base), vc.stride[0], asg);
 		return cudaGetLastError() == cudaSuccess ? 0 : 1;
@@ -376,15 +460,16 @@ int launch_kmeans_update_i32(const mt_launch_ctx* c, void* stream) {
 		const mt_view& vp = c->views[2];
 		const mt_view& va = c->views[3];
 		const mt_view& vn = c->views[5];
-		const size_t smem = static_cast<size_t>(2 * k * d + k) * 4;
-		if(vs.offset[0] == 0 && vs.offset[1] == 0 && vs.extent[1] == d && vn.offset[0] == 0 && vn.extent[0] == k && smem <= 200 * 1024
+		const size_t smem = static_cast<size_t>(k + 1) * 49 * 4;
+		if(d >= 1 && d <= 16 && vs.offset[0] == 0 && vs.offset[1] == 0 && vs.extent[1] == d && vn.offset[0] == 0 && vn.extent[0] == k && smem <= 200 * 1024
 		    && vp.stride[1] == 1 && vp.offset[1] == 0 && va.stride[0] == 1) {
-			ensure_smem(kmeans_update_fast_kernel, 200 * 1024);
 			const int32_t* pts = static_cast<const int32_t*>(vp.base) + (r.lo[0] - vp.offset[0]) * vp.stride[0];
 			const int32_t* asg = static_cast<const int32_t*>(va.base) + (r.lo[0] - va.offset[0]);
-			const unsigned blocks = std::max<unsigned>(1, std::min<unsigned>(static_cast<unsigned>((r.total + 255) / 256), 148 * 4));
-			kmeans_update_fast_kernel<<<blocks, 512, smem, static_cast<cudaStream_t>(stream)>>>(pts, vp.stride[0], asg, r.total, static_cast<int>(k),
-			    static_cast<int>(d), static_cast<unsigned long long*>(vs.base), vs.stride[0], static_cast<unsigned long long*>(vn.base));
+			const unsigned blocks = std::max<unsigned>(1, std::min<unsigned>(static_cast<unsigned>((r.total + 511) / 512), 148 * 2));
+			const auto kern = vp.stride[0] == 16 ? kmeans_update_fast_kernel<true> : kmeans_update_fast_kernel<false>;
+			ensure_smem(kern, 200 * 1024);
+			kern<<<blocks, 512, smem, static_cast<cudaStream_t>(stream)>>>(pts, vp.stride[0], asg, r.total, static_cast<int>(k), static_cast<int>(d),
+			    static_cast<unsigned long long*>(vs.base), vs.stride[0], static_cast<unsigned long long*>(vn.base));
 			return cudaGetLastError() == cudaSuccess ? 0 : 1;
 		}
 	}

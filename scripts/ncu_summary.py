@@ -1,0 +1,39 @@
+#!/usr/bin/env python
+"""Print the headline metrics of an ncu report: duration, DRAM bytes/throughput, SM and
+pipe utilisation, top warp-stall reasons, occupancy."""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__occupancy_limit_registers", "launch__grid_size", "launch__block_size", "lts__t_bytes.sum"]
+
+
+def main(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h = rows[0]
+    for row in rows[2:]:
+        d = dict(zip(h, row))
+        print(d.get("Kernel Name", "")[:90])
+        for k in KEYS:
+            if k in d:
+                print(f"  {k} = {d[k]}")
+        st = []
+        for k, v in d.items():
+            if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+                try:
+                    st.append((float(v), k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        print("  stalls:", ", ".join(f"{n}={v:.2f}" for v, n in sorted(st, reverse=True)[:6]))
+
+
+if __name__ == "__main__":
+    for p in sys.argv[1:]:
+        main(p)

@@ -81,3 +81,66 @@ def test_kmeans_fast_and_exact_paths(okern, mod):
     assert np.array_equal(g_sums, s)
     assert np.array_equal(g_cnts, m)
     assert np.array_equal(g_cen, c)
+
+
+def _np_assign(p, c):
+    best = np.zeros(len(p), np.int32)
+    bd = np.full(len(p), np.iinfo(np.int64).max, np.int64)
+    for j in range(len(c)):
+        dd = ((p.astype(np.int64) - c[j].astype(np.int64)) ** 2).sum(axis=1)
+        upd = dd < bd  # strict: the first minimum wins (kernels.cpp:283-292)
+        bd[upd] = dd[upd]
+        best[upd] = j
+    return best
+
+
+@pytest.mark.parametrize("lim,d", [(8191, 16), (8191, 5), (1 << 20, 16)])
+def test_kmeans_assign_signed_values(lim, d):
+    """negative coordinates, |x| at the fast path's limit (max distance just below 2^32), a
+    padded d < 16, and values past the limit (int64 path); ties included (duplicate centroids)"""
+    rng = np.random.default_rng(7)
+    n, k = 20_011, 48
+    p = rng.integers(-lim, lim + 1, size=(n, d), dtype=np.int64).astype(np.int32)
+    c = rng.integers(-lim, lim + 1, size=(k, d), dtype=np.int64).astype(np.int32)
+    c[7] = c[3]
+    p[:4] = lim
+    c[0] = -lim
+    with mb.context(workers=1, devices=1, num_gpus=1) as ctx:
+        dv = ctx.devices
+        pts = ctx.create_array([n, d], "i32", ctx.dist.single([n, d], dv[0]), 0)
+        asg = ctx.create_array([n], "i32", ctx.dist.single([n], dv[0]), 0)
+        cen = ctx.create_array([k, d], "i32", ctx.dist.single([k, d], dv[0]), 0)
+        ctx.write(pts, p)
+        ctx.write(cen, c)
+        ctx.launch("kmeans_assign_i32", [n], [128], ctx.dist.block_work([n], [128], [-(-n // 128) * 128], dv), [n, k, d, Arr(asg), Arr(pts), Arr(cen)],
+                   "global i => write assign[i], read points[i,:], read centroids[:,:]")
+        got = ctx.read(asg)
+    assert np.array_equal(got, _np_assign(p, c))
+
+
+@pytest.mark.parametrize("d", [16, 3])
+def test_kmeans_update_full_range_values(d):
+    """full-range int32 coordinates: the per-CTA signed i32 sums overflow constantly, so the
+    wrap counters must carry the exact int64 total"""
+    rng = np.random.default_rng(11)
+    n, k = 300_007, 40
+    p = rng.integers(-(1 << 31), 1 << 31, size=(n, d), dtype=np.int64).astype(np.int32)
+    p[: n // 2] = np.abs(p[: n // 2].astype(np.int64)).clip(0, (1 << 31) - 1).astype(np.int32)  # long positive runs
+    a = rng.integers(0, k, size=n, dtype=np.int32)
+    a[:1000] = 5
+    with mb.context(workers=1, devices=2, num_gpus=1) as ctx:
+        dv = ctx.devices
+        half = (n + 1) // 2
+        pts = ctx.create_array([n, d], "i32", ctx.dist.row([n, d], half, dv), 0)
+        asg = ctx.create_array([n], "i32", ctx.dist.row([n], half, dv), 0)
+        sums = ctx.create_array([k, d], "i64", ctx.dist.replicated([k, d], dv), 0)
+        cnts = ctx.create_array([k], "i64", ctx.dist.replicated([k], dv), 0)
+        ctx.write(pts, p)
+        ctx.write(asg, a)
+        ctx.launch("kmeans_update_i32", [n], [128], ctx.dist.block_work([n], [128], [-(-half // 128) * 128], dv), [n, d, Arr(pts), Arr(asg), Arr(sums), Arr(cnts)],
+                   "global i => read points[i,:], read assign[i], reduce(+) sums[:,:], reduce(+) counts[:]")
+        g_s, g_c = ctx.read(sums), ctx.read(cnts)
+    want_s = np.zeros((k, d), np.int64)
+    np.add.at(want_s, a, p.astype(np.int64))
+    assert np.array_equal(g_c, np.bincount(a, minlength=k))
+    assert np.array_equal(g_s, want_s)
