@@ -54,6 +54,10 @@ enum mt_task_kind {
 	MT_TASK_SEND = 4,
 	MT_TASK_RECV = 5,
 	MT_TASK_REDUCE = 6,
+	/* B200 extension (cfg.collective_reduce): one per worker, in place on `output`; the
+	 * group is `tag`, its data-carrying members are `inputs` in worker order (a worker
+	 * without a partial joins with an identity-filled buffer and is not in `inputs`) */
+	MT_TASK_ALLREDUCE = 7,
 };
 enum mt_fill_kind { MT_FILL_NONE = 0, MT_FILL_ZERO = 1, MT_FILL_ONE = 2, MT_FILL_IDENTITY = 3 };
 enum mt_reduce_op { MT_RED_PLUS = 0, MT_RED_TIMES = 1, MT_RED_MIN = 2, MT_RED_MAX = 3 };
@@ -101,6 +105,7 @@ typedef struct mt_arg_binding {
  *   copy   : src, dst, src_region, dst_region
  *   send   : chunk, region, peer, tag          recv: chunk, region, peer, tag
  *   reduce : op, inputs, output
+ *   allreduce: op, inputs (group members with data), output (this worker's member), tag (group)
  */
 typedef struct mt_task {
 	int64_t id;
@@ -163,6 +168,11 @@ typedef struct mt_config {
 	int32_t lookahead_tasks;        /* spill tier: tasks buffered ahead for Belady eviction (0 = 512) */
 	int32_t worker_rank;            /* with single_worker: the worker this process executes */
 	int32_t gpu_base;               /* with single_worker: CUDA ordinal of this process's first GPU */
+	int32_t collective_reduce;      /* 1: cross-worker reduce trees become one allreduce per worker
+	                                   (NCCL between processes, a peer-memory combine in one process)
+	                                   instead of send-to-root / root reduce / send-back
+	                                   (planner.cpp:389-517); 0: the reference's tree */
+	int32_t pad_;
 } mt_config;
 
 /* One planned chunk access (a create counts as a write of the whole chunk). */
@@ -234,6 +244,13 @@ mt_exec* mt_ctx_exec(mt_ctx* ctx);
  * GPU-driven NVLink rings with no host involvement. Barrier before destroying contexts. */
 int mt_ctx_peer_export(mt_ctx* ctx, void* buf, int64_t cap, int64_t* len);
 int mt_ctx_peer_import(mt_ctx* ctx, const void* blobs, int64_t blob_len, int32_t nblobs);
+/* NCCL communicator for allreduce tasks between processes (cfg.collective_reduce with
+ * cfg.single_worker; the reduce tree as ncclAllReduce over the partial box).
+ * Rank 0 creates the 128-byte unique id, it is broadcast out of band, then every rank calls
+ * mt_ctx_nccl_init collectively (rank = worker_rank, nranks = workers). `nccl_lib` is the
+ * libnccl.so.2 to load when none is loaded in the process yet (NULL: the default search). */
+int mt_ctx_nccl_unique_id(mt_ctx* ctx, const char* nccl_lib, void* id128);
+int mt_ctx_nccl_init(mt_ctx* ctx, const char* nccl_lib, const void* id128);
 
 /* ---- executor alone: drop-in for manta::system_runtime ------------------------------ */
 int mt_exec_create(const mt_config* cfg, mt_exec** out);

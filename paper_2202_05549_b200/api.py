@@ -12,6 +12,7 @@ work happens behind the C-ABI of include/manta_b200.h; this module only marshals
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
@@ -152,6 +153,9 @@ def _task_dict(t: capi.Task, pool, args) -> dict:
         d.update(chunk=t.chunk, region=t.region.box(), peer=t.peer, tag=t.tag)
     elif k == capi.REDUCE:
         d.update(op=t.op, inputs=[pool[t.inputs_off + i] for i in range(t.ninputs)], output=t.output)
+    elif k == capi.ALLREDUCE:
+        d.update(op=t.op, inputs=[pool[t.inputs_off + i] for i in range(t.ninputs)], output=t.output, tag=t.tag, region=t.region.box(),
+                 dtype=t.dtype)
     return d
 
 
@@ -168,12 +172,22 @@ class PlanBuffer:
         return [_task_dict(t, self.pool, self.args) for t in self.tasks]
 
 
+def _nccl_library():
+    """torch's bundled libnccl.so.2 (the one torch.distributed uses), else None (default search)"""
+    try:
+        import nvidia.nccl
+        path = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        return path.encode() if os.path.exists(path) else None
+    except ImportError:
+        return None
+
+
 class Context:
     """driver + executor over one library (product `mt_` or oracle shim `mr_`)."""
 
     def __init__(self, lib: capi.Lib, workers=1, devices=1, execute=True, compat_deps=False, suppress_conflict_deps=False,
                  num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0, record_accesses=False,
-                 lookahead_tasks=0, worker_rank=None, gpu_base=0):
+                 lookahead_tasks=0, worker_rank=None, gpu_base=0, collective_reduce=False):
         self.lib = lib
         self.dist = Distributions(lib)
         cfg = capi.Config()
@@ -188,8 +202,11 @@ class Context:
         cfg.staging_threshold = staging_threshold
         cfg.record_accesses = int(record_accesses)
         cfg.lookahead_tasks = int(lookahead_tasks)
+        cfg.collective_reduce = int(collective_reduce)
         if worker_rank is not None:  # one process per worker
             cfg.single_worker, cfg.worker_rank, cfg.gpu_base = 1, int(worker_rank), int(gpu_base)
+        self.single_worker = worker_rank is not None
+        self.collective_reduce = bool(collective_reduce)
         h = C.c_void_p()
         lib.check(lib.ctx_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -349,12 +366,22 @@ class Context:
         self.lib.check(self.lib.ctx_peer_import(self.h, data, size, len(blobs)))
 
     def connect_peers(self, group=None):
-        """Exchange mailboxes with every rank of the torch.distributed group and map them."""
+        """Exchange mailboxes with every rank of the torch.distributed group and map them; with
+        collective_reduce also create the NCCL communicator the allreduce tasks run on."""
         import torch.distributed as dist
         mine = self.peer_export()
         blobs = [None] * dist.get_world_size(group)
         dist.all_gather_object(blobs, mine, group=group)
         self.peer_import(blobs)
+        if self.collective_reduce and self.single_worker:
+            lib = _nccl_library()
+            ident = [None]
+            if dist.get_rank(group) == 0:
+                buf = C.create_string_buffer(128)
+                self.lib.check(self.lib.ctx_nccl_unique_id(self.h, lib, buf))
+                ident[0] = buf.raw
+            dist.broadcast_object_list(ident, src=0, group=group)
+            self.lib.check(self.lib.ctx_nccl_init(self.h, lib, ident[0]))
 
     # -- device timing (bench) ------------------------------------------------------
     def _ex(self):

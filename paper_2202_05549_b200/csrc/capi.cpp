@@ -129,6 +129,11 @@ void flatten(const task& t, mt_task& o, std::vector<int64_t>& pool, std::vector<
 		o.peer = t.peer;
 		o.tag = t.tag;
 		break;
+	case task_kind::allreduce:
+		o.region = from_box(t.region);
+		o.dtype = static_cast<int32_t>(t.type);
+		o.tag = t.tag;
+		[[fallthrough]];
 	case task_kind::reduce:
 		o.op = static_cast<int32_t>(t.op);
 		o.inputs_off = static_cast<int64_t>(pool.size());
@@ -143,7 +148,7 @@ task unflatten(const mt_task& o, const int64_t* pool, const mt_arg_binding* args
 	task t;
 	t.id = o.id;
 	t.worker = o.worker;
-	if(o.kind < 0 || o.kind > MT_TASK_REDUCE) throw validation_error("bad task kind");
+	if(o.kind < 0 || o.kind > MT_TASK_ALLREDUCE) throw validation_error("bad task kind");
 	t.kind = static_cast<task_kind>(o.kind);
 	t.resource = to_dev(o.resource);
 	for(int64_t i = 0; i < o.ndeps; ++i) t.deps.push_back(pool[o.deps_off + i]);
@@ -184,6 +189,11 @@ task unflatten(const mt_task& o, const int64_t* pool, const mt_arg_binding* args
 		t.peer = o.peer;
 		t.tag = o.tag;
 		break;
+	case task_kind::allreduce:
+		t.region = to_box(o.region);
+		t.type = to_dtype(o.dtype);
+		t.tag = o.tag;
+		[[fallthrough]];
 	case task_kind::reduce:
 		t.op = static_cast<reduce_op>(o.op);
 		for(int64_t i = 0; i < o.ninputs; ++i) t.inputs.push_back(pool[o.inputs_off + i]);
@@ -293,6 +303,7 @@ int mt_ctx_create(const mt_config* cfg, mt_ctx** out) {
 		pc.suppress_conflict_deps = cfg->suppress_conflict_deps != 0;
 		pc.compat_deps = cfg->compat_deps != 0;
 		pc.record_accesses = cfg->record_accesses != 0;
+		pc.collective_reduce = cfg->collective_reduce != 0;
 		ctx->plan = std::make_unique<planner>(pc);
 		if(cfg->execute) {
 			ctx->exec = std::make_unique<mt_exec>();
@@ -534,6 +545,17 @@ int mt_ctx_peer_import(mt_ctx* ctx, const void* blobs, int64_t blob_len, int32_t
 		const auto* p = static_cast<const uint8_t*>(blobs);
 		for(int32_t i = 0; i < nblobs; ++i) v.emplace_back(p + i * blob_len, p + (i + 1) * blob_len);
 		e.ex->peer_import(v);
+	});
+}
+
+int mt_ctx_nccl_unique_id(mt_ctx* ctx, const char* nccl_lib, void* id128) {
+	return guarded([&] { need_exec(ctx).ex->nccl_unique_id(nccl_lib, id128); });
+}
+
+int mt_ctx_nccl_init(mt_ctx* ctx, const char* nccl_lib, const void* id128) {
+	return guarded([&] {
+		if(!ctx->cfg.single_worker) throw validation_error("an NCCL communicator is only used with single_worker (one process per worker)");
+		need_exec(ctx).ex->nccl_init(nccl_lib, id128, ctx->cfg.workers, ctx->cfg.worker_rank);
 	});
 }
 

@@ -1,5 +1,8 @@
 #include "executor.hpp"
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -7,6 +10,22 @@
 #include <sstream>
 
 namespace mtb {
+
+namespace {
+struct nccl_fns {
+	ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+	ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+	ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+	ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+	const char* (*error_string)(ncclResult_t) = nullptr;
+};
+nccl_fns g_nccl;
+
+void nccl_check(ncclResult_t r, const char* what) {
+	if(r != ncclSuccess)
+		throw execution_error(std::string(what) + " failed: " + (g_nccl.error_string ? g_nccl.error_string(r) : std::to_string(static_cast<int>(r))));
+}
+} // namespace
 
 void check_cuda(cudaError_t e, const char* what) {
 	if(e != cudaSuccess) throw execution_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -316,6 +335,7 @@ executor::~executor() {
 		cudaSetDevice(G.ordinal);
 		cudaDeviceSynchronize();
 	}
+	if(nccl_comm_ && g_nccl.comm_destroy) g_nccl.comm_destroy(static_cast<ncclComm_t>(nccl_comm_));
 	// peers must have stopped writing into our mailbox (callers barrier before teardown)
 	for(void* p : opened_) cudaIpcCloseMemHandle(p);
 	if(mbox_) cudaFree(mbox_);
@@ -457,6 +477,7 @@ void executor::issue(const task& t) {
 	case task_kind::send: run_send(t); break;
 	case task_kind::recv: run_recv(t); break;
 	case task_kind::reduce: run_reduce(t); break;
+	case task_kind::allreduce: run_allreduce(t); break;
 	}
 	if(spill_) note_use(t);
 }
@@ -497,6 +518,16 @@ void executor::used_chunks(const task& t, std::vector<std::pair<int64_t, bool>>&
 		for(const auto c : t.inputs) out.emplace_back(c, false);
 		out.emplace_back(t.output, true);
 		break;
+	case task_kind::allreduce: {
+		// the last local member combines every member: keep them all resident
+		for(const auto c : t.inputs)
+			if(bufs_.count(c)) out.emplace_back(c, false);
+		const auto g = groups_.find(t.tag);
+		if(g != groups_.end())
+			for(const auto c : g->second.outputs) out.emplace_back(c, true);
+		out.emplace_back(t.output, true);
+		break;
+	}
 	}
 }
 
@@ -530,6 +561,11 @@ void executor::accesses_of(const task& t, std::vector<access_t>& out) const {
 	case task_kind::reduce:
 		for(const auto c : t.inputs) out.push_back({c, full(c), true, false, false});
 		out.push_back({t.output, full(t.output), false, true, false});
+		break;
+	case task_kind::allreduce:
+		for(const auto c : t.inputs)
+			if(c != t.output && bufs_.count(c)) out.push_back({c, full(c), true, false, false});
+		out.push_back({t.output, full(t.output), true, false, false}); // in place: read and written
 		break;
 	}
 }
@@ -962,22 +998,144 @@ void executor::run_reduce(const task& t) {
 	finish(t, s);
 }
 
+// ---- allreduce (collective reduce trees) ------------------------------------------------------
+//
+// The reference reduces every worker's partial at the root w0d0 and sends the total back
+// (planner.cpp:389-517). With cfg.collective_reduce the planner emits one allreduce task per
+// worker instead. Between processes it is one ncclAllReduce in place on the member buffer
+// (NVLink / NVLS inside NCCL; float sums in NCCL's order, within the reductions tolerance). In
+// one process the members are issued in worker order and the last one combines them with the
+// reduce kernel in the reference's root order, so the result is bit-identical to the tree.
+
+void executor::finish_id(int64_t id, cudaStream_t s, int gpu) {
+	cudaEvent_t ev = take_event(gpu);
+	check_cuda(cudaEventRecord(ev, s), "cudaEventRecord");
+	done_[id] = {ev, s, gpu};
+	tail_[s] = id;
+	++ctr_.tasks;
+}
+
+
+void executor::nccl_load(const char* lib) {
+	if(nccl_dl_) return;
+	void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD); // e.g. torch.distributed's copy
+	if(!h && lib && *lib) h = dlopen(lib, RTLD_NOW);
+	if(!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+	if(!h) throw execution_error(std::string("cannot load libnccl.so.2: ") + dlerror());
+	const auto sym = [&](const char* name) {
+		void* f = dlsym(h, name);
+		if(!f) throw execution_error(std::string("libnccl lacks ") + name);
+		return f;
+	};
+	g_nccl.get_unique_id = reinterpret_cast<decltype(g_nccl.get_unique_id)>(sym("ncclGetUniqueId"));
+	g_nccl.comm_init_rank = reinterpret_cast<decltype(g_nccl.comm_init_rank)>(sym("ncclCommInitRank"));
+	g_nccl.all_reduce = reinterpret_cast<decltype(g_nccl.all_reduce)>(sym("ncclAllReduce"));
+	g_nccl.comm_destroy = reinterpret_cast<decltype(g_nccl.comm_destroy)>(sym("ncclCommDestroy"));
+	g_nccl.error_string = reinterpret_cast<decltype(g_nccl.error_string)>(sym("ncclGetErrorString"));
+	nccl_dl_ = h;
+}
+
+void executor::nccl_unique_id(const char* lib, void* id128) {
+	nccl_load(lib);
+	ncclUniqueId id;
+	nccl_check(g_nccl.get_unique_id(&id), "ncclGetUniqueId");
+	static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+	std::memcpy(id128, &id, sizeof(id));
+}
+
+void executor::nccl_init(const char* lib, const void* id128, int nranks, int rank) {
+	nccl_load(lib);
+	if(nccl_comm_) throw validation_error("the NCCL communicator is already initialised");
+	ncclUniqueId id;
+	std::memcpy(&id, id128, sizeof(id));
+	check_cuda(cudaSetDevice(gpus_.at(0).ordinal), "cudaSetDevice");
+	ncclComm_t comm = nullptr;
+	nccl_check(g_nccl.comm_init_rank(&comm, nranks, id, rank), "ncclCommInitRank");
+	nccl_comm_ = comm;
+}
+
+void executor::run_allreduce(const task& t) {
+	ldev& L = dev(t.resource);
+	cudaStream_t s = pick_compute(t, L);
+	wait_deps(t, s);
+	const buffer& out = buf(t.output);
+	const uint64_t count = static_cast<uint64_t>(out.region.volume());
+	if(cfg_.local_workers >= 0 && cfg_.local_workers < cfg_.workers) {
+		if(cfg_.local_workers != 1) throw execution_error("an allreduce across processes needs one worker per process");
+		if(!nccl_comm_) throw execution_error("allreduce task but no NCCL communicator (mt_ctx_nccl_init / Context.connect_peers)");
+		ncclDataType_t dt = ncclFloat32;
+		switch(out.type) {
+		case dtype::i32: dt = ncclInt32; break;
+		case dtype::i64: dt = ncclInt64; break;
+		case dtype::f32: dt = ncclFloat32; break;
+		case dtype::f64: dt = ncclFloat64; break;
+		case dtype::bf16: dt = ncclBfloat16; break;
+		}
+		ncclRedOp_t op = ncclSum;
+		switch(t.op) {
+		case reduce_op::plus: op = ncclSum; break;
+		case reduce_op::times: op = ncclProd; break;
+		case reduce_op::min: op = ncclMin; break;
+		case reduce_op::max: op = ncclMax; break;
+		}
+		nccl_check(g_nccl.all_reduce(out.ptr, out.ptr, count, dt, op, static_cast<ncclComm_t>(nccl_comm_), s), "ncclAllReduce");
+		ctr_.bytes_sent += count * dtype_size(out.type);
+		finish(t, s);
+		return;
+	}
+	auto& g = groups_[t.tag];
+	g.tasks.push_back(t.id);
+	g.outputs.push_back(t.output);
+	if(static_cast<int>(g.tasks.size()) < cfg_.workers) {
+		cudaEvent_t ev = take_event(L.gpu);
+		check_cuda(cudaEventRecord(ev, s), "cudaEventRecord");
+		g.ready.emplace_back(ev, L.gpu);
+		return; // completes when the last member has combined the group
+	}
+	for(const auto& [ev, gi] : g.ready) check_cuda(cudaStreamWaitEvent(s, ev, 0), "cudaStreamWaitEvent");
+	const uint64_t bytes = count * dtype_size(out.type);
+	std::vector<const void*> ins;
+	for(const auto c : t.inputs) {
+		const buffer& b = buf(c);
+		if(b.region != out.region) throw execution_error("allreduce members cover different regions");
+		ins.push_back(b.ptr);
+	}
+	if(!ins.empty() && bytes > 0) {
+		void* total = nullptr;
+		check_cuda(cudaMallocFromPoolAsync(&total, bytes, gpus_[static_cast<size_t>(L.gpu)].pool, s), "cudaMallocFromPoolAsync");
+		device_reduce(total, ins.data(), static_cast<int>(ins.size()), count, out.type, t.op, s);
+		++ctr_.kernels;
+		for(const auto o : g.outputs) {
+			const buffer& b = buf(o);
+			if(b.gpu == L.gpu)
+				check_cuda(cudaMemcpyAsync(b.ptr, total, bytes, cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync");
+			else
+				check_cuda(cudaMemcpyPeerAsync(b.ptr, ord(b.gpu), total, ord(L.gpu), bytes, s), "cudaMemcpyPeerAsync");
+		}
+		check_cuda(cudaFreeAsync(total, s), "cudaFreeAsync");
+	}
+	for(const auto& [ev, gi] : g.ready) free_events_[static_cast<size_t>(gi)].push_back(ev);
+	for(const auto id : g.tasks) finish_id(id, s, L.gpu);
+	groups_.erase(t.tag);
+}
+
 void executor::mark(int slot) {
 	if(slot < 0 || slot > 1) throw validation_error("mark slot must be 0 or 1");
 	drain(true);
-	for(auto& G : gpus_) {
+	for(size_t g = 0; g < gpus_.size(); ++g) {
+		auto& G = gpus_[g];
 		check_cuda(cudaSetDevice(G.ordinal), "cudaSetDevice");
 		for(const auto& [s, tail] : tail_) {
 			const auto it = done_.find(tail);
-			if(it == done_.end() || it->second.gpu != G.ordinal) continue;
+			if(it == done_.end() || it->second.gpu != static_cast<int>(g)) continue; // done_ev.gpu is the executor GPU index
 			check_cuda(cudaStreamWaitEvent(G.timing, it->second.ev, 0), "cudaStreamWaitEvent");
 		}
 		// spill-tier transfers are not tasks: join their streams explicitly
 		for(cudaStream_t s : {G.h2d, G.d2h}) {
-			cudaEvent_t e = take_event(G.ordinal);
+			cudaEvent_t e = take_event(static_cast<int>(g));
 			check_cuda(cudaEventRecord(e, s), "cudaEventRecord");
 			check_cuda(cudaStreamWaitEvent(G.timing, e, 0), "cudaStreamWaitEvent");
-			free_events_[static_cast<size_t>(G.ordinal)].push_back(e);
+			free_events_[g].push_back(e);
 		}
 		check_cuda(cudaEventRecord(G.marks[slot], G.timing), "cudaEventRecord");
 	}

@@ -94,6 +94,11 @@ class executor {
 	// peer worker runs in another process. Every rank exports one IPC-mapped mailbox (a ring of
 	// kSlots x kSlotBytes per source rank, ready flags, consumption counters); after the blobs
 	// are exchanged out of band (torch.distributed), each rank maps every peer's mailbox.
+	// allreduce tasks between processes run on an NCCL communicator (libnccl loaded at run
+	// time: the one already in the process, else `lib`, else the default search path)
+	void nccl_unique_id(const char* lib, void* id128);
+	void nccl_init(const char* lib, const void* id128, int nranks, int rank);
+
 	std::vector<uint8_t> peer_export();
 	void peer_import(const std::vector<std::vector<uint8_t>>& blobs);
 	static constexpr int kSlots = 4;
@@ -229,6 +234,19 @@ class executor {
 	void run_send(const task& t);
 	void run_recv(const task& t);
 	void run_reduce(const task& t);
+	void run_allreduce(const task& t);
+	void finish_id(int64_t id, cudaStream_t s, int gpu);
+
+	// in-process allreduce groups: members issue in worker order, the last one combines
+	struct coll_group {
+		std::vector<int64_t> tasks;
+		std::vector<int64_t> outputs;
+		std::vector<std::pair<cudaEvent_t, int>> ready; // (event, gpu index)
+	};
+	std::map<uint64_t, coll_group> groups_;
+	void* nccl_dl_ = nullptr;
+	void* nccl_comm_ = nullptr;
+	void nccl_load(const char* lib);
 };
 
 // region copy helpers (rank <= 3, row-major chunks); enqueue on `s`. A gpu index of -1 marks

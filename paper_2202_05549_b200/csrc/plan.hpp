@@ -13,7 +13,7 @@ struct kernel_entry;
 
 namespace mtb {
 
-enum class task_kind : int32_t { create = 0, del = 1, execute = 2, copy = 3, send = 4, recv = 5, reduce = 6 };
+enum class task_kind : int32_t { create = 0, del = 1, execute = 2, copy = 3, send = 4, recv = 5, reduce = 6, allreduce = 7 };
 enum class fill_kind : int32_t { none = 0, zero = 1, one = 2, identity = 3 };
 enum class arg_kind : int32_t { scalar_int = 0, scalar_float = 1, chunk = 2, none = 3 };
 
@@ -54,7 +54,7 @@ struct task {
 	// send / recv
 	int peer = -1;
 	uint64_t tag = 0;
-	// reduce
+	// reduce / allreduce (group = tag, members with data = inputs, own member = output)
 	reduce_op op = reduce_op::plus;
 	std::vector<int64_t> inputs;
 	int64_t output = -1;
@@ -69,6 +69,7 @@ inline const char* task_kind_name(task_kind k) {
 	case task_kind::send: return "send";
 	case task_kind::recv: return "recv";
 	case task_kind::reduce: return "reduce";
+	case task_kind::allreduce: return "allreduce";
 	}
 	return "?";
 }

@@ -493,6 +493,65 @@ std::pair<int64_t, int64_t> planner::launch(const std::string& kernel, const box
 		std::map<int, partial> worker_result;
 		for(const auto& [w, res] : by_worker) worker_result[w] = res.size() == 1 ? res[0] : emit_reduce(w, chunk(res[0].chunk).desc.home, res);
 
+		if(cfg_.collective_reduce && cfg_.workers > 1) {
+			// every worker joins one allreduce group, in place on its worker result (an
+			// identity-filled box for a worker without partials), then copies the total into
+			// its own destination chunks; members with data are listed in worker order, the
+			// order of the reference's root reduce, so an in-process combine is bit-identical
+			std::vector<partial> member(static_cast<size_t>(cfg_.workers));
+			std::vector<int64_t> data;
+			for(int w = 0; w < cfg_.workers; ++w) {
+				const auto it = worker_result.find(w);
+				if(it != worker_result.end()) {
+					member[static_cast<size_t>(w)] = it->second;
+					data.push_back(it->second.chunk);
+					continue;
+				}
+				const device_id home{w, 0};
+				const int64_t filler = new_temp(b, home, type);
+				temps.push_back(filler);
+				const int64_t create = emit_create(w, home, filler, fill_kind::identity, op);
+				touch(filler, create);
+				member[static_cast<size_t>(w)] = {filler, create};
+			}
+			const uint64_t group = collectives_++;
+			std::vector<int64_t> ar(static_cast<size_t>(cfg_.workers));
+			for(int w = 0; w < cfg_.workers; ++w) {
+				const partial& m = member[static_cast<size_t>(w)];
+				task r;
+				r.worker = w;
+				r.resource = chunk(m.chunk).desc.home;
+				r.kind = task_kind::allreduce;
+				r.op = op;
+				r.tag = group;
+				r.inputs = data;
+				r.output = m.chunk;
+				r.type = type;
+				r.region = b;
+				r.deps.push_back(m.producer);
+				ar[static_cast<size_t>(w)] = emit(std::move(r));
+				touch(m.chunk, ar[static_cast<size_t>(w)]);
+			}
+			h.index.query(b, cand);
+			for(const int t : cand) {
+				const auto& target = h.chunks[static_cast<size_t>(t)];
+				const int w = target.home.worker;
+				transfer(member[static_cast<size_t>(w)].chunk, target.id, intersect(target.region, b), {ar[static_cast<size_t>(w)]}, {});
+			}
+			for(const int64_t id : temps) {
+				const auto& m = chunk(id);
+				task d;
+				d.worker = m.desc.home.worker;
+				d.resource = m.desc.home;
+				d.kind = task_kind::del;
+				d.deps = temp_users_.at(id);
+				d.chunk = id;
+				emit(std::move(d));
+				temp_users_.erase(id);
+			}
+			continue;
+		}
+
 		const device_id root{0, 0};
 		std::vector<int64_t> final_inputs, final_deps;
 		for(const auto& [w, res] : worker_result) {

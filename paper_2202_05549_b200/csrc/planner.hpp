@@ -25,6 +25,9 @@ struct planner_config {
 	bool compat_deps = false;
 	bool retain_plan = true; // keep every emitted task for mt_plan_export
 	bool record_accesses = false;
+	// cross-worker reduce trees as one allreduce task per worker (B200 extension; the
+	// default keeps the reference's send-to-root tree, planner.cpp:389-517)
+	bool collective_reduce = false;
 };
 
 struct launch_arg {
@@ -89,6 +92,7 @@ class planner {
 	std::vector<int> task_worker_;
 	std::vector<task> plan_, pending_;
 	std::map<std::pair<int, int>, uint64_t> tags_;
+	uint64_t collectives_ = 0; // allreduce group ids, in plan order
 	std::unordered_map<int64_t, std::vector<int64_t>> temp_users_;
 	std::vector<std::unique_ptr<kernel_entry>> local_kernels_;
 	std::vector<access_rec> accesses_;

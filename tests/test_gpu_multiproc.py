@@ -119,3 +119,60 @@ def test_two_process_reduce_tree(okern):
     okern.oracle_histogram_hashed(C.c_int64(0), C.c_int64(n), C.c_int64(bins), C.c_int64(5), want.ctypes.data_as(C.POINTER(C.c_int64)))
     for _, h in res:
         assert np.array_equal(h, want)
+
+
+def _coll_rank(rank, world, port, n, bins, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+    ctx = mb.context(workers=world, devices=1, worker_rank=rank, gpu_base=0, collective_reduce=True)
+    try:
+        ctx.connect_peers()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, "error", str(e)))
+        dist.barrier()
+        ctx.close()
+        dist.destroy_process_group()
+        return
+    devs = ctx.devices
+    per = n // world
+    x = ctx.create_array([n], "i32", ctx.dist.row([n], per, devs), 0)
+    h = ctx.create_array([bins], "i64", ctx.dist.replicated([bins], devs), 0)
+    w = ctx.dist.block_work([n], [128], [per], devs)
+    ctx.launch("hpattern1d", [n], [128], w, [n, bins, 5, Arr(x)], "global i => write out[i]")
+    ctx.launch("histogram", [n], [128], w, [n, bins, Arr(x), Arr(h)], "global i => read x[i], reduce(+) hist[:]")
+    ctx.synchronize()
+    q.put((rank, "ok", ctx.read(h)))
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_two_process_nccl_allreduce(okern):
+    """the reduce tree as ncclAllReduce between processes; NCCL refuses two ranks on one GPU,
+    so on a single-GPU box this reports a skip (the in-process combine is covered by
+    test_collective_reduce.py, the group ordering across ranks by test_multiproc.py)"""
+    import ctypes as C
+    n, bins, world = 1 << 20, 1000, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_coll_rank, args=(r, world, port, n, bins, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    errs = [r[2] for r in res if r[1] == "error"]
+    if errs:
+        import torch
+        if torch.cuda.device_count() < world:
+            pytest.skip(f"NCCL needs {world} GPUs: {errs[0][:200]}")
+        raise AssertionError(errs)
+    want = np.empty(bins, np.int64)
+    okern.oracle_histogram_hashed(C.c_int64(0), C.c_int64(n), C.c_int64(bins), C.c_int64(5), want.ctypes.data_as(C.POINTER(C.c_int64)))
+    for _, _, h in res:
+        assert np.array_equal(h, want)
