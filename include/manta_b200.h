@@ -264,7 +264,8 @@ int mt_exec_write_chunk(mt_exec* ex, int64_t chunk, const void* src, uint64_t by
 int mt_exec_report_json(mt_exec* ex, char* buf, int64_t cap, int64_t* len);
 
 /* counters: tasks, device launches, copies, bytes copied, bytes sent, bytes received, peak
- * device bytes, evictions, spill bytes D2H, spill bytes H2D (first n of them) */
+ * device bytes, evictions, spill bytes D2H, spill bytes H2D, dead drops (evictions without
+ * write-back), dead skips (restores without H2D), host reclaims (first n of them) */
 int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n);
 /* cudaStream_t of the most recent execute task (for event timing on the launching stream) */
 void* mt_exec_last_stream(mt_exec* ex);

@@ -345,7 +345,7 @@ class Context:
         if not ex or not self.lib.has("exec_stats"):
             return {}
         keys = ["tasks", "kernels", "copies", "bytes_copied", "bytes_sent", "bytes_received", "peak_device_bytes", "evictions",
-                "spill_bytes_d2h", "spill_bytes_h2d", "dead_drops", "dead_skips"]
+                "spill_bytes_d2h", "spill_bytes_h2d", "dead_drops", "dead_skips", "host_reclaims"]
         out = (C.c_uint64 * len(keys))()
         self.lib.check(self.lib.exec_stats(ex, out, len(keys)))
         return dict(zip(keys, [int(v) for v in out]))

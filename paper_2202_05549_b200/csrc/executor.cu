@@ -639,7 +639,7 @@ void executor::alloc_wait(int gpu, cudaStream_t s) {
 	if(cudaEvent_t e = alloc_event(gpu)) check_cuda(cudaStreamWaitEvent(s, e, 0), "cudaStreamWaitEvent");
 }
 
-void* executor::host_alloc(uint64_t bytes, int gpu) {
+void* executor::host_alloc(uint64_t bytes, int gpu, int64_t exclude) {
 	auto it = host_free_.find(bytes);
 	if(it != host_free_.end()) {
 		auto [p, ev] = it->second;
@@ -651,8 +651,38 @@ void* executor::host_alloc(uint64_t bytes, int gpu) {
 		}
 		return p;
 	}
-	if(host_used_ + bytes > cfg_.host_capacity)
-		throw execution_error("host tier exhausted: " + std::to_string(host_used_ + bytes) + " bytes needed, capacity " + std::to_string(cfg_.host_capacity));
+	// over capacity: take back host copies of chunks that are resident again — stale ones
+	// (written since) first, then clean ones (their next eviction writes back again)
+	while(host_used_ + bytes > cfg_.host_capacity) {
+		buffer* pick = nullptr;
+		for(auto& [id, b] : bufs_) {
+			if(id == exclude || !b.ptr || !b.host) continue;
+			const bool better = !pick || (pick->host_valid && !b.host_valid) || (pick->host_valid == b.host_valid && (pick->bytes != bytes && b.bytes == bytes));
+			if(better) pick = &b;
+		}
+		if(!pick)
+			throw execution_error("host tier exhausted: " + std::to_string(host_used_ + bytes) + " bytes needed, capacity " + std::to_string(cfg_.host_capacity));
+		void* blk = pick->host;
+		const uint64_t sz = pick->bytes;
+		pick->host = nullptr;
+		pick->host_valid = false;
+		// an H2D restore may still be reading the block
+		auto& H = gpus_[static_cast<size_t>(pick->gpu)];
+		cudaEvent_t after = nullptr;
+		check_cuda(cudaEventCreateWithFlags(&after, cudaEventDisableTiming), "cudaEventCreate");
+		check_cuda(cudaEventRecord(after, H.h2d), "cudaEventRecord");
+		if(sz == bytes) {
+			check_cuda(cudaStreamWaitEvent(gpus_[static_cast<size_t>(gpu)].d2h, after, 0), "cudaStreamWaitEvent");
+			cudaEventDestroy(after);
+			++ctr_.host_reclaims;
+			return blk;
+		}
+		check_cuda(cudaEventSynchronize(after), "cudaEventSynchronize");
+		cudaEventDestroy(after);
+		check_cuda(cudaFreeHost(blk), "cudaFreeHost");
+		host_used_ -= sz;
+		++ctr_.host_reclaims;
+	}
 	void* p = nullptr;
 	check_cuda(cudaHostAlloc(&p, bytes, cudaHostAllocPortable), "cudaHostAlloc");
 	host_used_ += bytes;
@@ -673,7 +703,7 @@ void executor::evict(int64_t chunk) {
 	if(!b.host_valid && dead_ahead(chunk, nullptr)) {
 		++ctr_.dead_drops; // overwritten before it is read again: no write-back
 	} else if(!b.host_valid) {
-		if(!b.host) b.host = host_alloc(b.bytes, b.gpu);
+		if(!b.host) b.host = host_alloc(b.bytes, b.gpu, chunk);
 		check_cuda(cudaMemcpyAsync(b.host, b.ptr, b.bytes, cudaMemcpyDeviceToHost, G.d2h), "cudaMemcpyAsync D2H (evict)");
 		b.host_valid = true;
 		ctr_.bytes_device_to_host += b.bytes;
@@ -699,14 +729,25 @@ void executor::ensure_room(int gpu, uint64_t bytes, const std::vector<int64_t>& 
 	if(bytes > G.capacity)
 		throw execution_error("a chunk of " + std::to_string(bytes) + " bytes can never fit the device capacity " + std::to_string(G.capacity));
 	if(G.used + bytes <= G.capacity) return;
-	// next READ of every chunk within the lookahead window (queue_ holds the future tasks): a
-	// chunk that is only overwritten ahead does not need its data kept (Belady on reads)
+	// next use of every chunk within the lookahead window (queue_ holds the future tasks) that
+	// needs its data on the device: a read, or a write of part of it (a halo row: the rest must
+	// be there). A chunk that is only overwritten ahead does not need its data kept (Belady on
+	// data uses; the dead-data check below catches piecewise overwrites)
 	std::unordered_map<int64_t, size_t> next;
 	std::vector<access_t> accs;
 	for(size_t i = 0; i < queue_.size(); ++i) {
 		accesses_of(queue_[i], accs);
-		for(const auto& a : accs)
-			if(a.read) next.emplace(a.chunk, i);
+		for(const auto& a : accs) {
+			if(next.count(a.chunk)) continue;
+			if(a.read || a.kill) {
+				if(!a.kill) next.emplace(a.chunk, i);
+				continue;
+			}
+			const auto b = bufs_.find(a.chunk);
+			if(!a.overwrite || b == bufs_.end()) continue;
+			// a partial write needs the data; a whole-chunk overwrite ends its life
+			next.emplace(a.chunk, intersect(a.region, b->second.region) == b->second.region ? SIZE_MAX : i);
+		}
 	}
 	while(G.used + bytes > G.capacity) {
 		int64_t victim = -1;

@@ -57,6 +57,7 @@ struct exec_counters {
 	uint64_t bytes_host_to_device = 0;
 	uint64_t dead_drops = 0; // evictions that skipped the write-back (data dead ahead)
 	uint64_t dead_skips = 0; // restores that skipped the H2D (data overwritten before read)
+	uint64_t host_reclaims = 0; // host copies of resident chunks taken back when the host tier is full
 };
 
 class executor {
@@ -222,7 +223,7 @@ class executor {
 	void ensure_room(int gpu, uint64_t bytes, const std::vector<int64_t>& pinned);
 	void evict(int64_t chunk);
 	void restore(int64_t chunk, const std::vector<int64_t>& pinned, const task& current);
-	void* host_alloc(uint64_t bytes, int gpu);
+	void* host_alloc(uint64_t bytes, int gpu, int64_t exclude);
 	void host_release(void* p, uint64_t bytes, cudaEvent_t after);
 	void alloc_wait(int gpu, cudaStream_t s);
 	cudaEvent_t alloc_event(int gpu) const;

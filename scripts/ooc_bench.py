@@ -92,13 +92,18 @@ def main():
     ws = 2 * rows * cols * 4
     h2d = (s1["spill_bytes_h2d"] - s0["spill_bytes_h2d"]) / args.iters
     d2h = (s1["spill_bytes_d2h"] - s0["spill_bytes_d2h"]) / args.iters
-    minimum = max(0, ws - cap)
+    # each iteration reads one array and overwrites the other; the overwritten one is dead, so
+    # at steady state only the part of an array that does not fit must cross the link each way
+    minimum = max(0, ws // 2 - cap)
+    survey_bound = max(0, ws - cap)  # SURVEY 8d's (working set - resident) each way
     per_iter = ms / args.iters / 1e3
     bound = minimum / (bw["duplex_each_way"] * 1e9)
     out = {"workload": f"out-of-core heat2d {rows}x{cols} f32 x2 arrays, {cr}-row chunks, device capacity {args.capacity_gib} GiB",
            "working_set_gib": ws / 2**30, "capacity_gib": args.capacity_gib, "iters": args.iters, "s_per_iter": per_iter,
            "cell_updates_per_s": rows * cols / per_iter, "h2d_gib_per_iter": h2d / 2**30, "d2h_gib_per_iter": d2h / 2**30,
            "min_gib_each_way_per_iter": minimum / 2**30, "moved_over_min": max(h2d, d2h) / minimum if minimum else None,
+           "survey_bound_gib_each_way": survey_bound / 2**30,
+           "time_over_survey_bound": per_iter / (survey_bound / (bw["duplex_each_way"] * 1e9)) if survey_bound else None,
            "link_gbs": bw, "bound_s_per_iter": bound, "time_over_bound": per_iter / bound if bound else None,
            "lookahead_tasks": la, "warmup_s": t_setup, "evictions": s1["evictions"] - s0["evictions"]}
     print(json.dumps(out))
