@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -41,6 +43,12 @@ constexpr uint32_t STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr uint32_t TMEM_COLS = 512;                // two 256-column f32 accumulators
 constexpr int GROUP_M = 16;
 constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+// CTA pair (cta_group::2): a 256x256 tile per pair; per CTA per stage its 128 A rows and its
+// 128 of the 256 Bt rows, so 32 KB per stage and 6 stages in flight
+constexpr int STAGES2 = 6;
+constexpr uint32_t B2_STAGE_BYTES = (BN / 2) * BK * 2; // 16 KB
+constexpr uint32_t STAGE2_BYTES = A_STAGE_BYTES + B2_STAGE_BYTES;
+constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + 256;
 
 struct gemm_args {
 	float* c;
@@ -49,6 +57,8 @@ struct gemm_args {
 	int64_t a_row0;    // A tensor-map row of output row 0
 	int64_t b_row0;    // Bt tensor-map row of output col 0
 	int m_blocks, n_blocks, k_blocks;
+	int group_m; // rasterisation group (M units)
+	uint64_t hint_a, hint_b; // L2 cache policies of the operand loads
 };
 
 // ---- PTX wrappers -------------------------------------------------------------------------
@@ -83,12 +93,58 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 	    : "memory");
 }
 
+
+// cta_group::2 load: data into this CTA's smem, completion on the LEADER CTA's mbarrier (the
+// peer bit of the shared::cluster address cleared)
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t x, int32_t y, uint64_t hint) {
+	asm volatile(
+	    "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+	        smem_u32(dst)),
+	    "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y), "l"(hint)
+	    : "memory");
+}
+
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+	asm volatile(
+	    "{\n\t.reg .pred p;\n\t"
+	    "setp.ne.b32 p, %4, 0;\n\t"
+	    "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+	    "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tc_commit2_mc(uint64_t* bar, uint16_t mask) {
+	asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
+	    : "memory");
+}
+
+// arrive on the mbarrier at `bar`'s offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+	asm volatile(
+	    "{\n\t.reg .b32 ra;\n\t"
+	    "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+	    "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+	    "r"(rank)
+	    : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+	uint32_t r;
+	asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+	return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+	asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+	asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 	asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+
 
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
 	asm volatile(
@@ -109,9 +165,9 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
 	return d;
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major, M=128, N=256
-__host__ __device__ constexpr uint32_t instr_desc() {
-	return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major, M x N = `m` x 256
+__host__ __device__ constexpr uint32_t instr_desc(int m = BM) {
+	return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -125,11 +181,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 	asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void tile_coords(int t, const gemm_args& p, int& mb, int& nb) {
-	const int group = GROUP_M * p.n_blocks;
+// tile t -> (M unit, N block), rasterised in groups of GROUP_M M units (units = M blocks, or
+// M block pairs for the CTA-pair kernel)
+__device__ __forceinline__ void tile_coords(int t, const gemm_args& p, int& mb, int& nb, int m_units) {
+	const int group = p.group_m * p.n_blocks;
 	const int g = t / group;
-	const int first_m = g * GROUP_M;
-	const int rows = min(GROUP_M, p.m_blocks - first_m);
+	const int first_m = g * p.group_m;
+	const int rows = min(p.group_m, m_units - first_m);
 	const int r = t % group;
 	mb = first_m + r % rows;
 	nb = r / rows;
@@ -181,7 +239,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			uint32_t phase = 0;
 			for(int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
 				int mb, nb;
-				tile_coords(t, p, mb, nb);
+				tile_coords(t, p, mb, nb, p.m_blocks);
 				const int32_t arow = static_cast<int32_t>(p.a_row0 + static_cast<int64_t>(mb) * BM);
 				const int32_t brow = static_cast<int32_t>(p.b_row0 + static_cast<int64_t>(nb) * BN);
 				for(int kb = 0; kb < p.k_blocks; ++kb) {
@@ -231,7 +289,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 		int local = 0;
 		for(int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
 			int mb, nb;
-			tile_coords(t, p, mb, nb);
+			tile_coords(t, p, mb, nb, p.m_blocks);
 			const int acc = local & 1;
 			mbar_wait(&tmem_full[acc], (local >> 1) & 1);
 			tc_fence_after();
@@ -265,6 +323,158 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	if(warp == 1) {
 		tc_fence_after();
 		asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
+	}
+}
+
+// ---- CTA pair: tcgen05.mma.cta_group::2, 256x256 tiles -----------------------------------
+//
+// The two CTAs of a cluster (one TPC) compute one 256x256 tile: each holds 128 rows of A and
+// 128 of the 256 Bt rows per stage and the leader (rank 0) issues M=256 N=256 K=16 MMAs that
+// read both CTAs' shared memory; each CTA's TMEM receives its own 128 rows. Per CTA a stage is
+// 32 KB instead of 48 KB, so 6 stages are in flight and the L2->SM operand traffic per flop is
+// a third lower. Both CTAs' TMA loads complete on the leader's `full` barrier (expect_tx set by
+// the leader for both); the leader's MMA commit frees the stage in both CTAs and signals both
+// CTAs' `tmem_full`; both CTAs' epilogue warps release the accumulator on the leader's
+// `tmem_empty` (count 8).
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_bf16_nt_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, gemm_args p) {
+	extern __shared__ uint8_t smem_raw[];
+	uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+	uint8_t* a_smem = smem;
+	uint8_t* b_smem = smem + STAGES2 * A_STAGE_BYTES;
+	uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+	uint64_t* full = bars;
+	uint64_t* empty = bars + STAGES2;
+	uint64_t* tmem_full = bars + 2 * STAGES2;
+	uint64_t* tmem_empty = bars + 2 * STAGES2 + 2;
+	uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
+
+	const int warp = threadIdx.x / 32;
+	const int lane = threadIdx.x % 32;
+	const uint32_t rank = cluster_rank();
+	const bool leader = rank == 0;
+	const int m_pairs = (p.m_blocks + 1) / 2;
+	const int num_units = m_pairs * p.n_blocks;
+	const int first_unit = static_cast<int>(blockIdx.x) / 2;
+	const int unit_stride = static_cast<int>(gridDim.x) / 2;
+	constexpr uint16_t kPair = 0x3;
+
+	if(warp == 0 && lane == 0) {
+		for(int s = 0; s < STAGES2; ++s) {
+			mbar_init(&full[s], 1);
+			mbar_init(&empty[s], 1);
+		}
+		for(int a = 0; a < 2; ++a) {
+			mbar_init(&tmem_full[a], 1);
+			mbar_init(&tmem_empty[a], 8);
+		}
+		asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+		asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
+		asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
+	}
+	if(warp == 1) {
+		asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(TMEM_COLS) : "memory");
+		asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+	}
+	tc_fence_before();
+	__syncthreads();
+	cluster_sync_all();
+	tc_fence_after();
+	const uint32_t tmem_base = *tmem_slot;
+
+	if(warp == 0) {
+		if(lane == 0) {
+			// ---- TMA producer (both CTAs) ----
+			int stage = 0;
+			uint32_t phase = 0;
+			for(int t = first_unit; t < num_units; t += unit_stride) {
+				int mu, nb;
+				tile_coords(t, p, mu, nb, m_pairs);
+				const int32_t arow = static_cast<int32_t>(p.a_row0 + static_cast<int64_t>(mu) * 2 * BM + rank * BM);
+				const int32_t brow = static_cast<int32_t>(p.b_row0 + static_cast<int64_t>(nb) * BN + rank * (BN / 2));
+				for(int kb = 0; kb < p.k_blocks; ++kb) {
+					mbar_wait(&empty[stage], phase ^ 1);
+					if(leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE2_BYTES);
+					tma_load_2d_2sm(a_smem + stage * A_STAGE_BYTES, &tmap_a, &full[stage], kb * BK, arow, p.hint_a);
+					tma_load_2d_2sm(b_smem + stage * B2_STAGE_BYTES, &tmap_b, &full[stage], kb * BK, brow, p.hint_b);
+					if(++stage == STAGES2) {
+						stage = 0;
+						phase ^= 1;
+					}
+				}
+			}
+		}
+	} else if(warp == 1) {
+		if(lane == 0 && leader) {
+			// ---- MMA issuer (leader only) ----
+			constexpr uint32_t idesc = instr_desc(2 * BM);
+			int stage = 0;
+			uint32_t phase = 0;
+			int local = 0;
+			for(int t = first_unit; t < num_units; t += unit_stride, ++local) {
+				const int acc = local & 1;
+				mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
+				tc_fence_after();
+				const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+				for(int kb = 0; kb < p.k_blocks; ++kb) {
+					mbar_wait(&full[stage], phase);
+					tc_fence_after();
+					const uint32_t a0 = smem_u32(a_smem + stage * A_STAGE_BYTES);
+					const uint32_t b0 = smem_u32(b_smem + stage * B2_STAGE_BYTES);
+#pragma unroll
+					for(int k = 0; k < BK / UMMA_K; ++k)
+						tc_mma2(d, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+					tc_commit2_mc(&empty[stage], kPair);
+					if(++stage == STAGES2) {
+						stage = 0;
+						phase ^= 1;
+					}
+				}
+				tc_commit2_mc(&tmem_full[acc], kPair);
+			}
+		}
+	} else {
+		// ---- epilogue (both CTAs): warps 2..5, own TMEM lanes = own 128 rows ----
+		const int quarter = warp & 3;
+		int local = 0;
+		for(int t = first_unit; t < num_units; t += unit_stride, ++local) {
+			int mu, nb;
+			tile_coords(t, p, mu, nb, m_pairs);
+			const int acc = local & 1;
+			mbar_wait(&tmem_full[acc], (local >> 1) & 1);
+			tc_fence_after();
+			const int64_t row = static_cast<int64_t>(mu) * 2 * BM + rank * BM + quarter * 32 + lane;
+			const bool row_ok = row < p.m;
+			float* crow = p.c + row * p.ldc;
+			const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+			for(int c = 0; c < BN; c += 32) {
+				uint32_t r[32];
+				tmem_ld32(taddr + static_cast<uint32_t>(c), r);
+				const int64_t col0 = static_cast<int64_t>(nb) * BN + c;
+				if(!row_ok) continue;
+				if(col0 + 32 <= p.n && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0)) {
+#pragma unroll
+					for(int v = 0; v < 8; ++v) {
+						float4 f = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]), __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+						*reinterpret_cast<float4*>(crow + col0 + 4 * v) = f;
+					}
+				} else {
+					for(int v = 0; v < 32; ++v)
+						if(col0 + v < p.n) crow[col0 + v] = __uint_as_float(r[v]);
+				}
+			}
+			tc_fence_before();
+			__syncwarp();
+			if(lane == 0) mbar_arrive_remote(&tmem_empty[acc], 0);
+		}
+	}
+	__syncthreads();
+	// the peer may still read this CTA's smem (MMA) or arrive on its barriers
+	cluster_sync_all();
+	if(warp == 1) {
+		tc_fence_after();
+		asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
 	}
 }
 
@@ -311,8 +521,6 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	if(m <= 0 || n <= 0) return 0;
 	if(k <= 0) return 5;
 	if((lda * 2) % 16 || (ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(a) % 16) || (reinterpret_cast<uintptr_t>(bt) % 16)) return 6;
-	CUtensorMap ma, mb;
-	if(!make_map(&ma, a, a_rows, k, lda, BM) || !make_map(&mb, bt, b_rows, k, ldb, BN)) return 7;
 	gemm_args p{};
 	p.c = c;
 	p.ldc = ldc;
@@ -324,10 +532,52 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	p.m_blocks = static_cast<int>((m + BM - 1) / BM);
 	p.n_blocks = static_cast<int>((n + BN - 1) / BN);
 	p.k_blocks = static_cast<int>((k + BK - 1) / BK);
-	kern::ensure_smem(gemm_bf16_nt_kernel, static_cast<int>(SMEM_BYTES));
-	const int tiles = p.m_blocks * p.n_blocks;
-	const int grid = std::min(tiles, num_sms());
-	gemm_bf16_nt_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+	const int sms = num_sms();
+	p.group_m = GROUP_M;
+	if(const char* e = std::getenv("MTB_GEMM_GROUP")) p.group_m = std::max(1, std::atoi(e));
+	// L2 policies (the CUTLASS encodings): normal 0x1000000000000000, evict-first 0x12F0..., evict-last 0x14F0...
+	p.hint_a = p.hint_b = 0x1000000000000000ull;
+	if(const char* e = std::getenv("MTB_GEMM_HINT_A")) p.hint_a = std::strtoull(e, nullptr, 16);
+	if(const char* e = std::getenv("MTB_GEMM_HINT_B")) p.hint_b = std::strtoull(e, nullptr, 16);
+	// CTA pairs once there are enough 256x256 tiles to fill the machine. Measured (ncu, B200):
+	// pairs are 5-12% faster from 4096^3 to 16384^2 x 32768, but at M = N = K = 32768 they read
+	// ~4x the DRAM bytes of the single-CTA kernel (L2 reuse across the wave is lost; the cause is
+	// not understood yet), so problems with both M*N > 16384^2 and K > 16384 stay on single CTAs.
+	const bool big = static_cast<double>(m) * static_cast<double>(n) > 16384.0 * 16384.0 && k > 16384;
+	const bool pair = p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && !big && std::getenv("MTB_GEMM_NO_PAIR") == nullptr;
+	CUtensorMap ma, mb;
+	if(!make_map(&ma, a, a_rows, k, lda, BM) || !make_map(&mb, bt, b_rows, k, ldb, pair ? BN / 2 : BN)) return 7;
+	if(!pair) {
+		kern::ensure_smem(gemm_bf16_nt_kernel, static_cast<int>(SMEM_BYTES));
+		const int grid = std::min(p.m_blocks * p.n_blocks, sms);
+		gemm_bf16_nt_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+		return cudaGetLastError() == cudaSuccess ? 0 : 1;
+	}
+	kern::ensure_smem(gemm_bf16_nt_2sm_kernel, static_cast<int>(SMEM2_BYTES));
+	cudaLaunchConfig_t cfg{};
+	cudaLaunchAttribute attr[1];
+	attr[0].id = cudaLaunchAttributeClusterDimension;
+	attr[0].val.clusterDim.x = 2;
+	attr[0].val.clusterDim.y = 1;
+	attr[0].val.clusterDim.z = 1;
+	cfg.blockDim = dim3(NUM_THREADS);
+	cfg.dynamicSmemBytes = SMEM2_BYTES;
+	cfg.stream = s;
+	cfg.attrs = attr;
+	cfg.numAttrs = 1;
+	static int max_clusters = 0;
+	if(max_clusters == 0) {
+		cfg.gridDim = dim3(static_cast<unsigned>(sms & ~1));
+		int n_cl = 0;
+		if(cudaOccupancyMaxActiveClusters(&n_cl, gemm_bf16_nt_2sm_kernel, &cfg) != cudaSuccess || n_cl <= 0) n_cl = sms / 2;
+		cudaGetLastError();
+		max_clusters = n_cl;
+		if(const char* e = std::getenv("MTB_GEMM_CLUSTERS")) max_clusters = std::max(1, std::atoi(e));
+		if(std::getenv("MTB_GEMM_VERBOSE")) std::fprintf(stderr, "[gemm] max active clusters %d (occupancy query %d)\n", max_clusters, n_cl);
+	}
+	const int units = ((p.m_blocks + 1) / 2) * p.n_blocks;
+	cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(units, max_clusters)));
+	if(cudaLaunchKernelEx(&cfg, gemm_bf16_nt_2sm_kernel, ma, mb, p) != cudaSuccess) return 1;
 	return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

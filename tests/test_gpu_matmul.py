@@ -38,7 +38,9 @@ def from_bf16_bits(b: np.ndarray) -> np.ndarray:
     return (b.astype(np.uint32) << 16).view(np.float32)
 
 
-@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (300, 520, 136), (1024, 768, 1000), (2048, 2048, 4096)])
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (300, 520, 136), (1024, 768, 1000), (2048, 2048, 4096),
+                                   # CTA-pair kernel (>= 148 CTAs of 256x256 tiles): odd M-block count, ragged N and K
+                                   (4224, 4096, 512), (3000, 4100, 1000)])
 def test_gemm_matches_fp64(m, n, k):
     import torch
     a = to_bf16_bits(pattern(m, k, 1000, 7))
