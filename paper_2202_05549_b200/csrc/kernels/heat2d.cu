@@ -15,8 +15,6 @@
 // per warp issue a scalar load per row. Rows are fetched kBatch at a time so every thread has
 // kBatch independent 128-bit loads in flight. Input bytes are read once from HBM except the 2
 // halo rows per segment (2/kSegRows extra, mostly L2 hits).
-#include <cstdlib>
-
 #include "../executor.hpp"
 #include "common.cuh"
 
@@ -54,8 +52,10 @@ __device__ __forceinline__ float load_one(const heat_args& p, int64_t i, int64_t
 	return __ldg(p.in + (i - p.in_r0) * p.in_ld + (j - p.in_c0));
 }
 
-template <int kSegRows, int kBatch, int kMinBlocks>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) heat2d_vec_kernel(heat_args p) {
+// 4 CTAs (32 warps) per SM: <= 64 registers. Measured alternatives (B200, 65536^2): 64- or
+// 256-row segments, 8-row batches (125 registers, 2 CTAs/SM: 0.74 of peak) and 5-8 CTAs/SM
+// (register caps with small spills) are all equal or slower.
+__global__ void __launch_bounds__(kThreads, 4) heat2d_vec_kernel(heat_args p) {
 	const int lane = threadIdx.x & 31;
 	const int64_t j = p.c0 + static_cast<int64_t>(blockIdx.x) * kColsPerCta + threadIdx.x * 4;
 	const bool active = j < p.c1;
@@ -153,19 +153,9 @@ int launch_heat2d(const mt_launch_ctx* c, void* stream) {
 			p.c0 = col_lo;
 			p.c1 = vec_hi;
 			const int64_t strips = (vec_hi - col_lo + kColsPerCta - 1) / kColsPerCta;
-			static const int variant = std::getenv("MTB_HEAT_VARIANT") ? std::atoi(std::getenv("MTB_HEAT_VARIANT")) : 0;
-			const int seg_rows = variant == 1 ? 256 : variant == 8 ? 64 : kSegRows;
-			const int64_t segs = (p.r1 - p.r0 + seg_rows - 1) / seg_rows;
+			const int64_t segs = (p.r1 - p.r0 + kSegRows - 1) / kSegRows;
 			if(segs > 65535) return 3;
-			const dim3 grid(static_cast<unsigned>(strips), static_cast<unsigned>(segs));
-			switch(variant) {
-			case 1: heat2d_vec_kernel<256, 4, 4><<<grid, kThreads, 0, s>>>(p); break;
-			case 5: heat2d_vec_kernel<128, 4, 5><<<grid, kThreads, 0, s>>>(p); break;
-			case 6: heat2d_vec_kernel<128, 4, 6><<<grid, kThreads, 0, s>>>(p); break;
-			case 7: heat2d_vec_kernel<128, 2, 8><<<grid, kThreads, 0, s>>>(p); break;
-			case 8: heat2d_vec_kernel<64, 4, 4><<<grid, kThreads, 0, s>>>(p); break;
-			default: heat2d_vec_kernel<kSegRows, kBatch, 4><<<grid, kThreads, 0, s>>>(p); break;
-			}
+			heat2d_vec_kernel<<<dim3(static_cast<unsigned>(strips), static_cast<unsigned>(segs)), kThreads, 0, s>>>(p);
 		}
 	}
 	if(vec_hi < col_hi) {
