@@ -21,12 +21,12 @@ def fuzz_scenario(ref, seed):
     return json.loads(buf.value)
 
 
-def run_product(sc, suppress=False):
+def run_product(sc, suppress=False, streams=0):
     sysd = sc.get("system", {})
     cap = int(sysd.get("device_capacity", 256 << 20))
     spill = cap < (256 << 20)
     with mb.context(workers=sysd.get("workers", 1), devices=sysd.get("devices", 1), num_gpus=1, suppress_conflict_deps=suppress,
-                    device_capacity=cap if spill else 0, host_capacity=(1 << 30) if spill else 0) as ctx:
+                    device_capacity=cap if spill else 0, host_capacity=(1 << 30) if spill else 0, streams_per_device=streams) as ctx:
         S.register_gather_kernels(ctx, sc)
         return S.run(ctx, sc)
 
@@ -57,19 +57,24 @@ def test_fuzz_campaign_matches_sequential_oracle(ref, block):
 
 
 def test_suppressed_conflict_edges_are_detected(ref):
-    """Acceptance c8 (mutation power): dropping the conflict edges must break some case."""
-    broken = 0
-    for i in range(40):
+    """Acceptance c8 (mutation power): dropping the conflict edges must break some case. On the
+    GPU a dropped edge only shows when the two tasks land on different streams and overlap in
+    time, so the campaign uses 16 streams per device and runs until the first detection."""
+    broken = tried = 0
+    for i in range(160):
         sc = fuzz_scenario(ref, 1000 + i * 7919)
         try:
             want, _ = S.reference_run(ref, sc, oracle_mode=True)
         except mb.MantaError:
             continue
+        tried += 1
         try:
-            got, coherent = run_product(sc, suppress=True)
+            got, coherent = run_product(sc, suppress=True, streams=16)
         except mb.MantaError:
             broken += 1
-            continue
-        if S.compare(got, want, 1e-6) or not coherent:
-            broken += 1
-    assert broken > 0
+        else:
+            if S.compare(got, want, 1e-6) or not coherent:
+                broken += 1
+        if broken:
+            break
+    assert broken > 0, f"no mutation detected in {tried} scenarios"
