@@ -58,6 +58,10 @@ enum mt_task_kind {
 	 * group is `tag`, its data-carrying members are `inputs` in worker order (a worker
 	 * without a partial joins with an identity-filled buffer and is not in `inputs`) */
 	MT_TASK_ALLREDUCE = 7,
+	/* B200 extension (mt_array_write_async / mt_array_read_async): copy `region` of chunk
+	 * `chunk` from / to the host array at address `tag` (row-major over `src_region`) */
+	MT_TASK_HOST_WRITE = 8,
+	MT_TASK_HOST_READ = 9,
 };
 enum mt_fill_kind { MT_FILL_NONE = 0, MT_FILL_ZERO = 1, MT_FILL_ONE = 2, MT_FILL_IDENTITY = 3 };
 enum mt_reduce_op { MT_RED_PLUS = 0, MT_RED_TIMES = 1, MT_RED_MIN = 2, MT_RED_MAX = 3 };
@@ -106,6 +110,8 @@ typedef struct mt_arg_binding {
  *   send   : chunk, region, peer, tag          recv: chunk, region, peer, tag
  *   reduce : op, inputs, output
  *   allreduce: op, inputs (group members with data), output (this worker's member), tag (group)
+ *   host_write / host_read: chunk, region (copied box), src_region (host array box),
+ *            dtype, tag (host address)
  */
 typedef struct mt_task {
 	int64_t id;
@@ -222,6 +228,14 @@ int mt_sync(mt_ctx* ctx);
 int mt_array_read(mt_ctx* ctx, int64_t array_id, void* host, uint64_t bytes);
 /* Uploads host data into every chunk of an array (B200 extension: e2e input path). */
 int mt_array_write(mt_ctx* ctx, int64_t array_id, const void* host, uint64_t bytes);
+/* B200 extension: asynchronous host transfers, planned as tasks and therefore ordered against
+ * launches by the dependency tracking (a write overwrites every chunk; a read copies each
+ * cell once, from the lowest-id chunk holding it). They return once queued; the host buffer
+ * (row-major over the domain; pinned memory for DMA overlap) must stay valid and untouched
+ * until mt_sync. Replaces the synchronous round trip of mt_array_write / mt_array_read
+ * (runtime.cpp:697-712 read_chunk) in pipelines that stream inputs and results. */
+int mt_array_write_async(mt_ctx* ctx, int64_t id, const void* host, uint64_t bytes);
+int mt_array_read_async(mt_ctx* ctx, int64_t id, void* host, uint64_t bytes);
 /* Byte-compares every overlapping chunk pair (check_replicas, scenario.cpp:486-509);
  * *coherent = 1 when all agree. */
 int mt_array_check_replicas(mt_ctx* ctx, int64_t array_id, int32_t* coherent);
@@ -265,7 +279,8 @@ int mt_exec_report_json(mt_exec* ex, char* buf, int64_t cap, int64_t* len);
 
 /* counters: tasks, device launches, copies, bytes copied, bytes sent, bytes received, peak
  * device bytes, evictions, spill bytes D2H, spill bytes H2D, dead drops (evictions without
- * write-back), dead skips (restores without H2D), host reclaims (first n of them) */
+ * write-back), dead skips (restores without H2D), host reclaims, host_write bytes, host_read
+ * bytes (first n of them) */
 int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n);
 /* cudaStream_t of the most recent execute task (for event timing on the launching stream) */
 void* mt_exec_last_stream(mt_exec* ex);

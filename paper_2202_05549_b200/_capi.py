@@ -19,8 +19,8 @@ I32, I64, F32, F64, BF16 = range(5)
 DTYPE_NAMES = {"i32": I32, "i64": I64, "f32": F32, "f64": F64, "bf16": BF16}
 DTYPE_SIZE = {I32: 4, I64: 8, F32: 4, F64: 8, BF16: 2}
 # task kinds (task.hpp:32-95)
-CREATE, DELETE, EXECUTE, COPY, SEND, RECV, REDUCE, ALLREDUCE = range(8)
-TASK_KIND_NAMES = ["create", "delete", "execute", "copy", "send", "recv", "reduce", "allreduce"]
+CREATE, DELETE, EXECUTE, COPY, SEND, RECV, REDUCE, ALLREDUCE, HOST_WRITE, HOST_READ = range(10)
+TASK_KIND_NAMES = ["create", "delete", "execute", "copy", "send", "recv", "reduce", "allreduce", "host_write", "host_read"]
 FILL_NONE, FILL_ZERO, FILL_ONE, FILL_IDENTITY = range(4)
 RED_PLUS, RED_TIMES, RED_MIN, RED_MAX = range(4)
 ARG_INT, ARG_FLOAT, ARG_CHUNK, ARG_NONE = range(4)
@@ -165,6 +165,8 @@ _SIGS = {
     "ctx_peer_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, P(C.c_int64)]),
     "ctx_peer_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),
     "ctx_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p]),
+    "array_write_async": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_uint64]),
+    "array_read_async": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_uint64]),
     "ctx_nccl_init": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p]),
     "fuzz_scenario_json": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int64, P(C.c_int64)]),
     "scenario_plan": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(Task), C.c_int64, P(C.c_int64), P(C.c_int64),
@@ -175,7 +177,7 @@ _SIGS = {
 }
 # entry points the oracle shim may lack
 _OPTIONAL = {"exec_stats", "exec_last_stream", "kernel_info", "host_threads", "ctx_kernel_register", "fuzz_scenario_json", "scenario_plan",
-             "scenario_run", "plan_accesses", "ctx_gather_register", "ctx_peer_export", "ctx_peer_import", "ctx_nccl_unique_id", "ctx_nccl_init", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
+             "scenario_run", "plan_accesses", "ctx_gather_register", "ctx_peer_export", "ctx_peer_import", "ctx_nccl_unique_id", "ctx_nccl_init", "array_write_async", "array_read_async", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
 
 
 class MantaError(RuntimeError):

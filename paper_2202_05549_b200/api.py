@@ -153,6 +153,8 @@ def _task_dict(t: capi.Task, pool, args) -> dict:
         d.update(chunk=t.chunk, region=t.region.box(), peer=t.peer, tag=t.tag)
     elif k == capi.REDUCE:
         d.update(op=t.op, inputs=[pool[t.inputs_off + i] for i in range(t.ninputs)], output=t.output)
+    elif k in (capi.HOST_WRITE, capi.HOST_READ):
+        d.update(chunk=t.chunk, region=t.region.box(), host_box=t.src_region.box(), host=t.tag, dtype=t.dtype)
     elif k == capi.ALLREDUCE:
         d.update(op=t.op, inputs=[pool[t.inputs_off + i] for i in range(t.ninputs)], output=t.output, tag=t.tag, region=t.region.box(),
                  dtype=t.dtype)
@@ -212,6 +214,7 @@ class Context:
         self.h = h
         self.executes = bool(execute)
         self._arrays: dict[int, tuple] = {}
+        self._inflight: list = []  # host buffers of queued async transfers
 
     def close(self):
         if self.h:
@@ -285,6 +288,7 @@ class Context:
 
     def synchronize(self):
         self.lib.check(self.lib.sync(self.h))
+        self._inflight.clear()
 
     # -- data ------------------------------------------------------------------------
     def shape_of(self, array_id: int):
@@ -301,6 +305,33 @@ class Context:
         shape, t = self.shape_of(array_id)
         data = np.ascontiguousarray(data, dtype=_NP_DTYPE[t]).reshape(shape)
         self.lib.check(self.lib.array_write(self.h, array_id, data.ctypes.data, data.nbytes))
+
+    # -- asynchronous host transfers (planned as tasks; see mt_array_write_async) ---------
+    def write_async(self, array_id: int, data) -> None:
+        """Queue an upload of `data` (C-contiguous, the array's shape and dtype; numpy or a
+        pinned torch tensor) into every chunk. The buffer must stay untouched until
+        synchronize(); the context keeps a reference until then."""
+        ptr, nbytes = self._host_buffer(array_id, data)
+        self.lib.check(self.lib.array_write_async(self.h, array_id, ptr, nbytes))
+        self._inflight.append(data)
+
+    def read_async(self, array_id: int, out) -> None:
+        """Queue a download of the array into `out` (C-contiguous, the array's shape and dtype);
+        valid after synchronize()."""
+        ptr, nbytes = self._host_buffer(array_id, out)
+        self.lib.check(self.lib.array_read_async(self.h, array_id, ptr, nbytes))
+        self._inflight.append(out)
+
+    def _host_buffer(self, array_id, buf):
+        shape, t = self.shape_of(array_id)
+        if isinstance(buf, np.ndarray):
+            if not buf.flags["C_CONTIGUOUS"] or buf.dtype != np.dtype(_NP_DTYPE[t]) or list(buf.shape) != list(shape):
+                raise ValidationError("host buffer must be C-contiguous with the array's shape and dtype")
+            return buf.ctypes.data, buf.nbytes
+        # torch tensor (e.g. pinned host memory)
+        if buf.is_cuda or not buf.is_contiguous() or list(buf.shape) != list(shape):
+            raise ValidationError("host buffer must be a contiguous host tensor with the array's shape")
+        return buf.data_ptr(), buf.numel() * buf.element_size()
 
     def replicas_coherent(self, array_id: int) -> bool:
         ok = C.c_int32(0)
@@ -345,7 +376,8 @@ class Context:
         if not ex or not self.lib.has("exec_stats"):
             return {}
         keys = ["tasks", "kernels", "copies", "bytes_copied", "bytes_sent", "bytes_received", "peak_device_bytes", "evictions",
-                "spill_bytes_d2h", "spill_bytes_h2d", "dead_drops", "dead_skips", "host_reclaims"]
+                "spill_bytes_d2h", "spill_bytes_h2d", "dead_drops", "dead_skips", "host_reclaims",
+                "host_write_bytes", "host_read_bytes"]
         out = (C.c_uint64 * len(keys))()
         self.lib.check(self.lib.exec_stats(ex, out, len(keys)))
         return dict(zip(keys, [int(v) for v in out]))

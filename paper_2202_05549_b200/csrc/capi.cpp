@@ -129,6 +129,13 @@ void flatten(const task& t, mt_task& o, std::vector<int64_t>& pool, std::vector<
 		o.peer = t.peer;
 		o.tag = t.tag;
 		break;
+	case task_kind::host_write:
+	case task_kind::host_read:
+		o.region = from_box(t.region);
+		o.src_region = from_box(t.src_region);
+		o.dtype = static_cast<int32_t>(t.type);
+		o.tag = t.tag;
+		break;
 	case task_kind::allreduce:
 		o.region = from_box(t.region);
 		o.dtype = static_cast<int32_t>(t.type);
@@ -148,7 +155,7 @@ task unflatten(const mt_task& o, const int64_t* pool, const mt_arg_binding* args
 	task t;
 	t.id = o.id;
 	t.worker = o.worker;
-	if(o.kind < 0 || o.kind > MT_TASK_ALLREDUCE) throw validation_error("bad task kind");
+	if(o.kind < 0 || o.kind > MT_TASK_HOST_READ) throw validation_error("bad task kind");
 	t.kind = static_cast<task_kind>(o.kind);
 	t.resource = to_dev(o.resource);
 	for(int64_t i = 0; i < o.ndeps; ++i) t.deps.push_back(pool[o.deps_off + i]);
@@ -187,6 +194,13 @@ task unflatten(const mt_task& o, const int64_t* pool, const mt_arg_binding* args
 	case task_kind::recv:
 		t.region = to_box(o.region);
 		t.peer = o.peer;
+		t.tag = o.tag;
+		break;
+	case task_kind::host_write:
+	case task_kind::host_read:
+		t.region = to_box(o.region);
+		t.src_region = to_box(o.src_region);
+		t.type = to_dtype(o.dtype);
 		t.tag = o.tag;
 		break;
 	case task_kind::allreduce:
@@ -396,6 +410,24 @@ int mt_array_write(mt_ctx* ctx, int64_t id, const void* host, uint64_t bytes) {
 	});
 }
 
+int mt_array_write_async(mt_ctx* ctx, int64_t id, const void* host, uint64_t bytes) {
+	return guarded([&] { // plan-only contexts just plan the transfer
+		const array_rec& a = ctx->plan->array(id);
+		if(bytes < static_cast<uint64_t>(a.domain.volume()) * dtype_size(a.type)) throw validation_error("host buffer too small");
+		ctx->plan->host_transfer(id, reinterpret_cast<uint64_t>(host), true);
+		flush(ctx);
+	});
+}
+
+int mt_array_read_async(mt_ctx* ctx, int64_t id, void* host, uint64_t bytes) {
+	return guarded([&] {
+		const array_rec& a = ctx->plan->array(id);
+		if(bytes < static_cast<uint64_t>(a.domain.volume()) * dtype_size(a.type)) throw validation_error("host buffer too small");
+		ctx->plan->host_transfer(id, reinterpret_cast<uint64_t>(host), false);
+		flush(ctx);
+	});
+}
+
 int mt_array_check_replicas(mt_ctx* ctx, int64_t id, int32_t* coherent) {
 	return guarded([&] {
 		mt_exec& e = need_exec(ctx);
@@ -522,7 +554,7 @@ int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n) {
 	return guarded([&] {
 		const auto& c = ex->ex->counters();
 		const uint64_t v[] = {c.tasks, c.kernels, c.copies, c.bytes_copied, c.bytes_sent, c.bytes_received, c.peak_device_bytes, c.evictions,
-		    c.bytes_device_to_host, c.bytes_host_to_device, c.dead_drops, c.dead_skips, c.host_reclaims};
+		    c.bytes_device_to_host, c.bytes_host_to_device, c.dead_drops, c.dead_skips, c.host_reclaims, c.bytes_host_in, c.bytes_host_out};
 		for(int32_t i = 0; i < n && i < static_cast<int32_t>(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
 	});
 }

@@ -326,6 +326,8 @@ executor::executor(const executor_config& cfg) : cfg_(cfg) {
 			for(auto& s : L.compute) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
 			check_cuda(cudaStreamCreateWithFlags(&L.copy, cudaStreamNonBlocking), "cudaStreamCreate");
 			check_cuda(cudaStreamCreateWithFlags(&L.recv, cudaStreamNonBlocking), "cudaStreamCreate");
+			check_cuda(cudaStreamCreateWithFlags(&L.host_in, cudaStreamNonBlocking), "cudaStreamCreate");
+			check_cuda(cudaStreamCreateWithFlags(&L.host_out, cudaStreamNonBlocking), "cudaStreamCreate");
 		}
 	}
 }
@@ -352,6 +354,8 @@ executor::~executor() {
 		for(auto s : L.compute) cudaStreamDestroy(s);
 		if(L.copy) cudaStreamDestroy(L.copy);
 		if(L.recv) cudaStreamDestroy(L.recv);
+		if(L.host_in) cudaStreamDestroy(L.host_in);
+		if(L.host_out) cudaStreamDestroy(L.host_out);
 	}
 	for(auto& G : gpus_) {
 		cudaSetDevice(G.ordinal);
@@ -478,6 +482,8 @@ void executor::issue(const task& t) {
 	case task_kind::recv: run_recv(t); break;
 	case task_kind::reduce: run_reduce(t); break;
 	case task_kind::allreduce: run_allreduce(t); break;
+	case task_kind::host_write:
+	case task_kind::host_read: run_host_io(t); break;
 	}
 	if(spill_) note_use(t);
 }
@@ -518,6 +524,8 @@ void executor::used_chunks(const task& t, std::vector<std::pair<int64_t, bool>>&
 		for(const auto c : t.inputs) out.emplace_back(c, false);
 		out.emplace_back(t.output, true);
 		break;
+	case task_kind::host_write: out.emplace_back(t.chunk, true); break;
+	case task_kind::host_read: out.emplace_back(t.chunk, false); break;
 	case task_kind::allreduce: {
 		// the last local member combines every member: keep them all resident
 		for(const auto c : t.inputs)
@@ -562,6 +570,8 @@ void executor::accesses_of(const task& t, std::vector<access_t>& out) const {
 		for(const auto c : t.inputs) out.push_back({c, full(c), true, false, false});
 		out.push_back({t.output, full(t.output), false, true, false});
 		break;
+	case task_kind::host_write: out.push_back({t.chunk, t.region, false, true, false}); break;
+	case task_kind::host_read: out.push_back({t.chunk, t.region, true, false, false}); break;
 	case task_kind::allreduce:
 		for(const auto c : t.inputs)
 			if(c != t.output && bufs_.count(c)) out.push_back({c, full(c), true, false, false});
@@ -1158,6 +1168,30 @@ void executor::run_allreduce(const task& t) {
 	for(const auto& [ev, gi] : g.ready) free_events_[static_cast<size_t>(gi)].push_back(ev);
 	for(const auto id : g.tasks) finish_id(id, s, L.gpu);
 	groups_.erase(t.tag);
+}
+
+// host_write / host_read: one region copy between the chunk and the host array, on the
+// device's host-in / host-out stream so uploads, downloads and kernels all overlap
+void executor::run_host_io(const task& t) {
+	buffer& b = buf(t.chunk);
+	ldev& L = dev(t.resource);
+	const bool in = t.kind == task_kind::host_write;
+	cudaStream_t s = in ? L.host_in : L.host_out;
+	wait_deps(t, s);
+	if(!encloses(b.region, t.region) || !encloses(t.src_region, t.region)) throw execution_error("host transfer region outside the chunk or the host array");
+	void* host = reinterpret_cast<void*>(static_cast<uintptr_t>(t.tag));
+	const size_t elem = dtype_size(b.type);
+	if(!b.ptr) throw execution_error("host transfer on a non-resident chunk");
+	if(in)
+		copy_box(host, t.src_region, -1, b.ptr, b.region, ord(b.gpu), t.region, elem, s);
+	else
+		copy_box(b.ptr, b.region, ord(b.gpu), host, t.src_region, -1, t.region, elem, s);
+	const uint64_t bytes = static_cast<uint64_t>(t.region.volume()) * elem;
+	if(in)
+		ctr_.bytes_host_in += bytes;
+	else
+		ctr_.bytes_host_out += bytes;
+	finish(t, s);
 }
 
 void executor::mark(int slot) {

@@ -58,6 +58,7 @@ struct exec_counters {
 	uint64_t dead_drops = 0; // evictions that skipped the write-back (data dead ahead)
 	uint64_t dead_skips = 0; // restores that skipped the H2D (data overwritten before read)
 	uint64_t host_reclaims = 0; // host copies of resident chunks taken back when the host tier is full
+	uint64_t bytes_host_in = 0, bytes_host_out = 0; // host_write / host_read tasks
 };
 
 class executor {
@@ -126,6 +127,7 @@ class executor {
 		std::vector<cudaStream_t> compute;
 		cudaStream_t copy = nullptr;
 		cudaStream_t recv = nullptr; // inter-process receives (never queued behind a spinning send)
+		cudaStream_t host_in = nullptr, host_out = nullptr; // host_write / host_read tasks (both PCIe directions at once)
 		size_t rr = 0;
 	};
 	struct peer_link {
@@ -236,6 +238,7 @@ class executor {
 	void run_recv(const task& t);
 	void run_reduce(const task& t);
 	void run_allreduce(const task& t);
+	void run_host_io(const task& t);
 	void finish_id(int64_t id, cudaStream_t s, int gpu);
 
 	// in-process allreduce groups: members issue in worker order, the last one combines

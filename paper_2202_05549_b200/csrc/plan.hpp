@@ -13,7 +13,7 @@ struct kernel_entry;
 
 namespace mtb {
 
-enum class task_kind : int32_t { create = 0, del = 1, execute = 2, copy = 3, send = 4, recv = 5, reduce = 6, allreduce = 7 };
+enum class task_kind : int32_t { create = 0, del = 1, execute = 2, copy = 3, send = 4, recv = 5, reduce = 6, allreduce = 7, host_write = 8, host_read = 9 };
 enum class fill_kind : int32_t { none = 0, zero = 1, one = 2, identity = 3 };
 enum class arg_kind : int32_t { scalar_int = 0, scalar_float = 1, chunk = 2, none = 3 };
 
@@ -51,7 +51,8 @@ struct task {
 	// copy
 	int64_t src = -1, dst = -1;
 	box src_region, dst_region;
-	// send / recv
+	// send / recv (host_write / host_read: tag = host address, src_region = host array box,
+	// region = the box copied)
 	int peer = -1;
 	uint64_t tag = 0;
 	// reduce / allreduce (group = tag, members with data = inputs, own member = output)
@@ -70,6 +71,8 @@ inline const char* task_kind_name(task_kind k) {
 	case task_kind::recv: return "recv";
 	case task_kind::reduce: return "reduce";
 	case task_kind::allreduce: return "allreduce";
+	case task_kind::host_write: return "host_write";
+	case task_kind::host_read: return "host_read";
 	}
 	return "?";
 }

@@ -604,4 +604,66 @@ std::pair<int64_t, int64_t> planner::launch(const std::string& kernel, const box
 	return {first, next_task_};
 }
 
+namespace {
+
+// a minus b as disjoint boxes (slab by slab along each axis)
+void subtract(const box& a, const box& b, std::vector<box>& out) {
+	if(!overlaps(a, b)) {
+		out.push_back(a);
+		return;
+	}
+	box rest = a;
+	for(int k = 0; k < a.rank(); ++k) {
+		if(rest.lo[k] < b.lo[k]) {
+			box s = rest;
+			s.hi[k] = b.lo[k];
+			out.push_back(s);
+			rest.lo[k] = b.lo[k];
+		}
+		if(rest.hi[k] > b.hi[k]) {
+			box s = rest;
+			s.lo[k] = b.hi[k];
+			out.push_back(s);
+			rest.hi[k] = b.hi[k];
+		}
+	}
+}
+
+} // namespace
+
+std::pair<int64_t, int64_t> planner::host_transfer(int64_t array_id, uint64_t host_addr, bool write) {
+	const array_rec& a = array(array_id);
+	const int64_t first = next_task_;
+	std::vector<box> covered;
+	for(const auto& c : a.chunks) {
+		std::vector<box> parts{c.region};
+		if(!write) {
+			for(const auto& done : covered) {
+				std::vector<box> next;
+				for(const auto& part : parts) subtract(part, done, next);
+				parts.swap(next);
+			}
+			covered.push_back(c.region);
+		}
+		for(const auto& r : parts) {
+			if(r.is_empty()) continue;
+			const int64_t tid = next_task_;
+			std::vector<int64_t> d;
+			record(c.id, tid, write, r, !write, d);
+			task t;
+			t.worker = c.home.worker;
+			t.resource = c.home;
+			t.kind = write ? task_kind::host_write : task_kind::host_read;
+			t.deps = std::move(d);
+			t.chunk = c.id;
+			t.region = r;
+			t.src_region = a.domain;
+			t.type = a.type;
+			t.tag = host_addr;
+			emit(std::move(t));
+		}
+	}
+	return {first, next_task_};
+}
+
 } // namespace mtb

@@ -63,6 +63,13 @@ class planner {
 	std::pair<int64_t, int64_t> launch(const std::string& kernel, const box& grid, const point& block, const std::vector<superblock>& work,
 	    const std::vector<launch_arg>& args, const annotation& ann);
 
+	// B200 extension: asynchronous host <-> array transfers planned as tasks, so they are
+	// ordered against launches by the same dependency tracking. write: every chunk's region
+	// from the host array (row-major over the domain); read: a disjoint cover of the domain
+	// (each cell from the lowest-id chunk holding it) into the host array. Returns the task
+	// range like launch().
+	std::pair<int64_t, int64_t> host_transfer(int64_t array_id, uint64_t host_addr, bool write);
+
 	std::vector<task> take_pending();
 	// context-local kernels shadow the global registry (the reference registers synthesized
 	// gather kernels per scenario, scenario.cpp:368-389)
