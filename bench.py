@@ -392,7 +392,7 @@ def run_reference_arm(args):
     sample = f"{rows}x{cols} rows sample of the {args.rows}x{args.cols} grid, {devices} chunks (stencil_dist halo [1,0]), 1 worker x {devices} device threads"
     print(json.dumps({
         "metric": METRIC, "impl": "reference", "value": rate, "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (ramp2d_f32 pattern)",
         "config": {"workload": "heat2d 2D 5-point stencil f32, row-block stencil distribution", "rows": rows, "cols": cols, "iterations_per_step": 1},
         "cpu_baseline": {"value": rate, "unit": "cell-updates/s", "cores": devices, "kind": "reference", "sample": sample},
