@@ -346,6 +346,18 @@ int mt_ctx_kernel_register(mt_ctx* ctx, const char* id, const mt_param_spec* par
  * body that folds the thread's read regions into its write/reduce regions */
 int mt_ctx_gather_register(mt_ctx* ctx, const char* id, const char* annotation_text, int32_t naccess, const int32_t* dtypes, const mt_rect* domains);
 int mt_kernel_info(int32_t index, char* id, int32_t id_cap, mt_param_spec* params, int32_t cap, int32_t* nparams);
+/* Runtime compilation, the paper's user model (wrapper kernels.cpp:522-596).
+ * `source` defines  __device__ void <id>(dim3 virtBlockIdx, <params in order>)  with scalars
+ * as int32_t/int64_t/float/double and arrays as manta::Vector<T> / Matrix<T> / Tensor<T>
+ * (const for read-only parameters; operator[] chains and operator() take GLOBAL indices).
+ * Per superblock the generated wrapper bakes the block offset and view offsets/strides as
+ * constants and NVRTC compiles it for sm_100a on first use (cached per device and instance).
+ * The source is compiled once here; compiler errors return MT_EVALIDATION with the log. */
+int mt_ctx_kernel_compile(mt_ctx* ctx, const char* id, const mt_param_spec* params, int32_t nparams, const char* source);
+/* the wrapper text for one instance (generate_wrapper_source, kernels.hpp:109-121):
+ * offsets/strides concatenated over the array parameters in signature order */
+int mt_wrapper_source(const char* id, const mt_param_spec* params, int32_t nparams, const int64_t* block_offset, int32_t rank, const int64_t* offsets,
+    const int64_t* strides, char* out, int64_t cap, int64_t* len);
 
 #ifdef __cplusplus
 }

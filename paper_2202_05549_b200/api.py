@@ -174,6 +174,34 @@ class PlanBuffer:
         return [_task_dict(t, self.pool, self.args) for t in self.tasks]
 
 
+def param_specs(params):
+    """[(name, "scalar"|"array", dtype, rank, writable), ...] -> mt_param_spec array"""
+    out = (capi.ParamSpec * max(1, len(params)))()
+    for i, (name, kind, dt, rank, writable) in enumerate(params):
+        out[i].name = name.encode()
+        out[i].kind = capi.PARAM_ARRAY if kind == "array" else capi.PARAM_SCALAR
+        out[i].dtype = capi.DTYPE_NAMES[dt]
+        out[i].rank = int(rank)
+        out[i].writable = int(bool(writable))
+    return out
+
+
+def wrapper_source(lib, kernel, params, block_offset, offsets, strides) -> str:
+    """The wrapper text one superblock instance compiles to (reference generate_wrapper_source,
+    kernels.cpp:540-596); offsets/strides: one list per array parameter."""
+    spec = param_specs(params)
+    bo = (C.c_int64 * max(1, len(block_offset)))(*block_offset)
+    flat_o = [v for o in offsets for v in o]
+    flat_s = [v for s_ in strides for v in s_]
+    o = (C.c_int64 * max(1, len(flat_o)))(*flat_o)
+    st = (C.c_int64 * max(1, len(flat_s)))(*flat_s)
+    n = C.c_int64(0)
+    lib.check(lib.wrapper_source(kernel.encode(), spec, len(params), bo, len(block_offset), o, st, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    lib.check(lib.wrapper_source(kernel.encode(), spec, len(params), bo, len(block_offset), o, st, buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
 def _nccl_library():
     """torch's bundled libnccl.so.2 (the one torch.distributed uses), else None (default search)"""
     try:
@@ -305,6 +333,14 @@ class Context:
         shape, t = self.shape_of(array_id)
         data = np.ascontiguousarray(data, dtype=_NP_DTYPE[t]).reshape(shape)
         self.lib.check(self.lib.array_write(self.h, array_id, data.ctypes.data, data.nbytes))
+
+    # -- runtime-compiled kernels -----------------------------------
+    def compile_kernel(self, kernel: str, params, source: str) -> None:
+        """Register `source` (a __device__ function named `kernel` taking the virtual block
+        index first, then `params` in order) for this context; compiled with NVRTC for
+        sm_100a now (errors raise ValidationError with the compiler log) and per superblock
+        instance on first launch."""
+        self.lib.check(self.lib.ctx_kernel_compile(self.h, kernel.encode(), param_specs(params), len(params), source.encode()))
 
     # -- asynchronous host transfers (planned as tasks; see mt_array_write_async) ---------
     def write_async(self, array_id: int, data) -> None:

@@ -7,6 +7,7 @@
 
 #include "executor.hpp"
 #include "planner.hpp"
+#include "rtc.hpp"
 
 using namespace mtb;
 
@@ -638,6 +639,33 @@ int mt_ctx_gather_register(mt_ctx* ctx, const char* id, const char* annotation_t
 		e.id = id;
 		ctx->owned.push_back(make_gather_kernel(annotation_text, types, doms, e));
 		ctx->plan->add_local_kernel(std::move(e));
+	});
+}
+
+int mt_ctx_kernel_compile(mt_ctx* ctx, const char* id, const mt_param_spec* params, int32_t nparams, const char* source) {
+	return guarded([&] {
+		if(!source) throw validation_error("kernel source must not be NULL");
+		kernel_entry e = make_entry(id, params, nparams, nullptr, nullptr);
+		ctx->owned.push_back(make_rtc_kernel(id, e.params, source, e));
+		ctx->plan->add_local_kernel(std::move(e));
+	});
+}
+
+int mt_wrapper_source(const char* id, const mt_param_spec* params, int32_t nparams, const int64_t* block_offset, int32_t rank, const int64_t* offsets,
+    const int64_t* strides, char* out, int64_t cap, int64_t* len) {
+	return guarded([&] {
+		const kernel_entry e = make_entry(id, params, nparams, nullptr, nullptr);
+		std::vector<std::vector<int64_t>> offs, sts;
+		size_t at = 0;
+		for(const auto& p : e.params) {
+			if(!p.is_array) continue;
+			offs.emplace_back(offsets + at, offsets + at + p.rank);
+			sts.emplace_back(strides + at, strides + at + p.rank);
+			at += static_cast<size_t>(p.rank);
+		}
+		const std::string s = wrapper_source(id, e.params, std::vector<int64_t>(block_offset, block_offset + rank), offs, sts);
+		*len = static_cast<int64_t>(s.size());
+		if(out && cap > *len) std::memcpy(out, s.c_str(), s.size() + 1);
 	});
 }
 
