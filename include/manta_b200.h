@@ -359,6 +359,12 @@ int mt_ctx_kernel_compile(mt_ctx* ctx, const char* id, const mt_param_spec* para
 int mt_wrapper_source(const char* id, const mt_param_spec* params, int32_t nparams, const int64_t* block_offset, int32_t rank, const int64_t* offsets,
     const int64_t* strides, char* out, int64_t cap, int64_t* len);
 
+/* ---- scenario fuzzing (make_fuzz_scenario, proj/src/scenario.cpp:653-807) ------------- */
+/* The reference's random scenario for `seed` as scenario-file JSON (scenario.cpp:131-167):
+ * same draws (std::mt19937_64, uniform_int_distribution) in the same order. Writes at most
+ * `cap` bytes including the NUL; *len receives the text length. */
+int mt_fuzz_scenario_json(uint64_t seed, char* buf, int64_t cap, int64_t* len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -825,6 +825,16 @@ int mr_scenario_plan(const char* json, int32_t workers, int32_t devices, int32_t
 	});
 }
 
+// export_dot (task.cpp:72-110) of the scenario's plan, to pin the product CLI's --dot output
+int mr_scenario_dot(const char* json, int32_t workers, int32_t devices, char* buf, int64_t cap, int64_t* len) {
+	return guarded([&] {
+		const auto sp = plan_scenario(scenario_from_json_text(json), make_overrides(workers, devices, 0, 0));
+		const std::string s = export_dot(sp.drv->plan());
+		*len = static_cast<int64_t>(s.size());
+		if(buf && cap > *len) std::memcpy(buf, s.c_str(), s.size() + 1);
+	});
+}
+
 // run_scenario (scenario.cpp:513-552): final arrays concatenated in scenario order
 int mr_scenario_run(const char* json, int32_t workers, int32_t devices, int32_t oracle_mode, int64_t ready_seed, int32_t use_seed, void* out,
     int64_t cap, int64_t* len, int32_t* coherent) {

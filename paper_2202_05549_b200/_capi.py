@@ -174,12 +174,13 @@ _SIGS = {
     "fuzz_scenario_json": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int64, P(C.c_int64)]),
     "scenario_plan": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(Task), C.c_int64, P(C.c_int64), P(C.c_int64),
                                 C.c_int64, P(C.c_int64), P(ArgBinding), C.c_int64, P(C.c_int64)]),
+    "scenario_dot": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_char_p, C.c_int64, P(C.c_int64)]),
     "scenario_run": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, P(C.c_int64),
                                P(C.c_int32)]),
     "kernel_info": (C.c_int, [C.c_int32, C.c_char_p, C.c_int32, P(ParamSpec), C.c_int32, P(C.c_int32)]),
 }
 # entry points the oracle shim may lack
-_OPTIONAL = {"exec_stats", "exec_last_stream", "kernel_info", "host_threads", "ctx_kernel_register", "fuzz_scenario_json", "scenario_plan",
+_OPTIONAL = {"exec_stats", "exec_last_stream", "kernel_info", "host_threads", "ctx_kernel_register", "fuzz_scenario_json", "scenario_plan", "scenario_dot",
              "scenario_run", "plan_accesses", "ctx_gather_register", "ctx_peer_export", "ctx_peer_import", "ctx_nccl_unique_id", "ctx_nccl_init", "array_write_async", "array_read_async", "ctx_kernel_compile", "wrapper_source", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
 
 

@@ -418,6 +418,15 @@ class Context:
         self.lib.check(self.lib.exec_stats(ex, out, len(keys)))
         return dict(zip(keys, [int(v) for v in out]))
 
+    def report_json(self) -> str:
+        """run_report::to_json of the attached executor (runtime.cpp:613-636)"""
+        ex = self._ex()
+        n = C.c_int64(0)
+        self.lib.check(self.lib.exec_report_json(ex, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self.lib.check(self.lib.exec_report_json(ex, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
     # -- one process per worker ------------------------------------------------------
     def peer_export(self) -> bytes:
         n = C.c_int64(0)

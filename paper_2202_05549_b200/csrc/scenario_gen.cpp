@@ -16,7 +16,6 @@
 #include <vector>
 
 #include "../../include/manta_b200.h"
-#include "errors.hpp"
 
 namespace {
 
@@ -45,8 +44,10 @@ std::string random_index(rng_t& rng, int rank) {
 	case 3: return ":" + random_expr(rng, rank);
 	default: {
 		const std::string center = random_expr(rng, rank);
-		const int lo = width(rng); // evaluation order of the reference's single expression
+		// the reference builds this in one operator+ chain; g++ evaluates the right-hand
+		// width(rng) first, so the upper width is drawn before the lower one
 		const int hi = width(rng);
+		const int lo = width(rng);
 		return center + "-" + std::to_string(lo) + ":" + center + "+" + std::to_string(hi);
 	}
 	}
