@@ -493,15 +493,18 @@ def run_b200(args):
                 times.append(dt)
         seq = rows * cols * args.e2e_iters * ws / (sum(times) / len(times))
         # (2) pipelined: the same steps queued back to back through mt_array_write_async /
-        # mt_array_read_async on two array sets, so step s+1's upload and step s-1's download
-        # (both PCIe directions) overlap step s's iterations; every step still moves its whole
+        # mt_array_read_async on `e2e_sets` array sets (triple buffering by default), so step
+        # s+1's upload (into a set nobody uses) and step s-1's download (from another) run in
+        # both PCIe directions at once under step s's iterations; with two sets the upload
+        # would wait for the download from the same set. Every step still moves its whole
         # input in and its whole result out inside the timed region
         pipe = None
         if args.e2e_pipeline > 0:
-            sets = [(a, b), setup_heat(ctx, rows, cols, ws)[:2]]
+            nsets = max(2, args.e2e_sets)
+            sets = [(a, b)] + [setup_heat(ctx, rows, cols, ws)[:2] for _ in range(nsets - 1)]
 
             def pstep(s):
-                x, y = sets[s % 2]
+                x, y = sets[s % nsets]
                 ctx.write_async(x, host_in)
                 for _ in range(args.e2e_iters):
                     ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(y), Arr(x)], ANN)
@@ -517,15 +520,16 @@ def run_b200(args):
             ctx.synchronize()
             pdt = time.perf_counter() - t0
             pipe = rows * cols * args.e2e_iters * args.e2e_pipeline / pdt
-            for arr in sets[1]:
-                ctx.delete_array(arr)
+            for st in sets[1:]:
+                for arr in st:
+                    ctx.delete_array(arr)
             ctx.synchronize()
         dt = barrier_max(max(times), ws) if times else float("nan")
         e2e = {"value": pipe if pipe else seq, "unit": "cell-updates/s", "h2d_bytes_per_step": rows * cols * 4, "d2h_bytes_per_step": rows * cols * 4,
                "iterations_per_step": args.e2e_iters, "steps": args.e2e_pipeline if pipe else len(times),
                "note": ("step = upload the grid from pinned host memory + e2e iterations + read the grid back, through the public API; "
-                        + ("steps pipelined with mt_array_write_async / mt_array_read_async over two array sets (uploads, downloads and "
-                           "kernels overlap)" if pipe else "synchronous mt_array_write / mt_array_read")),
+                        + (f"steps pipelined with mt_array_write_async / mt_array_read_async over {max(2, args.e2e_sets)} array sets (uploads, "
+                           "downloads and kernels overlap)" if pipe else "synchronous mt_array_write / mt_array_read")),
                "sequential": {"value": seq, "steps": len(times), "worst_step_s": dt,
                               "note": "each step synchronous: mt_array_write, iterations, mt_array_read"}}
         del host_in, host_out
@@ -606,6 +610,7 @@ def main():
     p.add_argument("--e2e-iters", type=int, default=100)
     p.add_argument("--e2e-runs", type=int, default=2)
     p.add_argument("--e2e-pipeline", type=int, default=8, help="pipelined e2e steps (0: report the sequential e2e)")
+    p.add_argument("--e2e-sets", type=int, default=3, help="array sets the pipelined e2e steps rotate over")
     p.add_argument("--ref-rows", type=int, default=512)
     p.add_argument("--ref-iters", type=int, default=6)
     p.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
