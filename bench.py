@@ -430,7 +430,7 @@ def run_b200(args):
         gloo = dist.new_group(backend="gloo")
         ctx = mb.context(workers=ws, devices=1, worker_rank=rank, gpu_base=gpu)
         ctx.connect_peers(gloo)
-        args.e2e_runs, args.matmul_n, args.c4 = 0, 0, False  # single-GPU legs: rank-local runs only at N=1
+        args.matmul_n, args.c4 = 0, False  # the C3/C4 legs are single-GPU workloads: reported at N=1 only
     else:
         ctx = mb.context(workers=1, devices=1, num_gpus=1)
     a, b, work = setup_heat(ctx, rows, cols, ws, strip=args.strip if ws > 1 else 0)
@@ -475,23 +475,54 @@ def run_b200(args):
     # e2e through the public API with host buffers
     e2e = None
     if args.e2e_runs > 0:
-        host_in = torch.empty((rows, cols), dtype=torch.float32, pin_memory=True)
-        host_out = [torch.empty((rows, cols), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        # host buffers: the whole grid at N=1; at N>1 each rank holds only its chunk's box
+        # (rows of its block plus halo rows) and moves it with mt_array_{write,read}_box_async,
+        # so the job as a whole uploads and downloads the grid once per step
+        box = None
+        if ws > 1:
+            mine = [c for c in ctx.chunks(a) if c.home[0] == rank][0]
+            box = (mine.lo, mine.hi)
+        hshape = (rows, cols) if box is None else (box[1][0] - box[0][0], cols)
+        host_in = (torch.empty if box is None else torch.zeros)(hshape, dtype=torch.float32, pin_memory=True)
+        host_out = [torch.empty(hshape, dtype=torch.float32, pin_memory=True) for _ in range(2)]
         hin = host_in.numpy()
         hout = host_out[0].numpy()
-        ctx.lib.check(ctx.lib.array_read(ctx.h, a, hin.ctypes.data, hin.nbytes))
+        if box is None:
+            ctx.lib.check(ctx.lib.array_read(ctx.h, a, hin.ctypes.data, hin.nbytes))
+        else:
+            ctx.read_async(a, host_in, box=box)
+            ctx.synchronize()
+        # whole job per step: every chunk is uploaded whole (halo rows included), every cell is
+        # downloaded once (from the lowest-id chunk holding it)
+        h2d_bytes = 4 * sum((c.hi[0] - c.lo[0]) * (c.hi[1] - c.lo[1]) for c in ctx.chunks(a)) if box else rows * cols * 4
+        d2h_bytes = rows * cols * 4
+
+        def sync_barrier():
+            ctx.synchronize()
+            if ws > 1:
+                import torch.distributed as dist
+                dist.barrier()
+
         # (1) sequential: each step uploads the grid, iterates, reads the grid back, synchronously
         times = []
         for run in range(args.e2e_runs + 1):
+            sync_barrier()
             t0 = time.perf_counter()
-            ctx.lib.check(ctx.lib.array_write(ctx.h, a, hin.ctypes.data, hin.nbytes))
+            if box is None:
+                ctx.lib.check(ctx.lib.array_write(ctx.h, a, hin.ctypes.data, hin.nbytes))
+            else:
+                ctx.write_async(a, host_in, box=box)
             for _ in range(args.e2e_iters):
                 step()
-            ctx.lib.check(ctx.lib.array_read(ctx.h, a, hout.ctypes.data, hout.nbytes))
-            dt = time.perf_counter() - t0
+            if box is None:
+                ctx.lib.check(ctx.lib.array_read(ctx.h, a, hout.ctypes.data, hout.nbytes))
+            else:
+                ctx.read_async(a, host_out[0], box=box)
+                ctx.synchronize()
+            dt = barrier_max(time.perf_counter() - t0, ws)
             if run > 0:  # first run is warm-up
                 times.append(dt)
-        seq = rows * cols * args.e2e_iters * ws / (sum(times) / len(times))
+        seq = rows * cols * args.e2e_iters / (sum(times) / len(times))
         # (2) pipelined: the same steps queued back to back through mt_array_write_async /
         # mt_array_read_async on `e2e_sets` array sets (triple buffering by default), so step
         # s+1's upload (into a set nobody uses) and step s-1's download (from another) run in
@@ -501,37 +532,39 @@ def run_b200(args):
         pipe = None
         if args.e2e_pipeline > 0:
             nsets = max(2, args.e2e_sets)
-            sets = [(a, b)] + [setup_heat(ctx, rows, cols, ws)[:2] for _ in range(nsets - 1)]
+            sets = [(a, b)] + [setup_heat(ctx, rows, cols, ws, strip=args.strip if ws > 1 else 0)[:2] for _ in range(nsets - 1)]
 
             def pstep(s):
                 x, y = sets[s % nsets]
-                ctx.write_async(x, host_in)
+                ctx.write_async(x, host_in, box=box)
                 for _ in range(args.e2e_iters):
                     ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(y), Arr(x)], ANN)
                     x, y = y, x
-                ctx.read_async(x, host_out[s % 2])
+                ctx.read_async(x, host_out[s % 2], box=box)
                 ctx.flush()
 
             pstep(0)
-            ctx.synchronize()
+            sync_barrier()
             t0 = time.perf_counter()
             for s in range(args.e2e_pipeline):
                 pstep(s)
             ctx.synchronize()
-            pdt = time.perf_counter() - t0
+            pdt = barrier_max(time.perf_counter() - t0, ws)
             pipe = rows * cols * args.e2e_iters * args.e2e_pipeline / pdt
             for st in sets[1:]:
                 for arr in st:
                     ctx.delete_array(arr)
             ctx.synchronize()
-        dt = barrier_max(max(times), ws) if times else float("nan")
-        e2e = {"value": pipe if pipe else seq, "unit": "cell-updates/s", "h2d_bytes_per_step": rows * cols * 4, "d2h_bytes_per_step": rows * cols * 4,
+        dt = max(times) if times else float("nan")
+        e2e = {"value": pipe if pipe else seq, "unit": "cell-updates/s", "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
                "iterations_per_step": args.e2e_iters, "steps": args.e2e_pipeline if pipe else len(times),
-               "note": ("step = upload the grid from pinned host memory + e2e iterations + read the grid back, through the public API; "
+               "note": ("step = upload the grid from pinned host memory + e2e iterations + read the grid back, through the public API"
+                        + (" (each rank its own chunk box, mt_array_*_box_async)" if box else "") + "; "
                         + (f"steps pipelined with mt_array_write_async / mt_array_read_async over {max(2, args.e2e_sets)} array sets (uploads, "
-                           "downloads and kernels overlap)" if pipe else "synchronous mt_array_write / mt_array_read")),
+                           "downloads and kernels overlap)" if pipe else "synchronous mt_array_write / mt_array_read")
+                        + "; wall clock, max over ranks"),
                "sequential": {"value": seq, "steps": len(times), "worst_step_s": dt,
-                              "note": "each step synchronous: mt_array_write, iterations, mt_array_read"}}
+                              "note": "each step synchronous: upload, iterations, download"}}
         del host_in, host_out
 
     cpu = None
@@ -609,7 +642,7 @@ def main():
     p.add_argument("--cols", type=int, default=65536)
     p.add_argument("--e2e-iters", type=int, default=100)
     p.add_argument("--e2e-runs", type=int, default=2)
-    p.add_argument("--e2e-pipeline", type=int, default=8, help="pipelined e2e steps (0: report the sequential e2e)")
+    p.add_argument("--e2e-pipeline", type=int, default=24, help="pipelined e2e steps (0: report the sequential e2e)")
     p.add_argument("--e2e-sets", type=int, default=3, help="array sets the pipelined e2e steps rotate over")
     p.add_argument("--ref-rows", type=int, default=512)
     p.add_argument("--ref-iters", type=int, default=6)

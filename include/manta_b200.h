@@ -236,6 +236,12 @@ int mt_array_write(mt_ctx* ctx, int64_t array_id, const void* host, uint64_t byt
  * (runtime.cpp:697-712 read_chunk) in pipelines that stream inputs and results. */
 int mt_array_write_async(mt_ctx* ctx, int64_t id, const void* host, uint64_t bytes);
 int mt_array_read_async(mt_ctx* ctx, int64_t id, void* host, uint64_t bytes);
+/* The same with a host array that covers only `host_box` (row-major over it). Task planning
+ * does not depend on the box, so in a one-process-per-GPU job every rank calls it collectively
+ * with its own box and buffer (e.g. its chunks' rows) and the ranks' plans stay identical;
+ * every transfer a rank executes must lie inside that rank's box (MT_EEXEC otherwise). */
+int mt_array_write_box_async(mt_ctx* ctx, int64_t id, const mt_rect* host_box, const void* host, uint64_t bytes);
+int mt_array_read_box_async(mt_ctx* ctx, int64_t id, const mt_rect* host_box, void* host, uint64_t bytes);
 /* Byte-compares every overlapping chunk pair (check_replicas, scenario.cpp:486-509);
  * *coherent = 1 when all agree. */
 int mt_array_check_replicas(mt_ctx* ctx, int64_t array_id, int32_t* coherent);

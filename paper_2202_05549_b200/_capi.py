@@ -169,6 +169,8 @@ _SIGS = {
     "ctx_kernel_compile": (C.c_int, [C.c_void_p, C.c_char_p, P(ParamSpec), C.c_int32, C.c_char_p]),
     "wrapper_source": (C.c_int, [C.c_char_p, P(ParamSpec), C.c_int32, P(C.c_int64), C.c_int32, P(C.c_int64), P(C.c_int64), C.c_char_p, C.c_int64,
                                  P(C.c_int64)]),
+    "array_write_box_async": (C.c_int, [C.c_void_p, C.c_int64, P(Rect), C.c_void_p, C.c_uint64]),
+    "array_read_box_async": (C.c_int, [C.c_void_p, C.c_int64, P(Rect), C.c_void_p, C.c_uint64]),
     "array_read_async": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_uint64]),
     "ctx_nccl_init": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p]),
     "fuzz_scenario_json": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int64, P(C.c_int64)]),
@@ -181,7 +183,7 @@ _SIGS = {
 }
 # entry points the oracle shim may lack
 _OPTIONAL = {"exec_stats", "exec_last_stream", "kernel_info", "host_threads", "ctx_kernel_register", "fuzz_scenario_json", "scenario_plan", "scenario_dot",
-             "scenario_run", "plan_accesses", "ctx_gather_register", "ctx_peer_export", "ctx_peer_import", "ctx_nccl_unique_id", "ctx_nccl_init", "array_write_async", "array_read_async", "ctx_kernel_compile", "wrapper_source", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
+             "scenario_run", "plan_accesses", "ctx_gather_register", "ctx_peer_export", "ctx_peer_import", "ctx_nccl_unique_id", "ctx_nccl_init", "array_write_async", "array_read_async", "array_write_box_async", "array_read_box_async", "ctx_kernel_compile", "wrapper_source", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
 
 
 class MantaError(RuntimeError):

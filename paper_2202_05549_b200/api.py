@@ -343,30 +343,42 @@ class Context:
         self.lib.check(self.lib.ctx_kernel_compile(self.h, kernel.encode(), param_specs(params), len(params), source.encode()))
 
     # -- asynchronous host transfers (planned as tasks; see mt_array_write_async) ---------
-    def write_async(self, array_id: int, data) -> None:
+    def write_async(self, array_id: int, data, box=None) -> None:
         """Queue an upload of `data` (C-contiguous, the array's shape and dtype; numpy or a
         pinned torch tensor) into every chunk. The buffer must stay untouched until
-        synchronize(); the context keeps a reference until then."""
-        ptr, nbytes = self._host_buffer(array_id, data)
-        self.lib.check(self.lib.array_write_async(self.h, array_id, ptr, nbytes))
+        synchronize(); the context keeps a reference until then. With `box` = (lo, hi) the
+        buffer holds only that box of the array (one process per GPU: each rank passes its
+        own chunks' box; mt_array_write_box_async)."""
+        ptr, nbytes = self._host_buffer(array_id, data, box)
+        if box is None:
+            self.lib.check(self.lib.array_write_async(self.h, array_id, ptr, nbytes))
+        else:
+            r = capi.Rect.make(*box)
+            self.lib.check(self.lib.array_write_box_async(self.h, array_id, C.byref(r), ptr, nbytes))
         self._inflight.append(data)
 
-    def read_async(self, array_id: int, out) -> None:
-        """Queue a download of the array into `out` (C-contiguous, the array's shape and dtype);
-        valid after synchronize()."""
-        ptr, nbytes = self._host_buffer(array_id, out)
-        self.lib.check(self.lib.array_read_async(self.h, array_id, ptr, nbytes))
+    def read_async(self, array_id: int, out, box=None) -> None:
+        """Queue a download of the array into `out` (C-contiguous, the array's shape and dtype,
+        or the shape of `box`); valid after synchronize()."""
+        ptr, nbytes = self._host_buffer(array_id, out, box)
+        if box is None:
+            self.lib.check(self.lib.array_read_async(self.h, array_id, ptr, nbytes))
+        else:
+            r = capi.Rect.make(*box)
+            self.lib.check(self.lib.array_read_box_async(self.h, array_id, C.byref(r), ptr, nbytes))
         self._inflight.append(out)
 
-    def _host_buffer(self, array_id, buf):
+    def _host_buffer(self, array_id, buf, box=None):
         shape, t = self.shape_of(array_id)
+        if box is not None:
+            shape = [h - l for l, h in zip(*box)]
         if isinstance(buf, np.ndarray):
             if not buf.flags["C_CONTIGUOUS"] or buf.dtype != np.dtype(_NP_DTYPE[t]) or list(buf.shape) != list(shape):
-                raise ValidationError("host buffer must be C-contiguous with the array's shape and dtype")
+                raise ValidationError("host buffer must be C-contiguous with the array's (or the box's) shape and dtype")
             return buf.ctypes.data, buf.nbytes
         # torch tensor (e.g. pinned host memory)
         if buf.is_cuda or not buf.is_contiguous() or list(buf.shape) != list(shape):
-            raise ValidationError("host buffer must be a contiguous host tensor with the array's shape")
+            raise ValidationError("host buffer must be a contiguous host tensor with the array's (or the box's) shape")
         return buf.data_ptr(), buf.numel() * buf.element_size()
 
     def replicas_coherent(self, array_id: int) -> bool:

@@ -429,6 +429,28 @@ int mt_array_read_async(mt_ctx* ctx, int64_t id, void* host, uint64_t bytes) {
 	});
 }
 
+namespace {
+int host_box_transfer(mt_ctx* ctx, int64_t id, const mt_rect* host_box, uint64_t host, uint64_t bytes, bool write) {
+	return guarded([&] {
+		const array_rec& a = ctx->plan->array(id);
+		if(!host_box) throw validation_error("host box is required");
+		const box hb = to_box(*host_box);
+		if(hb.rank() != a.domain.rank() || hb.is_empty() || !encloses(a.domain, hb)) throw validation_error("host box must be a non-empty box inside the array's domain");
+		if(bytes < static_cast<uint64_t>(hb.volume()) * dtype_size(a.type)) throw validation_error("host buffer too small");
+		ctx->plan->host_transfer(id, host, write, &hb);
+		flush(ctx);
+	});
+}
+} // namespace
+
+int mt_array_write_box_async(mt_ctx* ctx, int64_t id, const mt_rect* host_box, const void* host, uint64_t bytes) {
+	return host_box_transfer(ctx, id, host_box, reinterpret_cast<uint64_t>(host), bytes, true);
+}
+
+int mt_array_read_box_async(mt_ctx* ctx, int64_t id, const mt_rect* host_box, void* host, uint64_t bytes) {
+	return host_box_transfer(ctx, id, host_box, reinterpret_cast<uint64_t>(host), bytes, false);
+}
+
 int mt_array_check_replicas(mt_ctx* ctx, int64_t id, int32_t* coherent) {
 	return guarded([&] {
 		mt_exec& e = need_exec(ctx);

@@ -631,8 +631,12 @@ void subtract(const box& a, const box& b, std::vector<box>& out) {
 
 } // namespace
 
-std::pair<int64_t, int64_t> planner::host_transfer(int64_t array_id, uint64_t host_addr, bool write) {
+std::pair<int64_t, int64_t> planner::host_transfer(int64_t array_id, uint64_t host_addr, bool write, const box* host_box) {
 	const array_rec& a = array(array_id);
+	// the host array covers `host_box` (default: the whole domain). The tasks do not depend on
+	// it, so ranks of a one-process-per-GPU job that each pass their own box and buffer still
+	// plan identical task sequences; a task's region must lie inside the box on the rank that
+	// executes it (checked by the executor)
 	const int64_t first = next_task_;
 	std::vector<box> covered;
 	for(const auto& c : a.chunks) {
@@ -657,7 +661,7 @@ std::pair<int64_t, int64_t> planner::host_transfer(int64_t array_id, uint64_t ho
 			t.deps = std::move(d);
 			t.chunk = c.id;
 			t.region = r;
-			t.src_region = a.domain;
+			t.src_region = host_box ? *host_box : a.domain;
 			t.type = a.type;
 			t.tag = host_addr;
 			emit(std::move(t));

@@ -68,7 +68,7 @@ class planner {
 	// from the host array (row-major over the domain); read: a disjoint cover of the domain
 	// (each cell from the lowest-id chunk holding it) into the host array. Returns the task
 	// range like launch().
-	std::pair<int64_t, int64_t> host_transfer(int64_t array_id, uint64_t host_addr, bool write);
+	std::pair<int64_t, int64_t> host_transfer(int64_t array_id, uint64_t host_addr, bool write, const box* host_box = nullptr);
 
 	std::vector<task> take_pending();
 	// context-local kernels shadow the global registry (the reference registers synthesized

@@ -176,3 +176,68 @@ def test_two_process_nccl_allreduce(okern):
     okern.oracle_histogram_hashed(C.c_int64(0), C.c_int64(n), C.c_int64(bins), C.c_int64(5), want.ctypes.data_as(C.POINTER(C.c_int64)))
     for _, _, h in res:
         assert np.array_equal(h, want)
+
+
+def _heat_box_rank(rank, world, port, rows, cols, iters, q):
+    """each rank uploads and downloads only its own chunk's box (mt_array_*_box_async)"""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+    ctx = mb.context(workers=world, devices=1, worker_rank=rank, gpu_base=0)
+    ctx.connect_peers()
+    devs = ctx.devices
+    dist_ = lambda: ctx.dist.stencil([rows, cols], [rows // world, cols], [1, 0], devs)  # noqa: E731
+    a = ctx.create_array([rows, cols], "f32", dist_(), 0)
+    b = ctx.create_array([rows, cols], "f32", dist_(), 0)
+    work = ctx.dist.block_work([rows, cols], [16, 16], [rows // world, cols], devs)
+    mine = [c for c in ctx.chunks(a) if c.home[0] == rank][0]
+    box = (mine.lo, mine.hi)
+    full = np.random.default_rng(11).standard_normal((rows, cols)).astype(np.float32)
+    host_in = torch.from_numpy(full[mine.lo[0]:mine.hi[0]].copy()).pin_memory()
+    host_out = torch.full((mine.hi[0] - mine.lo[0], cols), float("nan"), dtype=torch.float32).pin_memory()
+    ctx.write_async(a, host_in, box=box)
+    for _ in range(iters):
+        ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT)
+        a, b = b, a
+    ctx.read_async(a, host_out, box=box)
+    ctx.synchronize()
+    per = rows // world
+    lo = 0 if rank == 0 else rank * per + 1  # rows this rank's read tasks cover (lowest-id chunk)
+    hi = min(rows, (rank + 1) * per + 1)
+    q.put((rank, host_out.numpy()[lo - mine.lo[0]:hi - mine.lo[0]].copy(), lo, hi))
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_two_process_box_host_io_matches_single_process():
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+    rows, cols, iters, world = 256, 512, 3, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_heat_box_rank, args=(r, world, port, rows, cols, iters, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert [(p[2], p[3]) for p in parts] == [(0, rows // 2 + 1), (rows // 2 + 1, rows)]
+    got = np.concatenate([p[1] for p in parts])
+    full = np.random.default_rng(11).standard_normal((rows, cols)).astype(np.float32)
+    with mb.context(workers=1, devices=world, num_gpus=1) as c:
+        devs = c.devices
+        a = c.create_array([rows, cols], "f32", c.dist.stencil([rows, cols], [rows // world, cols], [1, 0], devs), 0)
+        b = c.create_array([rows, cols], "f32", c.dist.stencil([rows, cols], [rows // world, cols], [1, 0], devs), 0)
+        w = c.dist.block_work([rows, cols], [16, 16], [rows // world, cols], devs)
+        c.write(a, full)
+        for _ in range(iters):
+            c.launch("heat2d", [rows, cols], [16, 16], w, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT)
+            a, b = b, a
+        want = c.read(a)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))

@@ -91,3 +91,36 @@ def test_pipelined_host_io_matches_synchronous():
     for g, x in zip(got, want):
         assert np.array_equal(g.view(np.uint32), x.view(np.uint32))
     assert st["host_read_bytes"] == steps * rows * cols * 4
+
+
+def test_box_transfers_plan_the_same_tasks():
+    """the host box changes only the host side of each task (src_region), never the task
+    sequence, so ranks passing different boxes keep identical plans; bad boxes are rejected"""
+    rows, cols = 256, 64
+
+    def plan(box):
+        with mb.context(workers=2, devices=1, execute=False) as ctx:
+            devs = ctx.devices
+            d = ctx.dist.stencil([rows, cols], [rows // 2, cols], [1, 0], devs)
+            a = ctx.create_array([rows, cols], "f32", d, 0)
+            r = mb._capi.Rect.make(*box) if box else None
+            vol = rows * cols if box is None else _vol(box) * 1
+            if box is None:
+                ctx.lib.check(ctx.lib.array_write_async(ctx.h, a, 0x1000, vol * 4))
+                ctx.lib.check(ctx.lib.array_read_async(ctx.h, a, 0x1000, vol * 4))
+            else:
+                ctx.lib.check(ctx.lib.array_write_box_async(ctx.h, a, r, 0x1000, vol * 4))
+                ctx.lib.check(ctx.lib.array_read_box_async(ctx.h, a, r, 0x1000, vol * 4))
+            return [{k: v for k, v in t.items() if k != "host_box"} for t in ctx.plan()], [t.get("host_box") for t in ctx.plan()]
+
+    base, _ = plan(None)
+    for box in [((0, 0), (129, 64)), ((127, 0), (256, 64))]:
+        tasks, boxes = plan(box)
+        assert tasks == base
+        assert all(b == box for b in boxes if b is not None)
+    with mb.context(workers=1, devices=1, execute=False) as ctx:
+        a = ctx.create_array([rows, cols], "f32", ctx.dist.single([rows, cols], ctx.devices[0]), 0)
+        with pytest.raises(mb.ValidationError):
+            ctx.lib.check(ctx.lib.array_write_box_async(ctx.h, a, mb._capi.Rect.make((0, 0), (rows + 1, cols)), 0x1000, (rows + 1) * cols * 4))
+        with pytest.raises(mb.ValidationError):
+            ctx.lib.check(ctx.lib.array_write_box_async(ctx.h, a, mb._capi.Rect.make((0, 0), (8, cols)), 0x1000, 8 * cols * 4 - 4))
