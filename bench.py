@@ -428,11 +428,11 @@ def run_b200(args):
         # (functional test of the multi-process path on a single-GPU box)
         dist.init_process_group("nccl" if torch.cuda.device_count() >= ws else "gloo")
         gloo = dist.new_group(backend="gloo")
-        ctx = mb.context(workers=ws, devices=1, worker_rank=rank, gpu_base=gpu)
+        ctx = mb.context(workers=ws, devices=1, worker_rank=rank, gpu_base=gpu, retain_plan=False)
         ctx.connect_peers(gloo)
         args.matmul_n, args.c4 = 0, False  # the C3/C4 legs are single-GPU workloads: reported at N=1 only
     else:
-        ctx = mb.context(workers=1, devices=1, num_gpus=1)
+        ctx = mb.context(workers=1, devices=1, num_gpus=1, retain_plan=False)
     a, b, work = setup_heat(ctx, rows, cols, ws, strip=args.strip if ws > 1 else 0)
     ctx.synchronize()
 

@@ -178,7 +178,8 @@ typedef struct mt_config {
 	                                   (NCCL between processes, a peer-memory combine in one process)
 	                                   instead of send-to-root / root reduce / send-back
 	                                   (planner.cpp:389-517); 0: the reference's tree */
-	int32_t pad_;
+	int32_t drop_executed_tasks;    /* 1: forget tasks once handed to the executor (long runs; mt_plan_export
+	                                   then sees only tasks not yet flushed); 0: retain the whole plan */
 } mt_config;
 
 /* One planned chunk access (a create counts as a write of the whole chunk). */

@@ -217,7 +217,7 @@ class Context:
 
     def __init__(self, lib: capi.Lib, workers=1, devices=1, execute=True, compat_deps=False, suppress_conflict_deps=False,
                  num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0, record_accesses=False,
-                 lookahead_tasks=0, worker_rank=None, gpu_base=0, collective_reduce=False):
+                 lookahead_tasks=0, worker_rank=None, gpu_base=0, collective_reduce=False, retain_plan=True):
         self.lib = lib
         self.dist = Distributions(lib)
         cfg = capi.Config()
@@ -233,6 +233,7 @@ class Context:
         cfg.record_accesses = int(record_accesses)
         cfg.lookahead_tasks = int(lookahead_tasks)
         cfg.collective_reduce = int(collective_reduce)
+        cfg.drop_executed_tasks = int(not retain_plan)  # long runs: forget tasks once queued
         if worker_rank is not None:  # one process per worker
             cfg.single_worker, cfg.worker_rank, cfg.gpu_base = 1, int(worker_rank), int(gpu_base)
         self.single_worker = worker_rank is not None
@@ -243,6 +244,7 @@ class Context:
         self.executes = bool(execute)
         self._arrays: dict[int, tuple] = {}
         self._inflight: list = []  # host buffers of queued async transfers
+        self._work_cache: dict = {}
 
     def close(self):
         if self.h:
@@ -291,10 +293,16 @@ class Context:
     def launch(self, kernel: str, grid, block, work: Sequence[Superblock], args: Iterable, annotation: str):
         g = _domain(grid)
         b = (C.c_int64 * 3)(*block)
-        w = (capi.Superblock * max(1, len(work)))()
-        for i, s in enumerate(work):
-            w[i].blocks = capi.Rect.make(s.lo, s.hi)
-            w[i].device = capi.Device(*s.device)
+        key = tuple(work)  # iterative launches reuse one decomposition: convert it once
+        w = self._work_cache.get(key)
+        if w is None:
+            w = (capi.Superblock * max(1, len(work)))()
+            for i, s in enumerate(work):
+                w[i].blocks = capi.Rect.make(s.lo, s.hi)
+                w[i].device = capi.Device(*s.device)
+            if len(self._work_cache) > 64:
+                self._work_cache.clear()
+            self._work_cache[key] = w
         args = list(args)
         la = (capi.LaunchArg * max(1, len(args)))()
         for i, a in enumerate(args):

@@ -266,8 +266,18 @@ void submit_tasks(mt_exec& e, const std::vector<task>& ts) {
 }
 
 void flush(mt_ctx* ctx) {
-	auto pending = ctx->plan->take_pending();
-	if(ctx->exec && !pending.empty()) submit_tasks(*ctx->exec, pending);
+	if(!ctx->exec) {
+		ctx->plan->consume_pending([](const task&) {});
+		return;
+	}
+	mt_exec& e = *ctx->exec;
+	bool any = false;
+	ctx->plan->consume_pending([&](const task& t) {
+		if(t.kind == task_kind::create) e.chunk_geom[t.chunk] = {t.region, t.type};
+		e.ex->submit_one(t);
+		any = true;
+	});
+	if(any) e.ex->end_submit();
 }
 
 mt_exec& need_exec(mt_ctx* ctx) {
@@ -319,6 +329,7 @@ int mt_ctx_create(const mt_config* cfg, mt_ctx** out) {
 		pc.compat_deps = cfg->compat_deps != 0;
 		pc.record_accesses = cfg->record_accesses != 0;
 		pc.collective_reduce = cfg->collective_reduce != 0;
+		pc.retain_plan = cfg->drop_executed_tasks == 0;
 		ctx->plan = std::make_unique<planner>(pc);
 		if(cfg->execute) {
 			ctx->exec = std::make_unique<mt_exec>();
@@ -493,7 +504,7 @@ int mt_plan_export(mt_ctx* ctx, int64_t first, int64_t last, mt_task* tasks, int
 	});
 }
 
-int64_t mt_plan_size(mt_ctx* ctx) { return static_cast<int64_t>(ctx->plan->plan().size()); }
+int64_t mt_plan_size(mt_ctx* ctx) { return ctx->plan->next_id(); }
 
 int mt_plan_accesses(mt_ctx* ctx, mt_access* out, int64_t cap, int64_t* n_out) {
 	return guarded([&] {

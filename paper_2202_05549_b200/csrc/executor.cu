@@ -451,15 +451,21 @@ void executor::retire_completed() {
 }
 
 void executor::submit(const std::vector<task>& tasks) {
-	for(const auto& t : tasks) {
-		if(t.id <= last_id_) throw validation_error("tasks must be submitted in ascending id order");
-		last_id_ = t.id;
-		if(cfg_.local_workers >= 0 && (t.worker < cfg_.first_worker || t.worker >= cfg_.first_worker + cfg_.local_workers)) continue;
-		if(spill_)
-			queue_.push_back(t);
-		else
-			issue(t);
-	}
+	for(const auto& t : tasks) submit_one(t);
+	end_submit();
+}
+
+void executor::submit_one(const task& t) {
+	if(t.id <= last_id_) throw validation_error("tasks must be submitted in ascending id order");
+	last_id_ = t.id;
+	if(cfg_.local_workers >= 0 && (t.worker < cfg_.first_worker || t.worker >= cfg_.first_worker + cfg_.local_workers)) return;
+	if(spill_)
+		queue_.push_back(t);
+	else
+		issue(t);
+}
+
+void executor::end_submit() {
 	if(spill_) drain(false);
 }
 

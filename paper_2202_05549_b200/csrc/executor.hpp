@@ -69,6 +69,9 @@ class executor {
 	executor& operator=(const executor&) = delete;
 
 	void submit(const std::vector<task>& tasks);
+	// the same one task at a time: submit_one for each (ascending ids), then end_submit
+	void submit_one(const task& t);
+	void end_submit();
 	void sync();
 	// host transfers: `host` holds the row-major box `host_box`; `region` is copied. Both
 	// synchronise the chunk's GPU first (call after the tasks that produce the data).

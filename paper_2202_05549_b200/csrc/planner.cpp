@@ -42,7 +42,7 @@ const kernel_entry* planner::find_kernel(const std::string& id) const {
 
 std::vector<task> planner::take_pending() {
 	std::vector<task> out;
-	out.swap(pending_);
+	consume_pending([&](const task& t) { out.push_back(t); });
 	return out; // already in id order: ids are assigned at emission
 }
 
@@ -51,8 +51,7 @@ int64_t planner::emit(task&& t) {
 	t.deps.erase(std::unique(t.deps.begin(), t.deps.end()), t.deps.end());
 	t.id = next_task_++;
 	task_worker_.push_back(t.worker);
-	if(cfg_.retain_plan) plan_.push_back(t);
-	pending_.push_back(std::move(t));
+	plan_.push_back(std::move(t));
 	return next_task_ - 1;
 }
 

@@ -7,6 +7,7 @@
 // reference's O(S^2 + S*C), so many launches can be planned ahead of GPU execution.
 #pragma once
 
+#include <deque>
 #include <map>
 #include <memory>
 #include <unordered_map>
@@ -23,7 +24,7 @@ struct planner_config {
 	int devices_per_worker = 1;
 	bool suppress_conflict_deps = false;
 	bool compat_deps = false;
-	bool retain_plan = true; // keep every emitted task for mt_plan_export
+	bool retain_plan = true; // keep every emitted task for mt_plan_export (else drop them once taken)
 	bool record_accesses = false;
 	// cross-worker reduce trees as one allreduce task per worker (B200 extension; the
 	// default keeps the reference's send-to-root tree, planner.cpp:389-517)
@@ -70,14 +71,25 @@ class planner {
 	// range like launch().
 	std::pair<int64_t, int64_t> host_transfer(int64_t array_id, uint64_t host_addr, bool write, const box* host_box = nullptr);
 
-	std::vector<task> take_pending();
+	std::vector<task> take_pending(); // copies (the C++ adapter / tests)
+	// hands every task emitted since the previous call to `f` (by reference, in id order, no
+	// copies), then drops them from memory unless the plan is retained
+	template <class F> void consume_pending(F&& f) {
+		for(int64_t id = pending_from_; id < next_task_; ++id) f(plan_[static_cast<size_t>(id - plan_base_)]);
+		pending_from_ = next_task_;
+		if(!cfg_.retain_plan) {
+			plan_.clear();
+			plan_base_ = next_task_;
+		}
+	}
 	// context-local kernels shadow the global registry (the reference registers synthesized
 	// gather kernels per scenario, scenario.cpp:368-389)
 	void add_local_kernel(kernel_entry e);
 	const kernel_entry* find_kernel(const std::string& id) const;
 	const array_rec& array(int64_t id) const;
 	const chunk_meta& chunk(int64_t id) const;
-	const std::vector<task>& plan() const { return plan_; }
+	const std::deque<task>& plan() const { return plan_; } // tasks [plan_base(), next_id()); appends never move them
+	int64_t plan_base() const { return plan_base_; }
 	int64_t next_id() const { return next_task_; }
 	int worker_of(int64_t task) const { return task_worker_[static_cast<size_t>(task)]; }
 	struct access_rec {
@@ -97,7 +109,9 @@ class planner {
 	int64_t next_task_ = 0;
 	std::unordered_map<int64_t, chunk_meta> chunks_;
 	std::vector<int> task_worker_;
-	std::vector<task> plan_, pending_;
+	std::deque<task> plan_;
+	int64_t plan_base_ = 0;    // id of plan_.front()
+	int64_t pending_from_ = 0; // first id not yet handed to the executor
 	std::map<std::pair<int, int>, uint64_t> tags_;
 	uint64_t collectives_ = 0; // allreduce group ids, in plan order
 	std::unordered_map<int64_t, std::vector<int64_t>> temp_users_;
