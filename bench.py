@@ -408,6 +408,93 @@ def run_reference_arm(args):
     }))
 
 
+def link_bandwidth(gib=4):
+    """pinned host <-> HBM copy bandwidth (GB/s): H2D, D2H and each way with both at once"""
+    import torch
+    n = gib << 30
+    h_src = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    h_dst = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d_src = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d_dst = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    res = {}
+    for name, fn in [("h2d", lambda: d_dst.copy_(h_src, non_blocking=True)), ("d2h", lambda: h_dst.copy_(d_src, non_blocking=True))]:
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        res[name] = 3 * n / (time.perf_counter() - t0) / 1e9
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            d_dst.copy_(h_src, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_dst.copy_(d_src, non_blocking=True)
+    torch.cuda.synchronize()
+    res["duplex_each_way"] = 3 * n / (time.perf_counter() - t0) / 1e9
+    del h_src, h_dst, d_src, d_dst
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ooc(rows, cols, chunk_rows, capacity_gib, host_gib, iters, warmup, lookahead=0):
+    """BASELINE config C5 (out-of-core heat2d) on one GPU with the pinned-host spill tier: two
+    rows x cols f32 arrays in chunk_rows-row chunks (halo [1,0]) with the device capacity capped.
+    Each iteration reads one array and overwrites the other (dead, never restored), so the
+    minimum traffic is the part of one array that does not fit, each way; the bound is that
+    volume over the measured duplex pinned bandwidth. Device-event timing."""
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+    bw = link_bandwidth()
+    cr = chunk_rows
+    cap = int(capacity_gib * (1 << 30))
+    la = lookahead or 3 * (rows // cr) * 3
+    ctx = mb.context(workers=1, devices=1, num_gpus=1, device_capacity=cap, host_capacity=int(host_gib * (1 << 30)), lookahead_tasks=la,
+                     retain_plan=False)
+    devs = ctx.devices
+    dist = lambda: ctx.dist.stencil([rows, cols], [cr, cols], [1, 0], devs)  # noqa: E731
+    a = ctx.create_array([rows, cols], "f32", dist(), 0)
+    b = ctx.create_array([rows, cols], "f32", dist(), 0)
+    work = ctx.dist.block_work([rows, cols], [16, 16], [cr, cols], devs)
+    ctx.launch("ramp2d_f32", [rows, cols], [16, 16], work, [rows, cols, 1000, 0.0, 1.0, Arr(a)], "global [i, j] => write out[i,j]")
+    t_setup = time.perf_counter()
+    for _ in range(warmup):
+        ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN)
+        ctx.flush()
+        a, b = b, a
+    ctx.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    s0 = ctx.exec_stats()
+    ctx.mark(0)
+    for _ in range(iters):
+        ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN)
+        ctx.flush()
+        a, b = b, a
+    ctx.mark(1)
+    ms = ctx.elapsed_ms()
+    ctx.synchronize()
+    s1 = ctx.exec_stats()
+    ctx.close()
+    wset = 2 * rows * cols * 4
+    h2d = (s1["spill_bytes_h2d"] - s0["spill_bytes_h2d"]) / iters
+    d2h = (s1["spill_bytes_d2h"] - s0["spill_bytes_d2h"]) / iters
+    minimum = max(0, wset // 2 - cap)
+    survey_bound = max(0, wset - cap)  # SURVEY 8d's looser (working set - resident) each way
+    per_iter = ms / iters / 1e3
+    bound = minimum / (bw["duplex_each_way"] * 1e9)
+    return {"workload": f"out-of-core heat2d {rows}x{cols} f32 x2 arrays, {cr}-row chunks, device capacity {capacity_gib} GiB",
+            "working_set_gib": wset / 2**30, "capacity_gib": capacity_gib, "iters": iters, "s_per_iter": per_iter,
+            "value": rows * cols / per_iter, "unit": "cell-updates/s", "h2d_gib_per_iter": h2d / 2**30, "d2h_gib_per_iter": d2h / 2**30,
+            "min_gib_each_way_per_iter": minimum / 2**30, "moved_over_min": max(h2d, d2h) / minimum if minimum else None,
+            "survey_bound_gib_each_way": survey_bound / 2**30,
+            "time_over_survey_bound": per_iter / (survey_bound / (bw["duplex_each_way"] * 1e9)) if survey_bound else None,
+            "link_gbs": bw, "bound_s_per_iter": bound, "time_over_bound": per_iter / bound if bound else None,
+            "lookahead_tasks": la, "warmup_s": t_setup, "evictions": s1["evictions"] - s0["evictions"]}
+
+
 def run_b200(args):
     import numpy as np
     import torch
@@ -603,6 +690,7 @@ def run_b200(args):
             hbm = 6650.0
         c4 = run_c4(ctx, args.hist_n, args.km_n, 5, hbm, rank == 0 and args.cpu_baseline)
     traffic = ncu_traffic("heat2d_ncu_summary.json", rows // ws, cols)
+    out = None
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -623,11 +711,22 @@ def run_b200(args):
             "contraction": contraction,
             "reductions": c4,
         }
-        print(json.dumps(out))
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()  # no rank may unmap its mailbox while a peer still writes into it
     ctx.close()
+    if ws == 1 and args.ooc_gib > 0:
+        # C5: spill-tier heat2d with both arrays in 1 GiB chunks and one array larger than the
+        # capped device capacity (a fresh context; the main one is closed)
+        import torch
+        torch.cuda.empty_cache()
+        try:
+            rows_ooc = int(args.ooc_gib * (1 << 30)) // (2 * 4 * cols) // 4096 * 4096
+            out["out_of_core"] = run_ooc(rows_ooc, cols, 4096, args.ooc_cap_gib, max(8.0, args.ooc_gib - args.ooc_cap_gib + 8.0), args.ooc_iters, 2)
+        except Exception as e:  # noqa: BLE001
+            out["out_of_core"] = {"unavailable": str(e)}
+    if rank == 0:
+        print(json.dumps(out))
     if ws > 1:
         dist.destroy_process_group()
 
@@ -653,6 +752,9 @@ def main():
     p.add_argument("--hist-n", type=int, default=4_000_000_000)
     p.add_argument("--strip", type=int, default=128, help="N>1: rows of the halo-facing superblocks per GPU")
     p.add_argument("--km-n", type=int, default=1_000_000_000)
+    p.add_argument("--ooc-gib", type=float, default=80.0, help="C5 out-of-core working set (2 arrays), 0 to skip")
+    p.add_argument("--ooc-cap-gib", type=float, default=24.0, help="device capacity for the C5 leg (one array must not fit)")
+    p.add_argument("--ooc-iters", type=int, default=12)
     args = p.parse_args()
     if args.impl == "reference":
         if args.ref_rows == 512:
