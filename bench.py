@@ -32,6 +32,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from ctypes import c_int as C_INT  # noqa: E402
+
 METRIC = "stencil cell-updates/s + matmul TFLOP/s at 1/2/4/8 B200; % roofline; vs CPU ref"
 ANN = "global [i, j] => read in[i-1:i+1, j-1:j+1], write out[i,j]"
 ALPHA = 0.1
@@ -163,10 +165,17 @@ def sample_rows(want: int, devices: int, block: int = 16) -> int:
     return per * max(1, round(want / per))
 
 
-def cpu_reference_rate(rows, cols, iters, devices) -> tuple[float, float]:
-    """Reference CPU executor (oracle/_ref) on a rows x cols sample: (cell-updates/s, seconds)."""
+def cpu_reference_rate(rows, cols, iters, devices, bounds_check=True) -> tuple[float, float]:
+    """Reference CPU executor (oracle/_ref) on a rows x cols sample: (cell-updates/s, seconds).
+    bounds_check: the reference's array_view index checks (memory.hpp:54, default on)."""
     import oracle
     from paper_2202_05549_b200 import Arr
+    ref = oracle.reference()
+    toggle = getattr(ref.dll, "mr_set_bounds_check", None)
+    if toggle is not None:
+        toggle(C_INT(1 if bounds_check else 0))
+    elif not bounds_check:
+        raise RuntimeError("reference build lacks mr_set_bounds_check")
     ctx = oracle.reference_context(workers=1, devices=devices, execute=True)
     a, b, work = setup_heat(ctx, rows, cols, devices)
     ctx.synchronize()
@@ -178,6 +187,8 @@ def cpu_reference_rate(rows, cols, iters, devices) -> tuple[float, float]:
     ctx.synchronize()
     dt = time.perf_counter() - t0
     ctx.close()
+    if toggle is not None:
+        toggle(C_INT(1))
     return rows * cols * iters / dt, dt
 
 
@@ -663,7 +674,13 @@ def run_b200(args):
             rrows = sample_rows(args.ref_rows, devices)
             rate, dt = cpu_reference_rate(rrows, cols, args.ref_iters, devices)
             cpu = {"value": rate, "unit": "cell-updates/s", "cores": devices, "kind": "reference",
-                   "sample": f"{rrows}x{cols} rows x {args.ref_iters} iterations ({dt:.1f} s), {devices} chunks, 1 worker x {devices} device threads"}
+                   "sample": f"{rrows}x{cols} rows x {args.ref_iters} iterations ({dt:.1f} s), {devices} chunks, 1 worker x {devices} device threads",
+                   "bounds_check": "on (the reference default, memory.hpp:54)"}
+            try:
+                rate_off, dt_off = cpu_reference_rate(rrows, cols, args.ref_iters, devices, bounds_check=False)
+                cpu["bounds_check_off"] = {"value": rate_off, "seconds": dt_off}
+            except Exception as e:  # noqa: BLE001
+                cpu["bounds_check_off"] = {"unavailable": str(e)}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "cell-updates/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 

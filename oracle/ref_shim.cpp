@@ -509,8 +509,13 @@ const kernel_registry& registry() {
 	return reg;
 }
 
+// array_view bounds checking in the reference executor (memory.hpp:54, default on); the bench
+// times the CPU baseline both ways
+bool g_bounds_check = true;
+
 system_config make_system_config(const mt_config& c) {
 	system_config sys;
+	sys.memory.bounds_check = g_bounds_check;
 	sys.workers = c.workers;
 	sys.devices_per_worker = c.devices_per_worker;
 	if(c.device_capacity) sys.memory.device_capacity = c.device_capacity;
@@ -779,6 +784,7 @@ int mr_kernel_count(void) {
 
 // Hardware threads the reference executor can use on this host (bench cpu_baseline).
 int mr_host_threads(void) { return static_cast<int>(std::thread::hardware_concurrency()); }
+void mr_set_bounds_check(int32_t on) { g_bounds_check = on != 0; }
 
 // ---- scenario harness of the reference (scenario.hpp:160-171), used as the parity oracle ----
 
