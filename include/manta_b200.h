@@ -298,6 +298,11 @@ int mt_exec_elapsed_ms(mt_exec* ex, double* ms);
 /* per-kernel CUDA-event timing on the launching stream (count, total ms since enabled) */
 int mt_exec_profile(mt_exec* ex, int32_t on);
 int mt_exec_kernel_time(mt_exec* ex, const char* kernel, int64_t* count, double* total_ms);
+/* per-task tracing (the reference's run_report task records, runtime.cpp:389, :514-525): while
+ * on, every task gets device timestamps (after its dependency waits, after its work, on its
+ * stream) and mt_exec_report_json lists {id, kind, start_ns, end_ns} per worker, ns since
+ * tracing was switched on */
+int mt_exec_trace(mt_exec* ex, int32_t on);
 
 /* ---- kernel plugin API (kernels.hpp:56-105) ------------------------------------------ */
 /* View of one chunk as seen by a kernel: element (g0,g1,g2) lives at

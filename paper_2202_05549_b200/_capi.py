@@ -157,6 +157,7 @@ _SIGS = {
     "exec_mark": (C.c_int, [C.c_void_p, C.c_int32]),
     "exec_elapsed_ms": (C.c_int, [C.c_void_p, P(C.c_double)]),
     "exec_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+    "exec_trace": (C.c_int, [C.c_void_p, C.c_int32]),
     "exec_kernel_time": (C.c_int, [C.c_void_p, C.c_char_p, P(C.c_int64), P(C.c_double)]),
     "kernel_register": (C.c_int, [C.c_char_p, P(ParamSpec), C.c_int32, LAUNCHER]),
     "kernel_count": (C.c_int, []),
@@ -183,7 +184,7 @@ _SIGS = {
 }
 # entry points the oracle shim may lack
 _OPTIONAL = {"exec_stats", "exec_last_stream", "kernel_info", "host_threads", "ctx_kernel_register", "fuzz_scenario_json", "scenario_plan", "scenario_dot",
-             "scenario_run", "plan_accesses", "ctx_gather_register", "ctx_peer_export", "ctx_peer_import", "ctx_nccl_unique_id", "ctx_nccl_init", "array_write_async", "array_read_async", "array_write_box_async", "array_read_box_async", "ctx_kernel_compile", "wrapper_source", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time"}
+             "scenario_run", "plan_accesses", "ctx_gather_register", "ctx_peer_export", "ctx_peer_import", "ctx_nccl_unique_id", "ctx_nccl_init", "array_write_async", "array_read_async", "array_write_box_async", "array_read_box_async", "ctx_kernel_compile", "wrapper_source", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time", "exec_trace"}
 
 
 class MantaError(RuntimeError):

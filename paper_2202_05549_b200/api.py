@@ -500,6 +500,10 @@ class Context:
     def profile_kernels(self, on=True):
         self.lib.check(self.lib.exec_profile(self._ex(), int(on)))
 
+    def trace(self, on=True):
+        """per-task device timestamps in report_json() (mt_exec_trace)"""
+        self.lib.check(self.lib.exec_trace(self._ex(), int(on)))
+
     def kernel_time(self, kernel: str) -> tuple[int, float]:
         n, ms = C.c_int64(0), C.c_double(0)
         self.lib.check(self.lib.exec_kernel_time(self._ex(), kernel.encode(), C.byref(n), C.byref(ms)))

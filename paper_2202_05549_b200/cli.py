@@ -109,9 +109,11 @@ def make_context(sysd: dict, execute: bool, oracle_mode=False, suppress=False, s
                    staging_threshold=int(sysd.get("staging_threshold", 0)))
 
 
-def run_scenario(sc: dict, sysd: dict, oracle_mode=False, suppress=False, streams=0, compat=False):
+def run_scenario(sc: dict, sysd: dict, oracle_mode=False, suppress=False, streams=0, compat=False, trace=False):
     """run_scenario on the GPU: (arrays by name, replicas coherent, report json)"""
     with make_context(sysd, True, oracle_mode, suppress, streams, compat) as ctx:
+        if trace:
+            ctx.trace(True)
         S.register_gather_kernels(ctx, sc)
         arrays, coherent = S.run(ctx, sc, oracle_mode=oracle_mode)
         report = ctx.report_json()
@@ -242,7 +244,8 @@ def _report_totals(report: str) -> dict:
 def cmd_run(args) -> int:
     sc = load(args.scenario)
     sysd = system_of(sc, args)
-    arrays, coherent, report = run_scenario(sc, sysd, suppress=args.no_conflict_deps, streams=args.streams, compat=args.compat_deps)
+    arrays, coherent, report = run_scenario(sc, sysd, suppress=args.no_conflict_deps, streams=args.streams, compat=args.compat_deps,
+                                            trace=bool(args.report))
     t = _report_totals(report)
     print(f"completed: {len(arrays)} arrays, evictions={t['evictions']}, bytes_sent={t['bytes_sent']}, "
           f"staging_checks={t['staging_checks']}, staging_violations={t['staging_violations']}")

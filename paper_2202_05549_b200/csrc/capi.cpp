@@ -637,6 +637,10 @@ int mt_exec_profile(mt_exec* ex, int32_t on) {
 	return guarded([&] { ex->ex->set_profile(on != 0); });
 }
 
+int mt_exec_trace(mt_exec* ex, int32_t on) {
+	return guarded([&] { ex->ex->set_trace(on != 0); });
+}
+
 int mt_exec_kernel_time(mt_exec* ex, const char* kernel, int64_t* count, double* total_ms) {
 	return guarded([&] { ex->ex->kernel_time(kernel, count, total_ms); });
 }

@@ -407,6 +407,29 @@ void executor::wait_deps(const task& t, cudaStream_t s) {
 	}
 	for(auto ev : stage_waits_) check_cuda(cudaStreamWaitEvent(s, ev, 0), "cudaStreamWaitEvent");
 	stage_waits_.clear();
+	if(trace_) {
+		int cur = 0;
+		cudaGetDevice(&cur);
+		trace_rec r{t.id, t.worker, t.kind, cur - cfg_.gpu_base};
+		check_cuda(cudaEventCreate(&r.t0), "cudaEventCreate");
+		check_cuda(cudaEventRecord(r.t0, s), "cudaEventRecord");
+		trace_open_[t.id] = trace_recs_.size();
+		trace_recs_.push_back(r);
+	}
+}
+
+void executor::set_trace(bool on) {
+	if(on && !trace_) {
+		trace_base_.assign(gpus_.size(), nullptr);
+		for(size_t g = 0; g < gpus_.size(); ++g) {
+			check_cuda(cudaSetDevice(gpus_[g].ordinal), "cudaSetDevice");
+			check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+			check_cuda(cudaEventCreate(&trace_base_[g]), "cudaEventCreate");
+			check_cuda(cudaEventRecord(trace_base_[g], gpus_[g].timing), "cudaEventRecord");
+			check_cuda(cudaEventSynchronize(trace_base_[g]), "cudaEventSynchronize");
+		}
+	}
+	trace_ = on;
 }
 
 cudaStream_t executor::pick_compute(const task& t, ldev& L) {
@@ -435,6 +458,15 @@ void executor::finish(const task& t, cudaStream_t s) {
 	done_[t.id] = {ev, s, cur};
 	tail_[s] = t.id;
 	++ctr_.tasks;
+	if(trace_) {
+		const auto it = trace_open_.find(t.id);
+		if(it != trace_open_.end()) {
+			auto& r = trace_recs_[it->second];
+			check_cuda(cudaEventCreate(&r.t1), "cudaEventCreate");
+			check_cuda(cudaEventRecord(r.t1, s), "cudaEventRecord");
+			trace_open_.erase(it);
+		}
+	}
 	if(done_.size() > 16384) retire_completed();
 }
 
@@ -1311,13 +1343,33 @@ void executor::upload(int64_t chunk, const void* host, const box& host_box) {
 
 namespace {
 
-__global__ void spin_until_geq(const uint64_t* flag, uint64_t value) {
-	uint64_t v = 0;
+// A peer that never sends (a crashed rank, a protocol bug) must not hang the GPU: after
+// `timeout_ns` of waiting the kernel traps, the context reports a launch failure and the next
+// mt_sync raises execution_error (the reference's stall detection, runtime.cpp:662-691).
+__global__ void spin_until_geq(const uint64_t* flag, uint64_t value, uint64_t timeout_ns) {
+	uint64_t v = 0, t0 = 0, now = 0;
+	asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
 	for(;;) {
 		asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
 		if(v >= value) break;
 		__nanosleep(64);
+		asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+		if(now - t0 > timeout_ns) {
+			printf("manta-b200: peer message wait timed out (flag %p: %llu < %llu)\n", flag, static_cast<unsigned long long>(v),
+			    static_cast<unsigned long long>(value));
+			__trap();
+		}
 	}
+}
+
+// MTB_PEER_TIMEOUT_S (default 120 s) bounds every inter-process wait
+uint64_t peer_timeout_ns() {
+	static const uint64_t ns = [] {
+		const char* e = std::getenv("MTB_PEER_TIMEOUT_S");
+		const double s = e ? std::atof(e) : 120.0;
+		return static_cast<uint64_t>((s > 0 ? s : 120.0) * 1e9);
+	}();
+	return ns;
 }
 
 __global__ void release_store(uint64_t* flag, uint64_t value) {
@@ -1405,7 +1457,7 @@ void executor::remote_send(const task& t) {
 		const uint64_t seg = std::min<uint64_t>(kSlotBytes, bytes - off);
 		const uint64_t q = link.tx_seq++;
 		const uint64_t slot = q % kSlots;
-		if(q >= static_cast<uint64_t>(kSlots)) spin_until_geq<<<1, 1, 0, s>>>(link.tx_consumed, q + 1 - kSlots);
+		if(q >= static_cast<uint64_t>(kSlots)) spin_until_geq<<<1, 1, 0, s>>>(link.tx_consumed, q + 1 - kSlots, peer_timeout_ns());
 		check_cuda(cudaMemcpyAsync(link.tx_ring + slot * kSlotBytes, static_cast<char*>(stage) + off, seg, cudaMemcpyDefault, s), "cudaMemcpyAsync (send)");
 		release_store<<<1, 1, 0, s>>>(link.tx_ready + slot, q + 1);
 	}
@@ -1431,7 +1483,7 @@ void executor::remote_recv(const task& t) {
 		const uint64_t seg = std::min<uint64_t>(kSlotBytes, bytes - off);
 		const uint64_t q = link.rx_seq++;
 		const uint64_t slot = q % kSlots;
-		spin_until_geq<<<1, 1, 0, s>>>(link.rx_ready + slot, q + 1);
+		spin_until_geq<<<1, 1, 0, s>>>(link.rx_ready + slot, q + 1, peer_timeout_ns());
 		check_cuda(cudaMemcpyAsync(static_cast<char*>(stage) + off, link.rx_ring + slot * kSlotBytes, seg, cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync (recv)");
 		release_store<<<1, 1, 0, s>>>(link.rx_consumed, q + 1);
 	}
@@ -1442,7 +1494,19 @@ void executor::remote_recv(const task& t) {
 	finish(t, s);
 }
 
-std::string executor::report_json() const {
+std::string executor::report_json() {
+	// traced tasks per worker: {"id", "kind", "start_ns", "end_ns"} (runtime.cpp:626-629)
+	std::vector<std::string> tasks(static_cast<size_t>(cfg_.workers));
+	for(const auto& r : trace_recs_) {
+		if(!r.t1 || r.worker < 0 || r.worker >= cfg_.workers) continue;
+		check_cuda(cudaEventSynchronize(r.t1), "cudaEventSynchronize");
+		float a = 0.f, b = 0.f;
+		check_cuda(cudaEventElapsedTime(&a, trace_base_[static_cast<size_t>(r.gpu)], r.t0), "cudaEventElapsedTime");
+		check_cuda(cudaEventElapsedTime(&b, trace_base_[static_cast<size_t>(r.gpu)], r.t1), "cudaEventElapsedTime");
+		std::string& o = tasks[static_cast<size_t>(r.worker)];
+		o += std::string(o.empty() ? "" : ", ") + "{\"id\": " + std::to_string(r.id) + ", \"kind\": \"" + task_kind_name(r.kind) + "\", \"start_ns\": "
+		     + std::to_string(static_cast<int64_t>(static_cast<double>(a) * 1e6)) + ", \"end_ns\": " + std::to_string(static_cast<int64_t>(static_cast<double>(b) * 1e6)) + "}";
+	}
 	std::ostringstream os;
 	os << "{\"workers\": [";
 	for(int w = 0; w < cfg_.workers; ++w) {
@@ -1450,7 +1514,8 @@ std::string executor::report_json() const {
 		   << ", \"bytes_device_to_host\": " << (w == 0 ? ctr_.bytes_device_to_host : 0) << ", \"bytes_host_to_disk\": 0"
 		   << ", \"bytes_host_to_device\": " << (w == 0 ? ctr_.bytes_host_to_device : 0) << ", \"bytes_disk_to_device\": 0"
 		   << ", \"bytes_sent\": " << (w == 0 ? ctr_.bytes_sent : 0) << ", \"bytes_received\": " << (w == 0 ? ctr_.bytes_received : 0)
-		   << ", \"staging_checks\": 0, \"staging_violations\": 0, \"peak_device_bytes\": [" << ctr_.peak_device_bytes << "], \"tasks\": []}";
+		   << ", \"staging_checks\": 0, \"staging_violations\": 0, \"peak_device_bytes\": [" << ctr_.peak_device_bytes << "], \"tasks\": ["
+		   << tasks[static_cast<size_t>(w)] << "]}";
 	}
 	os << "], \"tasks\": " << ctr_.tasks << ", \"kernel_launches\": " << ctr_.kernels << ", \"copies\": " << ctr_.copies << ", \"bytes_copied\": " << ctr_.bytes_copied
 	   << "}";

@@ -78,7 +78,7 @@ class executor {
 	void download(int64_t chunk, void* host, const box& host_box, const box& region);
 	void upload(int64_t chunk, const void* host, const box& host_box);
 	bool has_chunk(int64_t chunk) const { return bufs_.count(chunk) != 0; }
-	std::string report_json() const;
+	std::string report_json(); // waits for traced tasks' end events
 	const exec_counters& counters() const { return ctr_; }
 
 	// stream of the most recent execute on a chunk's device (bench timing hook)
@@ -93,6 +93,10 @@ class executor {
 	// Per-kernel event timing on the launching stream (bench roofline): when enabled every
 	// execute task's launcher call is bracketed by timing events.
 	void set_profile(bool on) { profile_ = on; }
+	// per-task device timestamps for report_json (the reference's run_report task records,
+	// runtime.cpp:389, :514-525): a timing event after a task's dependency waits and one after
+	// its work, both on its stream; times are ns since tracing was switched on
+	void set_trace(bool on);
 	void kernel_time(const std::string& kernel, int64_t* count, double* total_ms);
 
 	// One process per worker: GPU-driven point-to-point messaging for send/recv tasks whose
@@ -191,6 +195,17 @@ class executor {
 	exec_counters ctr_;
 	cudaStream_t last_exec_stream_ = nullptr;
 	bool profile_ = false;
+	struct trace_rec {
+		int64_t id;
+		int worker;
+		task_kind kind;
+		int gpu;
+		cudaEvent_t t0 = nullptr, t1 = nullptr;
+	};
+	bool trace_ = false;
+	std::vector<trace_rec> trace_recs_;
+	std::unordered_map<int64_t, size_t> trace_open_;
+	std::vector<cudaEvent_t> trace_base_; // per executor GPU
 	std::map<std::string, kernel_timing> ktimes_;
 
 	ldev& dev(device_id d);

@@ -1,0 +1,11 @@
+#!/bin/bash
+# compute-sanitizer (memcheck, racecheck, synccheck) over small GPU parity cases: heat2d halo
+# exchange, histogram / k-means reduce trees, bundled scenarios, the tcgen05 GEMM, gather fuzz
+mkdir -p gpurun_out/sanitizer
+SEL="tests/test_gpu_parity.py::test_heat2d_matches_reference_golden tests/test_gpu_parity.py::test_histogram_matches_reference_golden tests/test_gpu_parity.py::test_kmeans_i32_matches_reference_golden tests/test_gpu_parity.py::test_bundled_scenario_matches_reference tests/test_gpu_edges.py::test_heat2d_ragged_shapes tests/test_gpu_matmul.py::test_matmul_nt_bf16_through_the_planner tests/test_gpu_fuzz.py::test_correlator_like_scenario tests/test_gpu_nbody.py"
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --target-processes all --print-limit 20 \
+    python -m pytest $SEL -q -m gpu -p no:cacheprovider -x > gpurun_out/sanitizer/$tool.log 2>&1
+  echo "$tool rc=$?"
+  grep -E "ERROR SUMMARY|passed|failed" gpurun_out/sanitizer/$tool.log | tail -3
+done

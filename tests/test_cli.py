@@ -113,6 +113,13 @@ def test_run_oracle_passes(scenarios, tmp_path, name):
     with open(report) as f:
         r = json.load(f)
     assert len(r["workers"]) == scenarios[name].get("system", {}).get("workers", 1)
+    # traced task records like the reference's run_report (runtime.cpp:626-629)
+    recs = [t for w in r["workers"] for t in w["tasks"]]
+    assert recs and all(0 <= t["start_ns"] <= t["end_ns"] for t in recs)
+    kinds = {t["kind"] for t in recs}
+    assert "execute" in kinds and kinds <= {"create", "delete", "execute", "copy", "send", "recv", "reduce"}
+    if scenarios[name].get("arrays"):
+        assert "create" in kinds
 
 
 @pytest.mark.gpu

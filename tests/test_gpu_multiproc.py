@@ -241,3 +241,49 @@ def test_two_process_box_host_io_matches_single_process():
             a, b = b, a
         want = c.read(a)
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def _silent_peer_rank(rank, world, port, q):
+    """rank 1 never launches, so rank 0's halo receive has no sender: the bounded GPU-side wait
+    must turn that into an execution error instead of a hung GPU"""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), MTB_PEER_TIMEOUT_S="2")
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+    rows, cols = 64, 128
+    ctx = mb.context(workers=world, devices=1, worker_rank=rank, gpu_base=0)
+    ctx.connect_peers()
+    outcome = "ok"
+    if rank == 0:
+        devs = ctx.devices
+        dist_ = lambda: ctx.dist.stencil([rows, cols], [rows // world, cols], [1, 0], devs)  # noqa: E731
+        a = ctx.create_array([rows, cols], "f32", dist_(), 0)
+        b = ctx.create_array([rows, cols], "f32", dist_(), 0)
+        work = ctx.dist.block_work([rows, cols], [16, 16], [rows // world, cols], devs)
+        ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT)
+        try:
+            ctx.synchronize()
+            outcome = "returned"
+        except mb.MantaError as e:
+            outcome = type(e).__name__
+    q.put((rank, outcome))
+    dist.barrier()
+    if rank != 0:
+        ctx.close()
+    dist.destroy_process_group()
+    os._exit(0)  # rank 0's CUDA context is poisoned by the trap: skip teardown
+
+
+def test_missing_peer_message_times_out():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_silent_peer_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    assert res[0] == "ExecutionError"
