@@ -287,7 +287,7 @@ int mt_exec_report_json(mt_exec* ex, char* buf, int64_t cap, int64_t* len);
 /* counters: tasks, device launches, copies, bytes copied, bytes sent, bytes received, peak
  * device bytes, evictions, spill bytes D2H, spill bytes H2D, dead drops (evictions without
  * write-back), dead skips (restores without H2D), host reclaims, host_write bytes, host_read
- * bytes (first n of them) */
+ * bytes, CUDA-graph captures, CUDA-graph replays (first n of them) */
 int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n);
 /* cudaStream_t of the most recent execute task (for event timing on the launching stream) */
 void* mt_exec_last_stream(mt_exec* ex);

@@ -287,6 +287,7 @@ executor::executor(const executor_config& cfg) : cfg_(cfg) {
 		G.capacity = cfg.device_capacity ? cfg.device_capacity : static_cast<uint64_t>(static_cast<double>(free_b) * 0.9);
 		check_cuda(cudaStreamCreateWithFlags(&G.service, cudaStreamNonBlocking), "cudaStreamCreate");
 		check_cuda(cudaStreamCreateWithFlags(&G.timing, cudaStreamNonBlocking), "cudaStreamCreate");
+		check_cuda(cudaStreamCreateWithFlags(&G.graph, cudaStreamNonBlocking), "cudaStreamCreate");
 		check_cuda(cudaStreamCreateWithFlags(&G.h2d, cudaStreamNonBlocking), "cudaStreamCreate");
 		check_cuda(cudaStreamCreateWithFlags(&G.d2h, cudaStreamNonBlocking), "cudaStreamCreate");
 		for(auto& m : G.marks) check_cuda(cudaEventCreate(&m), "cudaEventCreate");
@@ -362,6 +363,7 @@ executor::~executor() {
 		cudaDeviceSynchronize();
 		if(G.service) cudaStreamDestroy(G.service);
 		if(G.timing) cudaStreamDestroy(G.timing);
+		if(G.graph) cudaStreamDestroy(G.graph);
 		if(G.h2d) cudaStreamDestroy(G.h2d);
 		if(G.d2h) cudaStreamDestroy(G.d2h);
 		for(auto m : G.marks)
@@ -401,6 +403,7 @@ cudaEvent_t executor::take_event(int gpu) {
 
 void executor::wait_deps(const task& t, cudaStream_t s) {
 	for(const auto d : t.deps) {
+		if(capturing_ && d < capture_first_) continue; // satisfied before the graph launch (replay)
 		const auto it = done_.find(d);
 		if(it == done_.end() || it->second.stream == s) continue;
 		check_cuda(cudaStreamWaitEvent(s, it->second.ev, 0), "cudaStreamWaitEvent");
@@ -467,13 +470,13 @@ void executor::finish(const task& t, cudaStream_t s) {
 			trace_open_.erase(it);
 		}
 	}
-	if(done_.size() > 16384) retire_completed();
+	if(done_.size() > 16384 && !capturing_) retire_completed();
 }
 
 void executor::retire_completed() {
 	for(auto it = done_.begin(); it != done_.end();) {
 		if(cudaEventQuery(it->second.ev) == cudaSuccess) {
-			free_events_[static_cast<size_t>(it->second.gpu)].push_back(it->second.ev);
+			release_done_event(it->second.ev, it->second.gpu);
 			it = done_.erase(it);
 		} else {
 			++it;
@@ -493,12 +496,222 @@ void executor::submit_one(const task& t) {
 	if(cfg_.local_workers >= 0 && (t.worker < cfg_.first_worker || t.worker >= cfg_.first_worker + cfg_.local_workers)) return;
 	if(spill_)
 		queue_.push_back(t);
+	else if(graphs_on_ && !trace_ && !profile_)
+		gbatch_.push_back(t);
 	else
 		issue(t);
 }
 
 void executor::end_submit() {
 	if(spill_) drain(false);
+	issue_batch();
+}
+
+void executor::issue_batch() {
+	if(gbatch_.empty()) return;
+	std::vector<task> b;
+	b.swap(gbatch_);
+	int gpu = -1;
+	if(graph_eligible(b, &gpu)) {
+		const std::string sig = signature(b);
+		auto it = graphs_.find(sig);
+		if(it == graphs_.end() && ++sig_seen_[sig] >= 2 && graphs_.size() < 256) {
+			graph_entry g;
+			if(capture(b, gpu, g)) it = graphs_.emplace(sig, g).first;
+			else sig_seen_[sig] = -1000000; // not capturable: never try again
+		}
+		if(it != graphs_.end()) {
+			replay(it->second, b);
+			return;
+		}
+		if(sig_seen_.size() > 4096) sig_seen_.clear();
+	}
+	for(const auto& t : b) issue(t);
+}
+
+bool executor::graph_eligible(const std::vector<task>& b, int* gpu) const {
+	if(spill_ || trace_ || profile_) return false;
+	// Only submissions whose GPU work is short enough that issuing them costs as much as running
+	// them: consecutive replays run back to back on one stream, which gives up the overlap
+	// between submissions that the multi-stream path keeps for large superblocks.
+	static const double max_threads = [] {
+		const char* e = std::getenv("MTB_GRAPH_MAX_THREADS");
+		return e ? std::atof(e) : 33554432.0;
+	}();
+	double threads = 0;
+	for(const auto& t : b)
+		if(t.kind == task_kind::execute) threads += static_cast<double>(t.sb_threads.volume());
+	if(threads > max_threads) return false;
+	int g = -1;
+	for(const auto& t : b) {
+		if(t.kind != task_kind::execute && t.kind != task_kind::copy) return false;
+		const auto chunk_gpu = [&](int64_t c) {
+			const auto it = bufs_.find(c);
+			return it == bufs_.end() || !it->second.ptr ? -1 : it->second.gpu;
+		};
+		int tg;
+		if(t.kind == task_kind::execute) {
+			if(t.device.worker < 0 || t.device.worker >= cfg_.workers || t.device.device < 0 || t.device.device >= cfg_.devices_per_worker) return false;
+			const auto& L = ldevs_[static_cast<size_t>(t.device.worker * cfg_.devices_per_worker + t.device.device)];
+			if(L.compute.empty() || !t.kern) return false;
+			tg = L.gpu;
+			for(const auto& a : t.args)
+				if(a.kind == arg_kind::chunk && chunk_gpu(a.chunk) != tg) return false;
+		} else {
+			tg = chunk_gpu(t.dst);
+			if(tg < 0 || chunk_gpu(t.src) != tg) return false;
+		}
+		if(g >= 0 && tg != g) return false;
+		g = tg;
+	}
+	*gpu = g;
+	return g >= 0;
+}
+
+std::string executor::signature(const std::vector<task>& b) const {
+	std::string s;
+	s.reserve(b.size() * 192);
+	const auto put = [&](const void* p, size_t n) { s.append(static_cast<const char*>(p), n); };
+	const auto put_box = [&](const box& r) {
+		const int k = r.rank();
+		put(&k, sizeof k);
+		for(int d = 0; d < k; ++d) {
+			const int64_t lo = r.lo[d], hi = r.hi[d];
+			put(&lo, 8);
+			put(&hi, 8);
+		}
+	};
+	const int64_t first = b.front().id;
+	for(const auto& t : b) {
+		const int64_t rel = t.id - first;
+		put(&rel, 8);
+		put(&t.kind, sizeof t.kind);
+		put(&t.resource, sizeof t.resource);
+		for(const auto d : t.deps)
+			if(d >= first) {
+				const int64_t r = d - first;
+				put(&r, 8);
+			}
+		const int64_t sep = -1;
+		put(&sep, 8);
+		if(t.kind == task_kind::execute) {
+			put(&t.kern, sizeof t.kern);
+			put(&t.device, sizeof t.device);
+			put_box(t.sb_blocks);
+			put_box(t.sb_threads);
+			put_box(box(t.block_size, t.block_size));
+			for(const auto& a : t.args) {
+				put(&a.kind, sizeof a.kind);
+				put(&a.i, 8);
+				put(&a.f, 8);
+				put(&a.chunk, 8);
+			}
+		} else {
+			put(&t.src, 8);
+			put(&t.dst, 8);
+			put_box(t.src_region);
+			put_box(t.dst_region);
+		}
+	}
+	return s;
+}
+
+bool executor::capture(const std::vector<task>& b, int gpu, graph_entry& out) {
+	auto& G = gpus_[static_cast<size_t>(gpu)];
+	check_cuda(cudaSetDevice(G.ordinal), "cudaSetDevice");
+	std::vector<cudaStream_t> streams;
+	for(const auto& L : ldevs_)
+		if(L.gpu == gpu && !L.compute.empty()) {
+			streams.insert(streams.end(), L.compute.begin(), L.compute.end());
+			streams.push_back(L.copy);
+		}
+	const exec_counters before = ctr_;
+	const auto tail_before = tail_;
+	cudaGraph_t graph = nullptr;
+	std::vector<cudaEvent_t> used; // events recorded inside the capture go back to the pool
+	bool ok = cudaStreamBeginCapture(G.graph, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+	if(ok) {
+		capturing_ = true;
+		capture_first_ = b.front().id;
+		try {
+			cudaEvent_t fork = take_event(gpu);
+			used.push_back(fork);
+			check_cuda(cudaEventRecord(fork, G.graph), "cudaEventRecord (fork)");
+			for(auto st : streams) check_cuda(cudaStreamWaitEvent(st, fork, 0), "cudaStreamWaitEvent (fork)");
+			for(const auto& t : b) issue(t);
+			for(auto st : streams) {
+				cudaEvent_t j = take_event(gpu);
+				used.push_back(j);
+				check_cuda(cudaEventRecord(j, st), "cudaEventRecord (join)");
+				check_cuda(cudaStreamWaitEvent(G.graph, j, 0), "cudaStreamWaitEvent (join)");
+			}
+		} catch(const std::exception&) {
+			ok = false;
+		}
+		capturing_ = false;
+		const cudaError_t e = cudaStreamEndCapture(G.graph, &graph);
+		ok = ok && e == cudaSuccess && graph;
+	}
+	cudaGetLastError();
+	if(ok) ok = cudaGraphInstantiate(&out.exec, graph, 0) == cudaSuccess;
+	cudaGetLastError();
+	if(graph) cudaGraphDestroy(graph);
+	// nothing of the submission ran: forget the capture-time completion records
+	for(const auto& t : b) {
+		const auto it = done_.find(t.id);
+		if(it == done_.end()) continue;
+		used.push_back(it->second.ev);
+		done_.erase(it);
+	}
+	for(auto e : used) free_events_[static_cast<size_t>(gpu)].push_back(e);
+	tail_ = tail_before;
+	out.gpu = gpu;
+	out.tasks = static_cast<int64_t>(ctr_.tasks - before.tasks);
+	out.kernels = static_cast<int64_t>(ctr_.kernels - before.kernels);
+	out.copies = static_cast<int64_t>(ctr_.copies - before.copies);
+	out.bytes_copied = ctr_.bytes_copied - before.bytes_copied;
+	ctr_ = before;
+	if(ok) ++ctr_.graph_captures;
+	return ok;
+}
+
+void executor::replay(const graph_entry& g, const std::vector<task>& b) {
+	auto& G = gpus_[static_cast<size_t>(g.gpu)];
+	check_cuda(cudaSetDevice(G.ordinal), "cudaSetDevice");
+	const int64_t first = b.front().id;
+	for(const auto& t : b)
+		for(const auto d : t.deps) {
+			if(d >= first) continue;
+			const auto it = done_.find(d);
+			if(it == done_.end() || it->second.stream == G.graph) continue;
+			check_cuda(cudaStreamWaitEvent(G.graph, it->second.ev, 0), "cudaStreamWaitEvent");
+		}
+	check_cuda(cudaGraphLaunch(g.exec, G.graph), "cudaGraphLaunch");
+	cudaEvent_t ev = take_event(g.gpu);
+	check_cuda(cudaEventRecord(ev, G.graph), "cudaEventRecord");
+	shared_ev_[ev] = static_cast<int>(b.size());
+	for(const auto& t : b) {
+		const auto old = done_.find(t.id);
+		if(old != done_.end()) release_done_event(old->second.ev, old->second.gpu);
+		done_[t.id] = {ev, G.graph, g.gpu};
+		tail_[G.graph] = t.id;
+	}
+	last_exec_stream_ = G.graph;
+	ctr_.tasks += static_cast<uint64_t>(g.tasks);
+	ctr_.kernels += static_cast<uint64_t>(g.kernels);
+	ctr_.copies += static_cast<uint64_t>(g.copies);
+	ctr_.bytes_copied += g.bytes_copied;
+	++ctr_.graph_replays;
+	if(done_.size() > 16384) retire_completed();
+}
+
+void executor::release_done_event(cudaEvent_t ev, int gpu) {
+	const auto it = shared_ev_.find(ev);
+	if(it != shared_ev_.end()) {
+		if(--it->second > 0) return;
+		shared_ev_.erase(it);
+	}
+	free_events_[static_cast<size_t>(gpu)].push_back(ev);
 }
 
 void executor::drain(bool all) {
@@ -1235,6 +1448,7 @@ void executor::run_host_io(const task& t) {
 void executor::mark(int slot) {
 	if(slot < 0 || slot > 1) throw validation_error("mark slot must be 0 or 1");
 	drain(true);
+	issue_batch();
 	for(size_t g = 0; g < gpus_.size(); ++g) {
 		auto& G = gpus_[g];
 		check_cuda(cudaSetDevice(G.ordinal), "cudaSetDevice");
@@ -1284,13 +1498,14 @@ void executor::kernel_time(const std::string& kernel, int64_t* count, double* to
 
 void executor::sync() {
 	drain(true);
+	issue_batch();
 	std::string err;
 	for(auto& G : gpus_) {
 		cudaSetDevice(G.ordinal);
 		const cudaError_t e = cudaDeviceSynchronize();
 		if(e != cudaSuccess && err.empty()) err = std::string("device execution failed: ") + cudaGetErrorString(e);
 	}
-	for(auto& [id, d] : done_) free_events_[static_cast<size_t>(d.gpu)].push_back(d.ev);
+	for(auto& [id, d] : done_) release_done_event(d.ev, d.gpu);
 	done_.clear();
 	tail_.clear();
 	if(!err.empty()) throw execution_error(err);

@@ -23,6 +23,7 @@
 #include <map>
 #include <string>
 #include <tuple>
+#include <cstdlib>
 #include <unordered_map>
 #include <vector>
 
@@ -59,6 +60,7 @@ struct exec_counters {
 	uint64_t dead_skips = 0; // restores that skipped the H2D (data overwritten before read)
 	uint64_t host_reclaims = 0; // host copies of resident chunks taken back when the host tier is full
 	uint64_t bytes_host_in = 0, bytes_host_out = 0; // host_write / host_read tasks
+	uint64_t graph_captures = 0, graph_replays = 0;  // CUDA-graph replay of repeated submissions
 };
 
 class executor {
@@ -162,6 +164,7 @@ class executor {
 		uint64_t capacity = 0;
 		cudaStream_t service = nullptr; // message-buffer releases
 		cudaStream_t timing = nullptr;
+		cudaStream_t graph = nullptr; // launches of replayed submissions (CUDA graphs)
 		cudaStream_t h2d = nullptr, d2h = nullptr; // spill tier
 		std::deque<cudaEvent_t> frees;             // one event per eviction (after its D2H + free), oldest first
 		cudaEvent_t marks[2] = {nullptr, nullptr};
@@ -207,6 +210,36 @@ class executor {
 	std::unordered_map<int64_t, size_t> trace_open_;
 	std::vector<cudaEvent_t> trace_base_; // per executor GPU
 	std::map<std::string, kernel_timing> ktimes_;
+
+	// ---- CUDA-graph replay of repeated submissions --------------------------------------
+	// Iterative programs submit the same task pattern again and again (a heat step a->b, then
+	// b->a, ...). When a submission (the tasks of one mt_flush) consists only of execute / copy
+	// tasks on one GPU, no spill tier, tracing or kernel profiling is active, and its signature
+	// (kinds, kernels, chunk ids, regions, arguments, intra-submission dependencies) has been seen
+	// before, its GPU work is captured once into a CUDA graph (stream capture forked over the
+	// device's streams, so the graph keeps the DAG's concurrency) and from then on each
+	// occurrence is one cudaGraphLaunch after waiting for its external dependencies. All tasks
+	// of a replay complete on one event (reference counted in shared_ev_). MTB_NO_GRAPHS=1
+	// disables it.
+	struct graph_entry {
+		cudaGraphExec_t exec = nullptr;
+		int gpu = 0;
+		int64_t tasks = 0, kernels = 0, copies = 0;
+		uint64_t bytes_copied = 0;
+	};
+	bool graphs_on_ = std::getenv("MTB_NO_GRAPHS") == nullptr;
+	bool capturing_ = false;
+	int64_t capture_first_ = -1;
+	std::vector<task> gbatch_; // buffered tasks of the current submission (graph mode)
+	std::unordered_map<std::string, graph_entry> graphs_;
+	std::unordered_map<std::string, int> sig_seen_;
+	std::unordered_map<cudaEvent_t, int> shared_ev_;
+	bool graph_eligible(const std::vector<task>& b, int* gpu) const;
+	std::string signature(const std::vector<task>& b) const;
+	bool capture(const std::vector<task>& b, int gpu, graph_entry& out);
+	void replay(const graph_entry& g, const std::vector<task>& b);
+	void release_done_event(cudaEvent_t ev, int gpu);
+	void issue_batch();
 
 	ldev& dev(device_id d);
 	int ord(int gpu_index) const { return gpus_[static_cast<size_t>(gpu_index)].ordinal; }

@@ -34,6 +34,7 @@ struct heat_args {
 	int64_t rows, cols; // domain (zero padding outside)
 	int64_t r0, r1;     // output rows [r0, r1)
 	int64_t c0, c1;     // vectorised output columns [c0, c1), (c1 - c0) % 4 == 0
+	int64_t seg;        // rows per CTA segment (kSegRows, fewer for small superblocks)
 	float a;
 };
 
@@ -63,8 +64,8 @@ __global__ void __launch_bounds__(kThreads, 4) heat2d_vec_kernel(heat_args p) {
 	const int64_t warp_j0 = j - lane * 4;
 	const int64_t rem = (p.c1 - warp_j0) / 4 - 1;
 	const int last_lane = rem < 31 ? static_cast<int>(rem) : 31;
-	const int64_t r0 = p.r0 + static_cast<int64_t>(blockIdx.y) * kSegRows;
-	const int64_t r1 = p.r1 < r0 + kSegRows ? p.r1 : r0 + kSegRows;
+	const int64_t r0 = p.r0 + static_cast<int64_t>(blockIdx.y) * p.seg;
+	const int64_t r1 = p.r1 < r0 + p.seg ? p.r1 : r0 + p.seg;
 	if(r0 >= r1) return;
 
 	float4 up = load_row4(p, r0 - 1, j, active);
@@ -153,7 +154,12 @@ int launch_heat2d(const mt_launch_ctx* c, void* stream) {
 			p.c0 = col_lo;
 			p.c1 = vec_hi;
 			const int64_t strips = (vec_hi - col_lo + kColsPerCta - 1) / kColsPerCta;
-			const int64_t segs = (p.r1 - p.r0 + kSegRows - 1) / kSegRows;
+			// small superblocks (e.g. the 1024 x 4096 chunks of BASELINE C1) would launch a few
+			// dozen CTAs: shorten the segments until the launch has two CTAs per SM (the extra
+			// halo-row reads, 2 per segment, mostly hit L2)
+			p.seg = kSegRows;
+			while(p.seg > 8 && strips * ((p.r1 - p.r0 + p.seg - 1) / p.seg) < 2 * 148) p.seg /= 2;
+			const int64_t segs = (p.r1 - p.r0 + p.seg - 1) / p.seg;
 			if(segs > 65535) return 3;
 			heat2d_vec_kernel<<<dim3(static_cast<unsigned>(strips), static_cast<unsigned>(segs)), kThreads, 0, s>>>(p);
 		}
