@@ -506,6 +506,47 @@ def run_ooc(rows, cols, chunk_rows, capacity_gib, host_gib, iters, warmup, looka
             "lookahead_tasks": la, "warmup_s": t_setup, "evictions": s1["evictions"] - s0["evictions"]}
 
 
+def run_c1(iters, ref_iters, hbm, cpu):
+    """BASELINE configs[0] (the reference's CPU scenario): heat2d 4096^2 f32, row-block stencil
+    distribution into 4 chunks, one distributed launch per iteration, on one GPU (4 logical
+    devices), next to the reference CPU executor on the same grid and chunking."""
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+    rows = cols = 4096
+    with mb.context(workers=1, devices=4, num_gpus=1, retain_plan=False) as ctx:
+        a, b, work = setup_heat(ctx, rows, cols, 4)
+
+        def run(n):
+            nonlocal a, b
+            for _ in range(n):
+                ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN)
+                ctx.flush()
+                a, b = b, a
+
+        run(10)
+        ctx.synchronize()
+        ctx.mark(0)
+        run(iters)
+        ctx.mark(1)
+        ms = ctx.elapsed_ms() / iters
+        ctx.synchronize()
+        st = ctx.exec_stats()
+    gbs = BYTES_PER_CELL * rows * cols / (ms / 1e3) / 1e9
+    out = {"workload": f"heat2d {rows}x{cols} f32, 4 chunks (stencil_dist halo [1,0]), {iters} iterations, one launch per iteration",
+           "value": rows * cols / (ms / 1e3), "unit": "cell-updates/s", "ms_per_iter": ms,
+           "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                        "note": "step time incl. planning, halo copies and graph launch; small grid: issue-bound"},
+           "graph_replays": st.get("graph_replays")}
+    if cpu:
+        try:
+            rate, dt = cpu_reference_rate(rows, cols, ref_iters, 4)
+            out["cpu_baseline"] = {"value": rate, "unit": "cell-updates/s", "cores": 4, "kind": "reference",
+                                   "sample": f"the same 4096^2 grid and 4 chunks (one device thread each), {ref_iters} iterations ({dt:.1f} s)"}
+        except Exception as e:  # noqa: BLE001
+            out["cpu_baseline"] = {"unavailable": str(e)}
+    return out
+
+
 def run_b200(args):
     import numpy as np
     import torch
@@ -698,6 +739,9 @@ def run_b200(args):
         contraction["roofline"] = {"bound": "tensor", "achieved": kach, "peak": tburst, "unit": "TFLOP/s", "frac": kach / tburst,
                                    "peak_kind": "measured burst (cuBLAS bf16 8192^3, best of 10)", "frac_of_sustained": kach / tpeak,
                                    "kernel": "gemm_bf16_nt_kernel (tcgen05.mma cta_group::1 M128 N256, TMA, TMEM)"}
+    c1 = None
+    if ws == 1 and args.c1:
+        c1 = run_c1(100, args.c1_ref_iters, peaks()[0], rank == 0 and args.cpu_baseline)
     c4 = None
     if args.c4:
         try:
@@ -727,6 +771,7 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "contraction": contraction,
             "reductions": c4,
+            "small_grid": c1,
         }
     if ws > 1:
         import torch.distributed as dist
@@ -769,6 +814,8 @@ def main():
     p.add_argument("--hist-n", type=int, default=4_000_000_000)
     p.add_argument("--strip", type=int, default=128, help="N>1: rows of the halo-facing superblocks per GPU")
     p.add_argument("--km-n", type=int, default=1_000_000_000)
+    p.add_argument("--no-c1", dest="c1", action="store_false", help="skip the BASELINE configs[0] leg (4096^2, 4 chunks)")
+    p.add_argument("--c1-ref-iters", type=int, default=5)
     p.add_argument("--ooc-gib", type=float, default=80.0, help="C5 out-of-core working set (2 arrays), 0 to skip")
     p.add_argument("--ooc-cap-gib", type=float, default=24.0, help="device capacity for the C5 leg (one array must not fit)")
     p.add_argument("--ooc-iters", type=int, default=12)
