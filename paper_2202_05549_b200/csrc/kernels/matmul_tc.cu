@@ -59,6 +59,8 @@ struct gemm_args {
 	int m_blocks, n_blocks, k_blocks;
 	int group_m; // rasterisation group (M units)
 	uint64_t hint_a, hint_b; // L2 cache policies of the operand loads
+	int no_store;            // diagnostics (MTB_GEMM_NOSTORE): skip the C stores
+	int n_major;             // diagnostics (MTB_GEMM_NMAJOR): rasterise N-first
 };
 
 // ---- PTX wrappers -------------------------------------------------------------------------
@@ -184,6 +186,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 // tile t -> (M unit, N block), rasterised in groups of GROUP_M M units (units = M blocks, or
 // M block pairs for the CTA-pair kernel)
 __device__ __forceinline__ void tile_coords(int t, const gemm_args& p, int& mb, int& nb, int m_units) {
+	if(p.n_major) { // diagnostics: groups of group_m N blocks, M fastest across the group
+		const int group = p.group_m * m_units;
+		const int g = t / group;
+		const int first_n = g * p.group_m;
+		const int cols = min(p.group_m, p.n_blocks - first_n);
+		const int r = t % group;
+		nb = first_n + r % cols;
+		mb = r / cols;
+		return;
+	}
 	const int group = p.group_m * p.n_blocks;
 	const int g = t / group;
 	const int first_m = g * p.group_m;
@@ -444,7 +456,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			mbar_wait(&tmem_full[acc], (local >> 1) & 1);
 			tc_fence_after();
 			const int64_t row = static_cast<int64_t>(mu) * 2 * BM + rank * BM + quarter * 32 + lane;
-			const bool row_ok = row < p.m;
+			const bool row_ok = row < p.m && !p.no_store;
 			float* crow = p.c + row * p.ldc;
 			const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
@@ -544,7 +556,10 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	// ~4x the DRAM bytes of the single-CTA kernel (L2 reuse across the wave is lost; the cause is
 	// not understood yet), so problems with both M*N > 16384^2 and K > 16384 stay on single CTAs.
 	const bool big = static_cast<double>(m) * static_cast<double>(n) > 16384.0 * 16384.0 && k > 16384;
-	const bool pair = p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && !big && std::getenv("MTB_GEMM_NO_PAIR") == nullptr;
+	p.no_store = std::getenv("MTB_GEMM_NOSTORE") != nullptr;
+	p.n_major = std::getenv("MTB_GEMM_NMAJOR") != nullptr;
+	const bool force_pair = std::getenv("MTB_GEMM_FORCE_PAIR") != nullptr;
+	const bool pair = p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && (!big || force_pair) && std::getenv("MTB_GEMM_NO_PAIR") == nullptr;
 	CUtensorMap ma, mb;
 	if(!make_map(&ma, a, a_rows, k, lda, BM) || !make_map(&mb, bt, b_rows, k, ldb, pair ? BN / 2 : BN)) return 7;
 	if(!pair) {
