@@ -521,6 +521,7 @@ system_config make_system_config(const mt_config& c) {
 	if(c.device_capacity) sys.memory.device_capacity = c.device_capacity;
 	if(c.host_capacity) sys.memory.host_capacity = c.host_capacity;
 	if(c.staging_threshold) sys.memory.staging_threshold = c.staging_threshold;
+	if(c.disk_capacity) sys.memory.disk_capacity = c.disk_capacity;
 	sys.memory.disk_in_memory = true;
 	sys.progress_timeout = std::chrono::milliseconds(600000);
 	return sys;

@@ -217,7 +217,8 @@ class Context:
 
     def __init__(self, lib: capi.Lib, workers=1, devices=1, execute=True, compat_deps=False, suppress_conflict_deps=False,
                  num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0, record_accesses=False,
-                 lookahead_tasks=0, worker_rank=None, gpu_base=0, collective_reduce=False, retain_plan=True):
+                 lookahead_tasks=0, worker_rank=None, gpu_base=0, collective_reduce=False, retain_plan=True, disk_capacity=0,
+                 spill_dir=None):
         self.lib = lib
         self.dist = Distributions(lib)
         cfg = capi.Config()
@@ -234,6 +235,9 @@ class Context:
         cfg.lookahead_tasks = int(lookahead_tasks)
         cfg.collective_reduce = int(collective_reduce)
         cfg.drop_executed_tasks = int(not retain_plan)  # long runs: forget tasks once queued
+        cfg.disk_capacity = int(disk_capacity)
+        self._spill_dir = spill_dir.encode() if spill_dir else None
+        cfg.spill_dir = self._spill_dir
         if worker_rank is not None:  # one process per worker
             cfg.single_worker, cfg.worker_rank, cfg.gpu_base = 1, int(worker_rank), int(gpu_base)
         self.single_worker = worker_rank is not None
@@ -433,7 +437,7 @@ class Context:
             return {}
         keys = ["tasks", "kernels", "copies", "bytes_copied", "bytes_sent", "bytes_received", "peak_device_bytes", "evictions",
                 "spill_bytes_d2h", "spill_bytes_h2d", "dead_drops", "dead_skips", "host_reclaims",
-                "host_write_bytes", "host_read_bytes", "graph_captures", "graph_replays"]
+                "host_write_bytes", "host_read_bytes", "graph_captures", "graph_replays", "bytes_host_to_disk", "bytes_disk_to_host"]
         out = (C.c_uint64 * len(keys))()
         self.lib.check(self.lib.exec_stats(ex, out, len(keys)))
         return dict(zip(keys, [int(v) for v in out]))

@@ -13,7 +13,7 @@ incoherent replicas, 3 internal error; manta.cpp:15-18, 166-178).
   restatement of make_fuzz_scenario (mt_fuzz_scenario_json), seed for seed the reference's.
 
 System flags follow add_system_flags (manta.cpp:46-54). On the GPU executor `--throttle` is
-informational, there is no disk tier (`--disk-capacity` is accepted and unused), and
+informational, `--disk-capacity` sizes the spill file below the pinned-host tier, and
 `--seed` (randomised ready-task choice in the reference's host scheduler) has no counterpart:
 tasks run as soon as their CUDA events allow, concurrently over `--streams` streams per device.
 """
@@ -82,7 +82,7 @@ def load(path: str) -> dict:
 def system_of(sc: dict, flags) -> dict:
     """the scenario's system block with command-line overrides (to_overrides, manta.cpp:30-44)"""
     s = dict(sc.get("system", {}))
-    for key in ("workers", "devices", "device_capacity", "host_capacity"):
+    for key in ("workers", "devices", "device_capacity", "host_capacity", "disk_capacity"):
         v = getattr(flags, key, None) if flags is not None else None
         if v is not None:
             s[key] = v
@@ -104,9 +104,10 @@ def make_context(sysd: dict, execute: bool, oracle_mode=False, suppress=False, s
     cap = int(sysd.get("device_capacity", DEFAULT_DEVICE_CAPACITY))
     spill = execute and not oracle_mode and cap < DEFAULT_DEVICE_CAPACITY
     host = int(sysd.get("host_capacity", DEFAULT_HOST_CAPACITY)) if spill else 0
+    disk = int(sysd.get("disk_capacity", 0)) if spill else 0
     return context(workers=workers, devices=devices, execute=execute, num_gpus=1 if execute else 0, suppress_conflict_deps=suppress, compat_deps=compat,
                    streams_per_device=streams, device_capacity=cap if spill else 0, host_capacity=max(host, cap) if spill else 0,
-                   staging_threshold=int(sysd.get("staging_threshold", 0)))
+                   staging_threshold=int(sysd.get("staging_threshold", 0)), disk_capacity=disk)
 
 
 def run_scenario(sc: dict, sysd: dict, oracle_mode=False, suppress=False, streams=0, compat=False, trace=False):
@@ -292,7 +293,7 @@ def _system_flags(p: argparse.ArgumentParser):
     p.add_argument("--devices", type=int, help="Override the devices per worker")
     p.add_argument("--device-capacity", dest="device_capacity", type=int, help="Device memory capacity in bytes")
     p.add_argument("--host-capacity", dest="host_capacity", type=int, help="Host memory capacity in bytes")
-    p.add_argument("--disk-capacity", dest="disk_capacity", type=int, help="Disk tier capacity in bytes (no disk tier on B200)")
+    p.add_argument("--disk-capacity", dest="disk_capacity", type=int, help="Disk tier capacity in bytes")
     p.add_argument("--throttle", type=int, help="Staging throttle threshold in bytes (informational)")
     p.add_argument("--seed", type=int, help="Accepted for compatibility; GPU tasks run as their events allow")
     p.add_argument("--streams", type=int, default=0, help="Compute streams per device (0 = 4)")

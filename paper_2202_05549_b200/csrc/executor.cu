@@ -3,6 +3,8 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <fcntl.h>
+#include <unistd.h>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -348,6 +350,10 @@ executor::~executor() {
 		if(b.host) cudaFreeHost(b.host);
 	}
 	for(auto& [sz, blk] : host_free_) cudaFreeHost(blk.first);
+	if(spill_fd_ >= 0) {
+		::close(spill_fd_);
+		::unlink(spill_path_.c_str());
+	}
 	for(auto& [id, d] : done_) cudaEventDestroy(d.ev);
 	for(auto& pool : free_events_)
 		for(auto ev : pool) cudaEventDestroy(ev);
@@ -917,9 +923,14 @@ void* executor::host_alloc(uint64_t bytes, int gpu, int64_t exclude) {
 	while(host_used_ + bytes > cfg_.host_capacity) {
 		buffer* pick = nullptr;
 		for(auto& [id, b] : bufs_) {
-			if(id == exclude || !b.ptr || !b.host) continue;
+			// resident chunks' copies, and blocks of evicted chunks whose data was dropped as dead
+			if(id == exclude || !b.host || (!b.ptr && b.host_valid)) continue;
 			const bool better = !pick || (pick->host_valid && !b.host_valid) || (pick->host_valid == b.host_valid && (pick->bytes != bytes && b.bytes == bytes));
 			if(better) pick = &b;
+		}
+		if(!pick && cfg_.disk_capacity > 0) {
+			if(void* blk = spill_host_to_disk(bytes, exclude)) return blk;
+			continue; // a block of another size went to disk and was freed
 		}
 		if(!pick)
 			throw execution_error("host tier exhausted: " + std::to_string(host_used_ + bytes) + " bytes needed, capacity " + std::to_string(cfg_.host_capacity));
@@ -952,6 +963,78 @@ void* executor::host_alloc(uint64_t bytes, int gpu, int64_t exclude) {
 
 void executor::host_release(void* p, uint64_t bytes, cudaEvent_t after) { host_free_.emplace(bytes, std::make_pair(p, after)); }
 
+uint64_t executor::disk_alloc(uint64_t bytes) {
+	if(spill_fd_ < 0) {
+		const char* dir = cfg_.spill_dir.empty() ? (std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp") : cfg_.spill_dir.c_str();
+		std::string tmpl = std::string(dir) + "/manta-b200-spill-XXXXXX";
+		std::vector<char> path(tmpl.begin(), tmpl.end());
+		path.push_back('\0');
+		spill_fd_ = ::mkstemp(path.data());
+		if(spill_fd_ < 0) throw execution_error("cannot create spill file in " + std::string(dir));
+		spill_path_ = path.data();
+	}
+	auto it = disk_free_.find(bytes);
+	if(it == disk_free_.end() && disk_end_ + bytes > cfg_.disk_capacity) it = disk_free_.lower_bound(bytes);
+	if(it != disk_free_.end()) {
+		const uint64_t off = it->second;
+		disk_free_.erase(it);
+		return off;
+	}
+	if(disk_end_ + bytes > cfg_.disk_capacity)
+		throw execution_error("disk tier exhausted: " + std::to_string(bytes) + " more bytes, capacity " + std::to_string(cfg_.disk_capacity));
+	const uint64_t off = disk_end_;
+	disk_end_ += bytes;
+	return off;
+}
+
+void executor::disk_release(buffer& b) {
+	if(b.disk_off >= 0) disk_free_.emplace(b.bytes, static_cast<uint64_t>(b.disk_off));
+	b.disk_off = -1;
+	b.disk_valid = false;
+}
+
+void executor::disk_read(const buffer& b, void* dst) {
+	uint64_t done = 0;
+	while(done < b.bytes) {
+		const ssize_t r = ::pread(spill_fd_, static_cast<char*>(dst) + done, b.bytes - done, static_cast<off_t>(b.disk_off + done));
+		if(r <= 0) throw execution_error("spill read failed");
+		done += static_cast<uint64_t>(r);
+	}
+	ctr_.bytes_disk_to_host += b.bytes;
+}
+
+// The host tier is full and holds only copies of evicted chunks: write the least recently used
+// one (same size as the request when possible) to the spill file and reuse or free its block.
+void* executor::spill_host_to_disk(uint64_t bytes, int64_t exclude) {
+	buffer* pick = nullptr;
+	for(auto& [id, b] : bufs_) {
+		if(id == exclude || b.ptr || !b.host || !b.host_valid) continue;
+		const bool better = !pick || (pick->bytes != bytes && b.bytes == bytes) || ((pick->bytes == bytes) == (b.bytes == bytes) && b.last_use < pick->last_use);
+		if(better) pick = &b;
+	}
+	if(!pick) throw execution_error("host tier exhausted and nothing left to spill to disk");
+	buffer& b = *pick;
+	if(b.evicted) check_cuda(cudaEventSynchronize(b.evicted), "cudaEventSynchronize"); // its D2H has landed
+	if(!b.disk_valid) {
+		if(b.disk_off < 0) b.disk_off = static_cast<int64_t>(disk_alloc(b.bytes));
+		uint64_t done = 0;
+		while(done < b.bytes) {
+			const ssize_t w = ::pwrite(spill_fd_, static_cast<const char*>(b.host) + done, b.bytes - done, static_cast<off_t>(b.disk_off + done));
+			if(w <= 0) throw execution_error("spill write failed");
+			done += static_cast<uint64_t>(w);
+		}
+		b.disk_valid = true;
+		ctr_.bytes_host_to_disk += b.bytes;
+	}
+	void* blk = b.host;
+	b.host = nullptr;
+	b.host_valid = false;
+	if(b.bytes == bytes) return blk;
+	check_cuda(cudaFreeHost(blk), "cudaFreeHost");
+	host_used_ -= b.bytes;
+	return nullptr;
+}
+
 void executor::evict(int64_t chunk) {
 	buffer& b = buf(chunk);
 	auto& G = gpus_[static_cast<size_t>(b.gpu)];
@@ -961,9 +1044,9 @@ void executor::evict(int64_t chunk) {
 		if(it != done_.end()) check_cuda(cudaStreamWaitEvent(G.d2h, it->second.ev, 0), "cudaStreamWaitEvent");
 	}
 	if(b.restored) check_cuda(cudaStreamWaitEvent(G.d2h, b.restored, 0), "cudaStreamWaitEvent");
-	if(!b.host_valid && dead_ahead(chunk, nullptr)) {
+	if(!b.host_valid && !b.disk_valid && dead_ahead(chunk, nullptr)) {
 		++ctr_.dead_drops; // overwritten before it is read again: no write-back
-	} else if(!b.host_valid) {
+	} else if(!b.host_valid && !b.disk_valid) {
 		if(!b.host) b.host = host_alloc(b.bytes, b.gpu, chunk);
 		check_cuda(cudaMemcpyAsync(b.host, b.ptr, b.bytes, cudaMemcpyDeviceToHost, G.d2h), "cudaMemcpyAsync D2H (evict)");
 		b.host_valid = true;
@@ -1050,7 +1133,7 @@ void executor::restore(int64_t chunk, const std::vector<int64_t>& pinned, const 
 	check_cuda(cudaSetDevice(ord(b.gpu)), "cudaSetDevice");
 	alloc_wait(b.gpu, G.h2d);
 	check_cuda(cudaMallocFromPoolAsync(&b.ptr, b.bytes, G.pool, G.h2d), "cudaMallocFromPoolAsync (restore)");
-	const bool needed = b.host_valid && !dead_ahead(chunk, &current);
+	const bool needed = (b.host_valid || b.disk_valid) && !dead_ahead(chunk, &current);
 	if(std::getenv("MTB_SPILL_TRACE"))
 		std::fprintf(stderr, "[spill] restore chunk %ld for task %ld (%s) copy %d\n", static_cast<long>(chunk), static_cast<long>(current.id),
 		    task_kind_name(current.kind), needed ? 1 : 0);
@@ -1064,6 +1147,14 @@ void executor::restore(int64_t chunk, const std::vector<int64_t>& pinned, const 
 		return;
 	}
 	if(b.evicted) check_cuda(cudaStreamWaitEvent(G.h2d, b.evicted, 0), "cudaStreamWaitEvent"); // its own write-back first
+	if(!b.host_valid) {
+		// the copy is on disk: bring it into a pinned block first (synchronous file read)
+		if(!b.host) b.host = host_alloc(b.bytes, b.gpu, chunk);
+		check_cuda(cudaStreamSynchronize(G.h2d), "cudaStreamSynchronize"); // the block's previous users
+		check_cuda(cudaStreamSynchronize(G.d2h), "cudaStreamSynchronize");
+		disk_read(b, b.host);
+		b.host_valid = true;
+	}
 	check_cuda(cudaMemcpyAsync(b.ptr, b.host, b.bytes, cudaMemcpyHostToDevice, G.h2d), "cudaMemcpyAsync H2D (restore)");
 	if(!b.restored) check_cuda(cudaEventCreateWithFlags(&b.restored, cudaEventDisableTiming), "cudaEventCreate");
 	check_cuda(cudaEventRecord(b.restored, G.h2d), "cudaEventRecord");
@@ -1100,7 +1191,10 @@ void executor::note_use(const task& t) {
 		buffer& b = it->second;
 		b.users.push_back(t.id);
 		b.last_use = clock_;
-		if(w) b.host_valid = false;
+		if(w) {
+			b.host_valid = false;
+			disk_release(b);
+		}
 		if(b.users.size() > 64) {
 			std::vector<int64_t> keep;
 			for(const auto u : b.users) {
@@ -1152,6 +1246,7 @@ void executor::run_delete(const task& t) {
 	}
 	if(b.restored) cudaEventDestroy(b.restored);
 	if(b.evicted) cudaEventDestroy(b.evicted);
+	disk_release(buf(t.chunk));
 	bufs_.erase(t.chunk);
 	finish(t, s);
 }
@@ -1519,10 +1614,17 @@ void executor::download(int64_t chunk, void* host, const box& host_box, const bo
 	check_cuda(cudaSetDevice(ord(b.gpu)), "cudaSetDevice");
 	cudaStream_t s = gpus_[static_cast<size_t>(b.gpu)].service;
 	check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+	std::vector<char> from_disk;
 	if(b.ptr)
 		copy_box(b.ptr, b.region, ord(b.gpu), host, host_box, -1, region, dtype_size(b.type), s);
-	else
+	else if(b.host && b.host_valid)
 		copy_box(b.host, b.region, -1, host, host_box, -1, region, dtype_size(b.type), s); // evicted: host copy is current
+	else if(b.disk_valid) {
+		from_disk.resize(b.bytes);
+		disk_read(b, from_disk.data());
+		copy_box(from_disk.data(), b.region, -1, host, host_box, -1, region, dtype_size(b.type), s);
+	} else if(b.host)
+		copy_box(b.host, b.region, -1, host, host_box, -1, region, dtype_size(b.type), s);
 	check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
 }
 
@@ -1537,8 +1639,10 @@ void executor::upload(int64_t chunk, const void* host, const box& host_box) {
 		copy_box(host, host_box, -1, b.ptr, b.region, ord(b.gpu), b.region, dtype_size(b.type), s);
 		b.host_valid = false;
 	} else {
+		if(!b.host) b.host = host_alloc(b.bytes, b.gpu, chunk);
 		copy_box(host, host_box, -1, b.host, b.region, -1, b.region, dtype_size(b.type), s);
 		b.host_valid = true;
+		disk_release(b);
 	}
 	check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
 }
@@ -1726,8 +1830,8 @@ std::string executor::report_json() {
 	os << "{\"workers\": [";
 	for(int w = 0; w < cfg_.workers; ++w) {
 		os << (w ? ", " : "") << "{\"worker\": " << w << ", \"evictions\": " << (w == 0 ? ctr_.evictions : 0)
-		   << ", \"bytes_device_to_host\": " << (w == 0 ? ctr_.bytes_device_to_host : 0) << ", \"bytes_host_to_disk\": 0"
-		   << ", \"bytes_host_to_device\": " << (w == 0 ? ctr_.bytes_host_to_device : 0) << ", \"bytes_disk_to_device\": 0"
+		   << ", \"bytes_device_to_host\": " << (w == 0 ? ctr_.bytes_device_to_host : 0) << ", \"bytes_host_to_disk\": " << (w == 0 ? ctr_.bytes_host_to_disk : 0)
+		   << ", \"bytes_host_to_device\": " << (w == 0 ? ctr_.bytes_host_to_device : 0) << ", \"bytes_disk_to_device\": " << (w == 0 ? ctr_.bytes_disk_to_host : 0)
 		   << ", \"bytes_sent\": " << (w == 0 ? ctr_.bytes_sent : 0) << ", \"bytes_received\": " << (w == 0 ? ctr_.bytes_received : 0)
 		   << ", \"staging_checks\": 0, \"staging_violations\": 0, \"peak_device_bytes\": [" << ctr_.peak_device_bytes << "], \"tasks\": ["
 		   << tasks[static_cast<size_t>(w)] << "]}";

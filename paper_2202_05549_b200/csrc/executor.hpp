@@ -43,6 +43,8 @@ struct executor_config {
 	int first_worker = 0;         // workers [first, first+local) execute here (multi-process)
 	int gpu_base = 0;             // first CUDA device ordinal this executor uses
 	int local_workers = -1;       // -1: all workers
+	uint64_t disk_capacity = 0;   // disk tier below the host tier (0: none)
+	std::string spill_dir;        // spill file directory ("" = system temp directory)
 };
 
 struct exec_counters {
@@ -61,6 +63,7 @@ struct exec_counters {
 	uint64_t host_reclaims = 0; // host copies of resident chunks taken back when the host tier is full
 	uint64_t bytes_host_in = 0, bytes_host_out = 0; // host_write / host_read tasks
 	uint64_t graph_captures = 0, graph_replays = 0;  // CUDA-graph replay of repeated submissions
+	uint64_t bytes_host_to_disk = 0, bytes_disk_to_host = 0; // disk tier
 };
 
 class executor {
@@ -127,6 +130,8 @@ class executor {
 		void* host = nullptr;     // pinned host copy
 		bool host_valid = false;  // host copy equals the device contents
 		std::vector<int64_t> users; // tasks that touched the device copy since it became resident
+		int64_t disk_off = -1;    // spill-file block holding a copy (disk tier)
+		bool disk_valid = false;  // that copy equals the current contents
 		cudaEvent_t restored = nullptr; // completes when the last H2D restore has landed
 		cudaEvent_t evicted = nullptr;  // completes when the last eviction's D2H has landed
 		uint64_t last_use = 0;
@@ -240,6 +245,17 @@ class executor {
 	void replay(const graph_entry& g, const std::vector<task>& b);
 	void release_done_event(cudaEvent_t ev, int gpu);
 	void issue_batch();
+
+	// ---- disk tier (memory.cpp:85-159): host copies of evicted chunks move to a spill file when
+	// the pinned-host tier is full, and come back through a pinned block on restore
+	int spill_fd_ = -1;
+	std::string spill_path_;
+	uint64_t disk_end_ = 0;
+	std::multimap<uint64_t, uint64_t> disk_free_; // block size -> offset
+	uint64_t disk_alloc(uint64_t bytes);
+	void disk_release(buffer& b);
+	void* spill_host_to_disk(uint64_t bytes, int64_t exclude);
+	void disk_read(const buffer& b, void* dst);
 
 	ldev& dev(device_id d);
 	int ord(int gpu_index) const { return gpus_[static_cast<size_t>(gpu_index)].ordinal; }

@@ -89,3 +89,52 @@ def test_stencil1d_eviction_matches_serial():
     tight, st = run(n * 4 // 2, 1 << 30)
     assert st["evictions"] > 0
     assert np.array_equal(free.view(np.uint32), tight.view(np.uint32))
+
+
+def test_disk_tier_below_the_host_tier(okern, tmp_path):
+    """device capacity 1/4 of the working set and a host tier of one chunk pair: evicted copies
+    must move on to the spill file (memory.cpp:113-159) and come back bit-exact"""
+    rows, cols, chunk_rows, iters = 1024, 2048, 64, 6
+    ws = 2 * rows * cols * 4  # 16 MiB in 32 chunks of 512 KiB
+    chunk = chunk_rows * cols * 4
+    with mb.context(workers=1, devices=1, num_gpus=1, device_capacity=ws // 4, host_capacity=6 * chunk, disk_capacity=ws,
+                    spill_dir=str(tmp_path)) as ctx:
+        devs = ctx.devices
+        dist = lambda: ctx.dist.stencil([rows, cols], [chunk_rows, cols], [1, 0], devs)  # noqa: E731
+        a = ctx.create_array([rows, cols], "f32", dist(), 0)
+        b = ctx.create_array([rows, cols], "f32", dist(), 0)
+        work = ctx.dist.block_work([rows, cols], [16, 16], [chunk_rows, cols], devs)
+        ctx.launch("ramp2d_f32", [rows, cols], [16, 16], work, [rows, cols, 1000, 0.0, 1.0, Arr(a)], "global [i, j] => write out[i,j]")
+        ctx.flush()
+        for _ in range(iters):
+            ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT)
+            ctx.flush()
+            a, b = b, a
+        ctx.synchronize()
+        stats = ctx.exec_stats()
+        out = ctx.read(a)
+        report = ctx.report_json()
+    assert stats["bytes_host_to_disk"] > 0 and stats["bytes_disk_to_host"] > 0
+    assert '"bytes_host_to_disk": %d' % stats["bytes_host_to_disk"] in report
+    want = oracle_heat(okern, rows, cols, iters)
+    assert np.array_equal(out.view(np.uint32), want.view(np.uint32))
+    assert list(tmp_path.iterdir()) == []  # the spill file is removed with the context
+
+
+def test_disk_tier_exhaustion_is_an_execution_error(tmp_path):
+    rows, cols, chunk_rows = 1024, 2048, 64
+    ws = 2 * rows * cols * 4
+    chunk = chunk_rows * cols * 4
+    with pytest.raises(mb.ExecutionError):
+        with mb.context(workers=1, devices=1, num_gpus=1, device_capacity=ws // 4, host_capacity=4 * chunk, disk_capacity=2 * chunk,
+                        spill_dir=str(tmp_path)) as ctx:
+            devs = ctx.devices
+            dist = lambda: ctx.dist.stencil([rows, cols], [chunk_rows, cols], [1, 0], devs)  # noqa: E731
+            a = ctx.create_array([rows, cols], "f32", dist(), 0)
+            b = ctx.create_array([rows, cols], "f32", dist(), 0)
+            work = ctx.dist.block_work([rows, cols], [16, 16], [chunk_rows, cols], devs)
+            ctx.launch("ramp2d_f32", [rows, cols], [16, 16], work, [rows, cols, 1000, 0.0, 1.0, Arr(a)], "global [i, j] => write out[i,j]")
+            for _ in range(4):
+                ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT)
+                a, b = b, a
+            ctx.synchronize()
