@@ -6,6 +6,7 @@
 #include <fcntl.h>
 #include <unistd.h>
 #include <cstdio>
+#include <set>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -354,7 +355,11 @@ executor::~executor() {
 		::close(spill_fd_);
 		::unlink(spill_path_.c_str());
 	}
-	for(auto& [id, d] : done_) cudaEventDestroy(d.ev);
+	std::set<cudaEvent_t> live; // replayed submissions share one completion event
+	for(auto& [id, d] : done_) live.insert(d.ev);
+	for(auto e : live) cudaEventDestroy(e);
+	for(auto& [sig, g] : graphs_)
+		if(g.exec) cudaGraphExecDestroy(g.exec);
 	for(auto& pool : free_events_)
 		for(auto ev : pool) cudaEventDestroy(ev);
 	for(auto& L : ldevs_) {
