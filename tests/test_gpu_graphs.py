@@ -100,3 +100,34 @@ def test_replay_interleaved_with_other_work(okern):
         okern.oracle_heat2d(C.c_int64(rows), C.c_int64(cols), C.c_double(al), cur.ctypes.data_as(F32), nxt.ctypes.data_as(F32))
         cur, nxt = nxt, cur
     assert np.array_equal(got.view(np.uint32), cur.view(np.uint32))
+
+
+def test_fuzz_scenarios_with_repeats_match_the_reference(ref):
+    """the reference's random scenarios with every launch repeated three times: repeated
+    submissions are captured and replayed as CUDA graphs (when eligible), and the final arrays
+    must still equal the reference's sequential oracle run"""
+    import ctypes as C2
+
+    from paper_2202_05549_b200 import scenario as S
+    replays = 0
+    checked = 0
+    for i in range(60):
+        seed = (0x9E3779B97F4A7C15 * (i + 101)) % (1 << 64)
+        n = C2.c_int64(0)
+        buf = C2.create_string_buffer(1 << 20)
+        ref.check(ref.fuzz_scenario_json(seed, buf, 1 << 20, C2.byref(n)))
+        sc = json.loads(buf.value)
+        for launch in sc["launches"]:
+            launch["repeat"] = 3
+        sc["system"]["device_capacity"] = 256 << 20  # no spill: graphs are eligible
+        try:
+            want, _ = S.reference_run(ref, sc, oracle_mode=True)
+        except mb.MantaError:
+            continue
+        with mb.context(workers=sc["system"]["workers"], devices=sc["system"]["devices"], num_gpus=1) as ctx:
+            S.register_gather_kernels(ctx, sc)
+            got, coherent = S.run(ctx, sc)
+            replays += ctx.exec_stats()["graph_replays"]
+        assert coherent and S.compare(got, want, 1e-6) == [], seed
+        checked += 1
+    assert checked >= 30 and replays > 0
