@@ -268,6 +268,7 @@ void submit_tasks(mt_exec& e, const std::vector<task>& ts) {
 }
 
 void flush(mt_ctx* ctx) {
+	nvtx3::scoped_range_in<mtb::nvtx_domain> range{"mt_flush"};
 	if(!ctx->exec) {
 		ctx->plan->consume_pending([](const task&) {});
 		return;
@@ -372,6 +373,7 @@ int mt_array_chunks(mt_ctx* ctx, int64_t id, mt_chunk_desc* out, int64_t cap, in
 int mt_launch(mt_ctx* ctx, const char* kernel, const mt_rect* grid, const int64_t* block, const mt_superblock* work, int64_t nwork,
     const mt_launch_arg* args, int32_t nargs, const char* ann_text, int64_t* first, int64_t* last) {
 	return guarded([&] {
+		nvtx3::scoped_range_in<mtb::nvtx_domain> range{kernel ? kernel : "mt_launch"}; // planning of one launch (NVTX, visible in nsys)
 		const box g = to_box(*grid);
 		std::vector<superblock> w;
 		w.reserve(static_cast<size_t>(nwork));

@@ -697,6 +697,7 @@ void executor::replay(const graph_entry& g, const std::vector<task>& b) {
 			if(it == done_.end() || it->second.stream == G.graph) continue;
 			check_cuda(cudaStreamWaitEvent(G.graph, it->second.ev, 0), "cudaStreamWaitEvent");
 		}
+	nvtx3::scoped_range_in<nvtx_domain> range{"graph replay"};
 	check_cuda(cudaGraphLaunch(g.exec, G.graph), "cudaGraphLaunch");
 	cudaEvent_t ev = take_event(g.gpu);
 	check_cuda(cudaEventRecord(ev, G.graph), "cudaEventRecord");
@@ -734,6 +735,7 @@ void executor::drain(bool all) {
 }
 
 void executor::issue(const task& t) {
+	nvtx3::scoped_range_in<nvtx_domain> range{task_kind_name(t.kind)};
 	if(spill_) stage(t);
 	switch(t.kind) {
 	case task_kind::create: run_create(t); break;

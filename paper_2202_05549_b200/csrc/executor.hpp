@@ -24,6 +24,7 @@
 #include <string>
 #include <tuple>
 #include <cstdlib>
+#include <nvtx3/nvtx3.hpp>
 #include <unordered_map>
 #include <vector>
 
@@ -31,6 +32,12 @@
 #include "registry.hpp"
 
 namespace mtb {
+
+// NVTX ranges (tracing): planning of each launch, each flush, and the host-side issue
+// of every task by kind, in the "manta-b200" domain. Header-only NVTX 3; no cost without a tool.
+struct nvtx_domain {
+	static constexpr char const* name{"manta-b200"};
+};
 
 struct executor_config {
 	int workers = 1;
