@@ -9,12 +9,18 @@ resident in HBM (2 x 16 GiB, far larger than the 126 MB L2, so no flush is neede
 Reports (one JSON line, rank 0):
   value     cell-updates/s over K timed steps, CUDA events (all streams joined), max over ranks
   e2e       same metric through the public API with HOST buffers: per step, upload the grid
-            from pinned memory (mt_array_write), run `e2e_iters` heat iterations, read the
-            grid back (mt_array_read); wall clock around the synchronous calls
+            from pinned memory, run `e2e_iters` heat iterations, read the grid back; steps
+            pipelined with mt_array_write_async / mt_array_read_async over three array sets
+            (N > 1: each rank moves its own chunk box); wall clock, max over ranks; the
+            synchronous figure is reported beside it
   roofline  heat2d kernel: 8 algorithmic bytes per cell update / its average duration (CUDA
             events on the launching stream) vs MEASURED_PEAKS.json hbm_gbs
+  clocks    nvidia-smi SM clocks and throttle reasons sampled during the timed region
   cpu_baseline  the reference CPU executor (oracle/_ref, the unmodified reference compiled from
             its sources) running the same kernel on a bounded row sample, all host threads
+  N = 1 only: contraction (C3, tcgen05 bf16 32768^3), reductions (C4 histogram / k-means),
+            small_grid (C1, 4096^2 in 4 chunks, with the reference on the same grid),
+            out_of_core (C5 analog: spill tier against the pinned-link bound)
 
 `--impl reference` times the reference CPU executor as the main arm (rank 0 only).
 """
