@@ -360,6 +360,12 @@ executor::~executor() {
 	for(auto e : live) cudaEventDestroy(e);
 	for(auto& [sig, g] : graphs_)
 		if(g.exec) cudaGraphExecDestroy(g.exec);
+	for(auto& r : trace_recs_) {
+		if(r.t0) cudaEventDestroy(r.t0);
+		if(r.t1) cudaEventDestroy(r.t1);
+	}
+	for(auto e : trace_base_)
+		if(e) cudaEventDestroy(e);
 	for(auto& pool : free_events_)
 		for(auto ev : pool) cudaEventDestroy(ev);
 	for(auto& L : ldevs_) {
