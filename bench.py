@@ -756,7 +756,7 @@ def run_b200(args):
         except Exception:
             hbm = 6650.0
         c4 = run_c4(ctx, args.hist_n, args.km_n, 5, hbm, rank == 0 and args.cpu_baseline)
-    traffic = ncu_traffic("heat2d_ncu_summary.json", rows // ws, cols)
+    traffic = ncu_traffic("heat2d_tma_ncu_summary.json", rows // ws, cols)
     out = None
     if rank == 0:
         out = {
@@ -769,7 +769,7 @@ def run_b200(args):
                        "superblocks_per_gpu": 3 if ws > 1 else 1, "l2": "inputs (2 x 16 GiB total) >> L2, no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic[0] if traffic else None, "traffic_source": traffic[1] if traffic else None,
-                         "kernel": "heat2d_vec_kernel", "kernel_ms": kern_ms, "peak_kind": peak_kind,
+                         "kernel": "heat2d_tma_kernel (TMA-staged rows, mbarrier ring)", "kernel_ms": kern_ms, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": BYTES_PER_CELL * (rows // ws) * cols},
             "clocks": clocks,
             "gpu_launches": int(stats1.get("kernels", 0) - stats0.get("kernels", 0)),
