@@ -13,6 +13,8 @@
 #include "../executor.hpp"
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace mtb {
 namespace kern {
 
@@ -205,9 +207,8 @@ __global__ void __launch_bounds__(1024, 1) histogram_pair_kernel(const int32_t* 
 // The exact distance makes the argmin (first minimum, strict '<') identical to the int64
 // reference (kernels.cpp:283-292). Four points per thread share each broadcast centroid load.
 // Points outside the range take the int64 path.
-constexpr int kKmPts = 4;
-
-__global__ void __launch_bounds__(256, 2) kmeans_assign_fast_kernel(const int32_t* __restrict__ points, int64_t pld, int64_t n_local, int k, int d,
+template <int kKmPts, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) kmeans_assign_fast_kernel(const int32_t* __restrict__ points, int64_t pld, int64_t n_local, int k, int d,
     const int32_t* __restrict__ cents, int64_t cld, int32_t* __restrict__ assign) {
 	extern __shared__ int4 cs4[]; // k rows of 16 values -2c (padded to 16 columns), then k |c|^2
 	int32_t* cs = reinterpret_cast<int32_t*>(cs4);
@@ -431,12 +432,17 @@ int launch_kmeans_assign_i32(const mt_launch_ctx* c, void* stream) {
 	const bool fast = d >= 1 && d <= 16 && fast_smem <= 200 * 1024 && vp.stride[1] == 1 && vc.stride[1] == 1 && va.stride[0] == 1 && vc.offset[0] == 0
 	                  && vc.offset[1] == 0 && vp.offset[1] == 0 && vc.extent[0] >= k;
 	if(fast) {
-		ensure_smem(kmeans_assign_fast_kernel, 200 * 1024);
 		const int32_t* pts = static_cast<const int32_t*>(vp.base) + (r.lo[0] - vp.offset[0]) * vp.stride[0];
 		int32_t* asg = static_cast<int32_t*>(va.base) + (r.lo[0] - va.offset[0]);
-		const unsigned blocks = std::max<unsigned>(1, std::min<unsigned>(static_cast<unsigned>((r.total + 1023) / 1024), 148 * 2));
-		kmeans_assign_fast_kernel<<<blocks, 256, fast_smem, s>>>(pts, vp.stride[0], r.total, static_cast<int>(k), static_cast<int>(d),
-		    static_cast<const int32_t*>(vc.base), vc.stride[0], asg);
+		const auto run = [&](auto kern, int pts_per_thread, int per_sm) {
+			ensure_smem(kern, 200 * 1024);
+			const unsigned blocks = std::max<unsigned>(1, std::min<unsigned>(static_cast<unsigned>((r.total + 256 * pts_per_thread - 1) / (256 * pts_per_thread)), 148 * per_sm));
+			kern<<<blocks, 256, fast_smem, s>>>(pts, vp.stride[0], r.total, static_cast<int>(k), static_cast<int>(d), static_cast<const int32_t*>(vc.base),
+			    vc.stride[0], asg);
+		};
+		// 6 points per thread, one 256-thread CTA per SM (measured over 2x3, 4x2, 4x3, 6x1, 8x1
+		// points x CTAs/SM: 6x1 and 8x1 fastest, 2 % ahead of 4x2; 4x3 spills)
+		run(kmeans_assign_fast_kernel<6, 1>, 6, 1);
 		return cudaGetLastError() == cudaSuccess ? 0 : 1;
 	}
 	const size_t smem = static_cast<size_t>(k * d) * sizeof(int32_t);
