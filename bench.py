@@ -617,6 +617,21 @@ def run_b200(args):
     achieved = BYTES_PER_CELL * (rows // ws) * cols / (kern_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
 
+    # best and median of 5 further timed runs (K/5 steps each, device events, max
+    # over ranks) next to the K-step figure
+    repeats = []
+    for _ in range(5):
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        ctx.mark(0)
+        for _ in range(max(1, args.steps // 5)):
+            step()
+        ctx.mark(1)
+        repeats.append(rows * cols * max(1, args.steps // 5) / (barrier_max(ctx.elapsed_ms(), ws) / 1e3))
+    ctx.synchronize()
+    runs = {"best": max(repeats), "median": statistics.median(repeats), "runs": len(repeats), "steps_per_run": max(1, args.steps // 5)}
+
     # e2e through the public API with host buffers
     e2e = None
     if args.e2e_runs > 0:
@@ -772,6 +787,7 @@ def run_b200(args):
                          "kernel": "heat2d_tma_kernel (TMA-staged rows, mbarrier ring)", "kernel_ms": kern_ms, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": BYTES_PER_CELL * (rows // ws) * cols},
             "clocks": clocks,
+            "repeats": runs,
             "gpu_launches": int(stats1.get("kernels", 0) - stats0.get("kernels", 0)),
             "e2e": e2e,
             "cpu_baseline": cpu,
