@@ -825,7 +825,7 @@ def main():
     p.add_argument("--cols", type=int, default=65536)
     p.add_argument("--e2e-iters", type=int, default=100)
     p.add_argument("--e2e-runs", type=int, default=2)
-    p.add_argument("--e2e-pipeline", type=int, default=24, help="pipelined e2e steps (0: report the sequential e2e)")
+    p.add_argument("--e2e-pipeline", type=int, default=40, help="pipelined e2e steps (0: report the sequential e2e)")
     p.add_argument("--e2e-sets", type=int, default=3, help="array sets the pipelined e2e steps rotate over")
     p.add_argument("--ref-rows", type=int, default=512)
     p.add_argument("--ref-iters", type=int, default=6)
