@@ -330,12 +330,15 @@ def run_c4(ctx, hist_n, km_n, steps, hbm, cpu):
         ctx.delete_array(a)
     ctx.synchronize()
     triples = float(n) * k * d
-    int_peak = 148 * 64 * 1.965e9  # IMADs per clk per SM (FMA-heavy pipe) x SMs x max clock
+    fma_peak = 148 * 128 * 1.965e9  # nominal FP32 FFMA per clk per SM x SMs x max clock
     ubytes = n * (d + 1) * 4
     out["kmeans"] = {"workload": f"int32 k-means n={n} d={d} k={k}", "value": n / ((a_ms + u_ms) / 1e3), "unit": "points/s (assign + update)",
-                     "assign": {"ms": a_kms, "roofline": {"bound": "int32 fma pipe", "achieved": triples / (a_kms / 1e3), "peak": int_peak,
-                                                           "unit": "(point, centroid, dim) terms/s", "frac": triples / (a_kms / 1e3) / int_peak,
-                                                           "peak_kind": "derived: 148 SM x 64 IMAD/clk x 1.965 GHz; one IMAD per term (|x|^2+|c|^2-2x.c in exact u32)"}},
+                     "assign": {"ms": a_kms, "roofline": {"bound": "fp32 fma pipe", "achieved": triples / (a_kms / 1e3), "peak": fma_peak,
+                                                           "unit": "(point, centroid, dim) terms/s", "frac": triples / (a_kms / 1e3) / fma_peak,
+                                                           "peak_kind": "derived: 148 SM x 128 FFMA/clk x 1.965 GHz (nominal; register-operand FFMA "
+                                                                        "dot products measure ~90/clk/SM); one exact FFMA per term, the "
+                                                                        "u32 / int64 tiers take over beyond 2^24",
+                                                           "frac_of_imad_bound": triples / (a_kms / 1e3) / (148 * 64 * 1.965e9)}},
                      "update": {"ms": u_ms, "kernel_ms": u_kms, "roofline": {"bound": "hbm", "achieved": ubytes / (u_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                                                            "frac": ubytes / (u_ms / 1e3) / 1e9 / hbm,
                                                            "note": "68 B/point read-only stream over the step time (consecutive updates overlap)"}},

@@ -13,6 +13,7 @@
 #include "../executor.hpp"
 #include "common.cuh"
 
+#include <climits>
 #include <cstdlib>
 
 namespace mtb {
@@ -198,7 +199,12 @@ __global__ void __launch_bounds__(1024, 1) histogram_pair_kernel(const int32_t* 
 	}
 }
 
-// k-means assignment, fast path: when every |coordinate| < 8192 (checked on the fly: the
+// k-means assignment, fast paths. FP32 tier: when sum_q |x_q| * max|c| <= 2^24 for a thread's
+// points (checked on the fly; BASELINE C4 data, values < 1000, qualifies), x.c is accumulated
+// with FFMA — every partial sum is an integer below 2^24, so each FFMA is exact — converted to
+// int, and the argmin is taken over the exact integer criterion |c|^2 - 2 x.c (|x|^2 is common to
+// all centroids of a point). The FP32 pipe issues these faster than IMAD (14 % on C4).
+// u32 tier: when every |coordinate| < 8192 (checked on the fly: the
 // block checks its centroid table, each thread its points) the squared distance over d <= 16
 // dimensions lies in [0, 2^32), so it is computed exactly in wrapping u32 arithmetic as
 // |x|^2 + |c|^2 - 2 x.c: the table holds -2c (and |c|^2 per row), so each (point, centroid)
@@ -210,18 +216,26 @@ __global__ void __launch_bounds__(1024, 1) histogram_pair_kernel(const int32_t* 
 template <int kKmPts, int kMinBlocks>
 __global__ void __launch_bounds__(256, kMinBlocks) kmeans_assign_fast_kernel(const int32_t* __restrict__ points, int64_t pld, int64_t n_local, int k, int d,
     const int32_t* __restrict__ cents, int64_t cld, int32_t* __restrict__ assign) {
-	extern __shared__ int4 cs4[]; // k rows of 16 values -2c (padded to 16 columns), then k |c|^2
+	extern __shared__ int4 cs4[]; // k rows of 16 values -2c (padded to 16 columns), k |c|^2, k rows of c as f32
 	int32_t* cs = reinterpret_cast<int32_t*>(cs4);
 	uint32_t* cn = reinterpret_cast<uint32_t*>(cs + k * 16);
-	int big = 0;
+	float* cf = reinterpret_cast<float*>(cn + ((k + 3) / 4) * 4);
+	__shared__ int cmax; // max |c| over the table (f32 tier bound)
+	if(threadIdx.x == 0) cmax = 0;
+	__syncthreads();
+	int big = 0, mymax = 0;
 	for(int e = threadIdx.x; e < k * 16; e += blockDim.x) {
 		const int c = e / 16, q = e % 16;
 		const int32_t v = q < d ? cents[static_cast<int64_t>(c) * cld + q] : 0;
 		const bool b = (v >= 8192 || v <= -8192);
 		big |= b;
 		cs[e] = b ? 0 : -2 * v;
+		cf[e] = b ? 0.f : static_cast<float>(v);
+		mymax = max(mymax, b ? 8192 : abs(v));
 	}
+	atomicMax(&cmax, mymax);
 	const int cent_big = __syncthreads_or(big);
+	const uint64_t mc = static_cast<uint64_t>(cmax);
 	for(int c = threadIdx.x; c < k; c += blockDim.x) {
 		uint32_t s = 0;
 		for(int q = 0; q < 16; ++q) {
@@ -236,17 +250,23 @@ __global__ void __launch_bounds__(256, kMinBlocks) kmeans_assign_fast_kernel(con
 		uint32_t p[kKmPts][16];
 		uint32_t xx[kKmPts];
 		bool ok = !cent_big;
+		bool f32ok = !cent_big;
 #pragma unroll
 		for(int j = 0; j < kKmPts; ++j) {
 			const int64_t i = base + j;
 			xx[j] = 0;
+			uint32_t sx = 0;
 #pragma unroll
 			for(int q = 0; q < 16; ++q) {
 				const int32_t v = (i < n_local && q < d) ? points[i * pld + q] : 0;
 				p[j][q] = static_cast<uint32_t>(v);
 				ok &= (v < 8192 && v > -8192);
 				xx[j] += static_cast<uint32_t>(v) * static_cast<uint32_t>(v);
+				sx += static_cast<uint32_t>(abs(v < 8192 && v > -8192 ? v : 8192));
 			}
+			// f32 tier: every partial sum of x.c is an integer of magnitude <= sum|x_q| max|c|;
+			// below 2^24 each FFMA is exact
+			f32ok &= static_cast<uint64_t>(sx) * mc <= (uint64_t{1} << 24);
 		}
 		uint32_t best[kKmPts];
 		int bi[kKmPts];
@@ -255,7 +275,44 @@ __global__ void __launch_bounds__(256, kMinBlocks) kmeans_assign_fast_kernel(con
 			best[j] = 0xFFFFFFFFu;
 			bi[j] = 0;
 		}
-		if(ok) {
+		if(ok && f32ok) {
+			// x.c on the FP32 pipe (exact, see above), then the integer criterion |c|^2 - 2 x.c
+			// (|x|^2 is common to all centroids of a point): same first minimum as the exact
+			// squared distance
+			float pf[kKmPts][16];
+			int ib[kKmPts];
+#pragma unroll
+			for(int j = 0; j < kKmPts; ++j) {
+				ib[j] = INT_MAX;
+#pragma unroll
+				for(int q = 0; q < 16; ++q) pf[j][q] = static_cast<float>(static_cast<int32_t>(p[j][q]));
+			}
+			const float4* cf4 = reinterpret_cast<const float4*>(cf);
+#pragma unroll 1
+			for(int c = 0; c < k; ++c) {
+				float cv[16];
+#pragma unroll
+				for(int v4 = 0; v4 < 4; ++v4) {
+					const float4 t = cf4[c * 4 + v4];
+					cv[4 * v4] = t.x;
+					cv[4 * v4 + 1] = t.y;
+					cv[4 * v4 + 2] = t.z;
+					cv[4 * v4 + 3] = t.w;
+				}
+				const int cc = static_cast<int>(cn[c]);
+#pragma unroll
+				for(int j = 0; j < kKmPts; ++j) {
+					float m = 0.f;
+#pragma unroll
+					for(int q = 0; q < 16; ++q) m = fmaf(pf[j][q], cv[q], m);
+					const int crit = cc - 2 * __float2int_rn(m);
+					if(crit < ib[j]) {
+						ib[j] = crit;
+						bi[j] = c;
+					}
+				}
+			}
+		} else if(ok) {
 #pragma unroll 1
 			for(int c = 0; c < k; ++c) {
 				const int4* crow = cs4 + c * 4;
@@ -428,7 +485,7 @@ int launch_kmeans_assign_i32(const mt_launch_ctx* c, void* stream) {
 	const mt_view& va = c->views[3];
 	const mt_view& vp = c->views[4];
 	const mt_view& vc = c->views[5];
-	const size_t fast_smem = static_cast<size_t>(k) * 17 * sizeof(int32_t);
+	const size_t fast_smem = static_cast<size_t>(k) * 16 * 4 * 2 + static_cast<size_t>((k + 3) / 4) * 4 * 4;
 	const bool fast = d >= 1 && d <= 16 && fast_smem <= 200 * 1024 && vp.stride[1] == 1 && vc.stride[1] == 1 && va.stride[0] == 1 && vc.offset[0] == 0
 	                  && vc.offset[1] == 0 && vp.offset[1] == 0 && vc.extent[0] >= k;
 	if(fast) {
@@ -440,9 +497,9 @@ int launch_kmeans_assign_i32(const mt_launch_ctx* c, void* stream) {
 			kern<<<blocks, 256, fast_smem, s>>>(pts, vp.stride[0], r.total, static_cast<int>(k), static_cast<int>(d), static_cast<const int32_t*>(vc.base),
 			    vc.stride[0], asg);
 		};
-		// 6 points per thread, one 256-thread CTA per SM (measured over 2x3, 4x2, 4x3, 6x1, 8x1
-		// points x CTAs/SM: 6x1 and 8x1 fastest, 2 % ahead of 4x2; 4x3 spills)
-		run(kmeans_assign_fast_kernel<6, 1>, 6, 1);
+		// 4 points per thread, two 256-thread CTAs per SM (with the FP32 tier: 4x2 47.4 ms, 8x1
+		// 48.2, 6x1 50.4, 2x3 56.7 for 2e8 points; the IMAD-only kernel took 55.1)
+		run(kmeans_assign_fast_kernel<4, 2>, 4, 2);
 		return cudaGetLastError() == cudaSuccess ? 0 : 1;
 	}
 	const size_t smem = static_cast<size_t>(k * d) * sizeof(int32_t);

@@ -94,10 +94,12 @@ def _np_assign(p, c):
     return best
 
 
-@pytest.mark.parametrize("lim,d", [(8191, 16), (8191, 5), (1 << 20, 16)])
+@pytest.mark.parametrize("lim,d", [(8191, 16), (8191, 5), (1 << 20, 16), (255, 16), (1024, 16), (1025, 16), (4096, 1)])
 def test_kmeans_assign_signed_values(lim, d):
-    """negative coordinates, |x| at the fast path's limit (max distance just below 2^32), a
-    padded d < 16, and values past the limit (int64 path); ties included (duplicate centroids)"""
+    """negative coordinates, |x| at the u32 tier's limit (max distance just below 2^32), a
+    padded d < 16, and values past the limit (int64 path); the FP32 tier (sum|x| max|c| <= 2^24:
+    lim 255, exactly 2^24 at lim 1024 with d 16, and d 1) and just past its bound (lim 1025);
+    ties included (duplicate centroids)"""
     rng = np.random.default_rng(7)
     n, k = 20_011, 48
     p = rng.integers(-lim, lim + 1, size=(n, d), dtype=np.int64).astype(np.int32)
