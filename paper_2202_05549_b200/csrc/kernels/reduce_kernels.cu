@@ -302,9 +302,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) kmeans_assign_fast_kernel(con
 				const int cc = static_cast<int>(cn[c]);
 #pragma unroll
 				for(int j = 0; j < kKmPts; ++j) {
-					float m = 0.f;
+					float m0 = 0.f, m1 = 0.f; // two independent chains (both partial sums exact)
 #pragma unroll
-					for(int q = 0; q < 16; ++q) m = fmaf(pf[j][q], cv[q], m);
+					for(int q = 0; q < 16; q += 2) {
+						m0 = fmaf(pf[j][q], cv[q], m0);
+						m1 = fmaf(pf[j][q + 1], cv[q + 1], m1);
+					}
+					const float m = m0 + m1;
 					const int crit = cc - 2 * __float2int_rn(m);
 					if(crit < ib[j]) {
 						ib[j] = crit;

@@ -1,1 +1,1 @@
-for v in 0 1 2 3; do MTB_KM_VARIANT=$v python scripts/c4_perf.py --hist-n 1048576 --km-n 200000000 --steps 2 2>&1 | grep kmeans_assign | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($v, round(d['kernel_ms'],2))"; done
+python scripts/c4_perf.py --hist-n 1048576 --km-n 200000000 --steps 2 2>&1 | grep kmeans_assign | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['kernel_ms'],2))"
