@@ -158,3 +158,35 @@ def test_kmeans_c4_size_properties():
     assert np.array_equal(a[idx], dist.argmin(axis=1).astype(np.int32))  # argmin: first minimum, like the reference
     # the counts agree with the assignment vector
     assert np.array_equal(np.bincount(a, minlength=k), c)
+
+
+def test_heat2d_random_layouts(okern):
+    """random grids, chunkings (row and column splits, halos), block shapes and alphas: the
+    TMA-staged kernel, its scalar tail and the register kernel where the TMA one does not apply
+    must all agree with the oracle bit for bit"""
+    rng = np.random.default_rng(2024)
+    for case in range(30):
+        rows = int(rng.integers(1, 700))
+        cols = int(rng.integers(1, 1300))
+        ndev = int(rng.integers(1, 5))
+        er = int(rng.integers(1, rows + 1))
+        ec = cols if rng.random() < 0.6 else int(rng.integers(1, cols + 1))
+        halo = [1, 1 if ec < cols else int(rng.integers(0, 2))]
+        block = [int(rng.integers(1, 33)), int(rng.integers(1, 65))]
+        alpha = float(rng.choice([0.1, 0.25, 0.01]))
+        iters = int(rng.integers(1, 4))
+        x = rng.standard_normal((rows, cols)).astype(np.float32)
+        with mb.context(workers=1, devices=ndev, num_gpus=1) as ctx:
+            devs = ctx.devices
+            dist = lambda: ctx.dist.stencil([rows, cols], [er, ec], halo, devs)  # noqa: E731
+            a = ctx.create_array([rows, cols], "f32", dist(), 0)
+            b = ctx.create_array([rows, cols], "f32", dist(), 0)
+            ctx.write(a, x)
+            sb = [-(-er // block[0]) * block[0], -(-ec // block[1]) * block[1]]
+            work = ctx.dist.block_work([rows, cols], block, sb, devs)
+            for _ in range(iters):
+                ctx.launch("heat2d", [rows, cols], block, work, [rows, cols, alpha, Arr(b), Arr(a)], HEAT)
+                a, b = b, a
+            got = ctx.read(a)
+        want = oracle_heat(okern, x, iters, alpha)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (case, rows, cols, er, ec, halo, block)
