@@ -163,6 +163,16 @@ struct launch_result {
 	task_id past_last_task = 0;
 };
 
+// memory_config (memory.hpp:43-55): capacities of the device pool, the pinned-host spill tier and
+// the disk tier below it (0 = the runtime's default: 90% of free HBM / no host tier / no disk tier)
+struct memory_config {
+	uint64_t device_capacity = 0;
+	uint64_t host_capacity = 0;
+	uint64_t disk_capacity = 0;
+	uint64_t staging_threshold = 0; // informational on the GPU executor
+	std::string spill_dir;          // "" = the system temp directory
+};
+
 struct driver_config {
 	int workers = 1;
 	int devices_per_worker = 1;
@@ -170,6 +180,7 @@ struct driver_config {
 	bool compat_deps = false; // B200 extension: reference whole-chunk edges
 	bool execute = true;      // B200 extension: planner and executor in one context
 	int num_gpus = 0;
+	memory_config memory{};
 };
 
 // driver + executor in one context (the reference's harness pattern, test_runtime.cpp:12-43)
@@ -183,6 +194,12 @@ class driver {
 		c.compat_deps = cfg.compat_deps;
 		c.execute = cfg.execute;
 		c.num_gpus = cfg.num_gpus;
+		c.device_capacity = cfg.memory.device_capacity;
+		c.host_capacity = cfg.memory.host_capacity;
+		c.disk_capacity = cfg.memory.disk_capacity;
+		c.staging_threshold = cfg.memory.staging_threshold;
+		spill_dir_ = cfg.memory.spill_dir;
+		c.spill_dir = spill_dir_.empty() ? nullptr : spill_dir_.c_str();
 		check(mt_ctx_create(&c, &ctx_));
 	}
 	~driver() { mt_ctx_destroy(ctx_); }
@@ -225,11 +242,30 @@ class driver {
 		check(mt_array_read(ctx_, id, out.data(), count * sizeof(T)));
 		return out;
 	}
+	// B200 extensions: upload a whole array, and queue host transfers ordered against the
+	// launches by the dependency tracking (buffers must stay valid until synchronize())
+	template <typename T>
+	void write(array_id id, const std::vector<T>& data) {
+		check(mt_array_write(ctx_, id, data.data(), data.size() * sizeof(T)));
+	}
+	void write_async(array_id id, const void* host, uint64_t bytes) { check(mt_array_write_async(ctx_, id, host, bytes)); }
+	void read_async(array_id id, void* host, uint64_t bytes) { check(mt_array_read_async(ctx_, id, host, bytes)); }
+	// per-task device timestamps in report_json() (run_report::to_json, runtime.cpp:613-636)
+	void trace(bool on) { check(mt_exec_trace(mt_ctx_exec(ctx_), on ? 1 : 0)); }
+	std::string report_json() {
+		int64_t n = 0;
+		check(mt_exec_report_json(mt_ctx_exec(ctx_), nullptr, 0, &n));
+		std::string out(static_cast<size_t>(n) + 1, '\0');
+		check(mt_exec_report_json(mt_ctx_exec(ctx_), out.data(), n + 1, &n));
+		out.resize(static_cast<size_t>(n));
+		return out;
+	}
 
 	mt_ctx* handle() { return ctx_; }
 
   private:
 	mt_ctx* ctx_ = nullptr;
+	std::string spill_dir_;
 };
 
 // The executor alone: the drop-in for manta::system_runtime (consumes flat task records)

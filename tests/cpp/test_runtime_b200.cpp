@@ -37,7 +37,42 @@ static std::vector<float> run_stencil(int workers, int devices, int iterations, 
 	return drv.read<float>(in, static_cast<size_t>(n));
 }
 
+// the same stencil with device, pinned-host and disk tiers all in play (memory_config,
+// memory.hpp:43-55): spill traffic must reach the disk tier and the result stay bit-exact
+static std::vector<float> run_stencil_tiered(int iterations, int64_t n, std::string* report) {
+	driver_config cfg{1, 1, false, false, true, 1};
+	const uint64_t chunk = static_cast<uint64_t>(n / 8 + 2) * sizeof(float);
+	cfg.memory.device_capacity = 4 * chunk;
+	cfg.memory.host_capacity = 4 * chunk;
+	cfg.memory.disk_capacity = 64 * chunk;
+	driver drv(cfg);
+	const auto devs = drv.devices();
+	const rect dom({0}, {n});
+	auto in = drv.create_array(dom, dtype::f32, stencil_dist(dom, {n / 8}, {1}, devs), fill_spec::one());
+	auto out = drv.create_array(dom, dtype::f32, stencil_dist(dom, {n / 8}, {1}, devs), fill_spec::zero());
+	drv.flush();
+	const auto work = block_work_dist(dom, {16}, {n / 8}, devs);
+	for(int it = 0; it < iterations; ++it) {
+		drv.launch("stencil1d", dom, {16}, work, {launch_arg::scalar(n), launch_arg::array(out), launch_arg::array(in)},
+		    "global i => read input[i-1:i+1], write output[i]");
+		drv.flush();
+		std::swap(in, out);
+	}
+	drv.synchronize();
+	*report = drv.report_json();
+	return drv.read<float>(in, static_cast<size_t>(n));
+}
+
 int main() {
+	// device + host + disk tiers (B200 memory_config): bit-exact against the unconstrained run
+	{
+		std::string report;
+		const auto tiered = run_stencil_tiered(6, 1 << 20, &report);
+		const auto plain = run_stencil(1, 1, 6, 1 << 20);
+		CHECK(std::memcmp(tiered.data(), plain.data(), plain.size() * sizeof(float)) == 0);
+		CHECK(report.find("\"bytes_host_to_disk\": 0,") == std::string::npos);
+		CHECK(report.find("\"bytes_host_to_disk\"") != std::string::npos);
+	}
 	// distributed stencil equals the single-device serial run (test_runtime.cpp:67-72), bit-exact
 	{
 		const auto serial = run_stencil(1, 1, 4, 4096);
