@@ -127,3 +127,18 @@ def test_fuzz_campaign_passes():
     rc, out, err = run_cli("fuzz", "--cases", "40", "--seed", "1", timeout=1200)
     assert rc == 0, err[-3000:]
     assert out.strip() == "fuzz: 40 cases passed"
+
+
+@pytest.mark.gpu
+def test_run_with_all_memory_tiers(scenarios, tmp_path):
+    """`run` with the reference's memory flags small enough that chunks spill to pinned host
+    memory and on to the disk tier; still equal to the oracle-mode run"""
+    report = str(tmp_path / "report.json")
+    rc, out, err = run_cli("run", _write(tmp_path, "stencil", scenarios["stencil"]), "--oracle", "--report", report,
+                           "--device-capacity", str(3 * 256_008), "--host-capacity", str(4 * 256_008), "--disk-capacity", str(64 << 20))
+    assert rc == 0, out + err
+    assert "oracle: PASS" in out
+    with open(report) as f:
+        r = json.load(f)
+    assert sum(w["evictions"] for w in r["workers"]) > 0
+    assert sum(w["bytes_host_to_disk"] for w in r["workers"]) > 0
