@@ -140,11 +140,15 @@ __global__ void kmeans_update_i32_kernel(range r, int64_t k, int64_t d, dview po
 		if(acc[k * d + c]) atomicAdd(reinterpret_cast<unsigned long long*>(at1<int64_t>(counts, c)), acc[k * d + c]);
 }
 
-// Up to ~110K bins: two u16 counters per u32 shared word (65536 bins = 128 KB). A half that
-// wraps past 0xFFFF is detected from the atomic's old value and its 65536 moved to the global
-// partial (for the low half the carry that leaked into the high half is taken back). With
-// uniformly spread values the kernel is bound by shared-memory atomic throughput under random
-// bank conflicts, not by HBM.
+// Up to ~110K bins: two u16 counters per u32 shared word (65536 bins = 128 KB). The word only
+// ever receives additions, and every wrap is accounted from the old value its own atomic
+// returned, so no thread can misread a transient state: a low half that wraps adds 65536 to its
+// bin in the global partial and -1 to the high bin (its carry landed in the high half, and the
+// end-of-kernel flush will count it), and if that carry also wrapped the high half, 65536 to the
+// high bin; a high half that wraps adds 65536 to its bin. (Taking the carry back with a shared
+// atomicSub instead would leave a window in which a concurrent high-bin increment reads the
+// carried value and misses its own wrap.) With uniformly spread values the kernel is bound by
+// shared-memory atomic throughput under random bank conflicts, not by HBM.
 constexpr int kHistPairMaxBins = 110000;
 
 __global__ void __launch_bounds__(1024, 1) histogram_pair_kernel(const int32_t* x, int64_t n_local, int bins, unsigned long long* hist) {
@@ -154,9 +158,12 @@ __global__ void __launch_bounds__(1024, 1) histogram_pair_kernel(const int32_t* 
 	__syncthreads();
 	const auto fixup = [&](int32_t v, uint32_t old) {
 		const uint32_t sh = (v & 1) * 16;
-		if(((old >> sh) & 0xFFFFu) == 0xFFFFu) {
-			if(sh == 0) atomicSub(&w[v >> 1], 1u << 16);
+		if(((old >> sh) & 0xFFFFu) == 0xFFFFu) { // this add wrapped its half (rare)
 			atomicAdd(hist + v, 65536ull);
+			if(sh == 0 && v + 1 < bins) {
+				atomicAdd(hist + v + 1, ~0ull); // -1: the carry is counted by the flush of the high half
+				if((old >> 16) == 0xFFFFu) atomicAdd(hist + v + 1, 65536ull); // and it wrapped the high half
+			}
 		}
 	};
 	const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;

@@ -41,6 +41,32 @@ def test_histogram_u16_overflow():
     assert got[1] == n and got.sum() == n
 
 
+@pytest.mark.parametrize("pattern", ["pair", "lo_heavy", "hi_heavy", "odd_bins"])
+def test_histogram_u16_wraps_in_shared_words(pattern):
+    """two hot bins sharing one packed word (a low half whose carries land in a hot high half),
+    both wrapping many times in every CTA: exact counts"""
+    n = 1 << 26
+    i = np.arange(n, dtype=np.int64)
+    bins = 65536 if pattern != "odd_bins" else 65535
+    if pattern == "pair":
+        x = (2 + (i & 1)).astype(np.int32)                    # bins 2 and 3 alternate
+    elif pattern == "lo_heavy":
+        x = np.where(i % 5 == 0, 7, 6).astype(np.int32)       # bin 6 (low half) 4x as hot as bin 7
+    elif pattern == "hi_heavy":
+        x = np.where(i % 5 == 0, 6, 7).astype(np.int32)
+    else:
+        x = np.where(i % 3 == 0, 65533, 65534).astype(np.int32)  # last word's high half is no bin
+    want = np.bincount(x, minlength=bins).astype(np.int64)
+    with mb.context(workers=1, devices=1, num_gpus=1) as ctx:
+        d = ctx.devices
+        xa = ctx.create_array([n], "i32", ctx.dist.single([n], d[0]), 0)
+        h = ctx.create_array([bins], "i64", ctx.dist.single([bins], d[0]), 0)
+        ctx.write(xa, x)
+        ctx.launch("histogram", [n], [256], ctx.dist.block_work([n], [256], [n], d), [n, bins, Arr(xa), Arr(h)], "global i => read x[i], reduce(+) hist[:]")
+        got = ctx.read(h)
+    assert np.array_equal(got, want)
+
+
 @pytest.mark.parametrize("mod", [1000, 20000])
 def test_kmeans_fast_and_exact_paths(okern, mod):
     """mod 1000: all coordinates < 8192 (u32 fast path); mod 20000: int64 path."""
