@@ -150,6 +150,7 @@ __global__ void kmeans_update_i32_kernel(range r, int64_t k, int64_t d, dview po
 // carried value and misses its own wrap.) With uniformly spread values the kernel is bound by
 // shared-memory atomic throughput under random bank conflicts, not by HBM.
 constexpr int kHistPairMaxBins = 110000;
+constexpr int kHistQuadMaxBins = 220000; // u8 counters: 55000 words = 220 KB of shared memory
 
 __global__ void __launch_bounds__(1024, 1) histogram_pair_kernel(const int32_t* x, int64_t n_local, int bins, unsigned long long* hist) {
 	extern __shared__ uint32_t w[];
@@ -203,6 +204,67 @@ __global__ void __launch_bounds__(1024, 1) histogram_pair_kernel(const int32_t* 
 		const uint32_t v = w[b];
 		if(v & 0xFFFFu) atomicAdd(hist + 2 * b, static_cast<unsigned long long>(v & 0xFFFFu));
 		if((v >> 16) && 2 * b + 1 < bins) atomicAdd(hist + 2 * b + 1, static_cast<unsigned long long>(v >> 16));
+	}
+}
+
+// Four u8 counters per u32 shared word (65536 bins = 64 KB), so two 1024-thread CTAs share an
+// SM. As with the u16 kernel the word only receives additions and every wrap is booked from the
+// old value the thread's own atomic returned: adding 1 to byte b of `old` changes bytes b..3 by
+// the carry chain, and each bin k in that chain gets (its true increment) - (its stored change)
+// added to the global partial, which is 0 except when a byte wraps.
+__global__ void __launch_bounds__(1024, 2) histogram_quad_kernel(const int32_t* x, int64_t n_local, int bins, unsigned long long* hist) {
+	extern __shared__ uint32_t w[];
+	const int words = (bins + 3) / 4;
+	for(int b = threadIdx.x; b < words; b += blockDim.x) w[b] = 0;
+	__syncthreads();
+	const auto add = [&](int32_t v) {
+		if(static_cast<uint32_t>(v) >= static_cast<uint32_t>(bins)) return;
+		const uint32_t sh = (v & 3) * 8;
+		const uint32_t old = atomicAdd(&w[v >> 2], 1u << sh);
+		if(((old >> sh) & 0xFFu) == 0xFFu) { // this add wrapped its byte (rare): book the carry chain
+			const uint32_t nw = old + (1u << sh);
+			for(int kb = v & 3; kb < 4; ++kb) {
+				const int bin = (v & ~3) + kb;
+				const int delta = static_cast<int>((nw >> (8 * kb)) & 0xFFu) - static_cast<int>((old >> (8 * kb)) & 0xFFu);
+				const long long fix = (kb == (v & 3) ? 1 : 0) - delta;
+				if(fix != 0 && bin < bins) atomicAdd(hist + bin, static_cast<unsigned long long>(fix));
+				if(delta != -255) break; // the carry stops at the first byte that did not wrap
+			}
+		}
+	};
+	const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+	const int64_t nvec = n_local / 4;
+	const int4* xv = reinterpret_cast<const int4*>(x);
+	constexpr int U = 4;
+	int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+	for(; t + (U - 1) * stride < nvec; t += U * stride) {
+		int4 q[U];
+#pragma unroll
+		for(int u = 0; u < U; ++u) q[u] = __ldcs(xv + t + u * stride);
+#pragma unroll
+		for(int u = 0; u < U; ++u) {
+			add(q[u].x);
+			add(q[u].y);
+			add(q[u].z);
+			add(q[u].w);
+		}
+	}
+	for(; t < nvec; t += stride) {
+		const int4 q = __ldcs(xv + t);
+		add(q.x);
+		add(q.y);
+		add(q.z);
+		add(q.w);
+	}
+	for(int64_t e = nvec * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_local; e += stride) add(x[e]);
+	__syncthreads();
+	for(int b = threadIdx.x; b < words; b += blockDim.x) {
+		const uint32_t v = w[b];
+#pragma unroll
+		for(int kb = 0; kb < 4; ++kb) {
+			const uint32_t c = (v >> (8 * kb)) & 0xFFu;
+			if(c && 4 * b + kb < bins) atomicAdd(hist + 4 * b + kb, static_cast<unsigned long long>(c));
+		}
 	}
 }
 
@@ -474,6 +536,15 @@ int launch_histogram(const mt_launch_ctx* c, void* stream) {
 		int64_t blocks = (n_local / 4 + 511) / 512;
 		blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 4));
 		histogram_smem_kernel<<<static_cast<unsigned>(blocks), 512, smem, s>>>(x, lo, n_local, bins, hist);
+	} else if(bins <= kHistQuadMaxBins && reinterpret_cast<uintptr_t>(x) % 16 == 0 && !(std::getenv("MTB_HIST_QUAD") && std::atoi(std::getenv("MTB_HIST_QUAD")) == 0)) {
+		// u8 counters: two CTAs per SM up to 110K bins (65536 bins: 2.67 vs 2.85 ms for the u16
+		// single-CTA kernel), one CTA per SM up to 220K bins
+		const size_t smem = static_cast<size_t>((bins + 3) / 4) * sizeof(uint32_t);
+		ensure_smem(histogram_quad_kernel, static_cast<int>(((kHistQuadMaxBins + 3) / 4) * 4));
+		const int per_sm = bins <= kHistPairMaxBins ? 2 : 1;
+		int64_t blocks = (n_local / 4 + 1023) / 1024;
+		blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, per_sm * 148));
+		histogram_quad_kernel<<<static_cast<unsigned>(blocks), 1024, smem, s>>>(x, n_local, static_cast<int>(bins), hist);
 	} else if(bins <= kHistPairMaxBins && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
 		const size_t smem = static_cast<size_t>((bins + 1) / 2) * sizeof(uint32_t);
 		ensure_smem(histogram_pair_kernel, static_cast<int>(((kHistPairMaxBins + 1) / 2) * 4));

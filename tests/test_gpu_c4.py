@@ -13,7 +13,7 @@ I32 = C.POINTER(C.c_int32)
 I64 = C.POINTER(C.c_int64)
 
 
-@pytest.mark.parametrize("bins", [7, 256, 16384, 65536, 100000, 300000])
+@pytest.mark.parametrize("bins", [7, 256, 16384, 16385, 65536, 100000, 110001, 220000, 300000])
 def test_histogram_paths(okern, bins):
     n = 3_000_017
     with mb.context(workers=1, devices=2, num_gpus=1) as ctx:
