@@ -729,6 +729,10 @@ def run_b200(args):
                "sequential": {"value": seq, "steps": len(times), "worst_step_s": dt,
                               "note": "each step synchronous: upload, iterations, download"}}
         del host_in, host_out
+        try:  # hand the pinned host buffers back (torch caches freed pinned blocks) before the C5 leg pins its own
+            torch._C._host_emptyCache()
+        except Exception:  # noqa: BLE001
+            pass
 
     cpu = None
     if rank == 0 and args.cpu_baseline:
