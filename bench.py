@@ -515,6 +515,11 @@ def run_ooc(rows, cols, chunk_rows, capacity_gib, host_gib, iters, warmup, looka
             "lookahead_tasks": la, "warmup_s": t_setup, "evictions": s1["evictions"] - s0["evictions"]}
 
 
+# launches per mt_flush in the C1 leg: a 10-launch submission is replayed as one CUDA graph whose
+# edges run across iterations (profiles/round1/c1_flush_sweep.md)
+C1_PER_FLUSH = 10
+
+
 def run_c1(iters, ref_iters, hbm, cpu):
     """BASELINE configs[0] (the reference's CPU scenario): heat2d 4096^2 f32, row-block stencil
     distribution into 4 chunks, one distributed launch per iteration, on one GPU (4 logical
@@ -527,12 +532,14 @@ def run_c1(iters, ref_iters, hbm, cpu):
 
         def run(n):
             nonlocal a, b
-            for _ in range(n):
+            for i in range(n):
                 ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN)
-                ctx.flush()
+                if (i + 1) % C1_PER_FLUSH == 0:
+                    ctx.flush()
                 a, b = b, a
+            ctx.flush()
 
-        run(10)
+        run(3 * C1_PER_FLUSH)
         ctx.synchronize()
         ctx.mark(0)
         run(iters)
@@ -541,7 +548,8 @@ def run_c1(iters, ref_iters, hbm, cpu):
         ctx.synchronize()
         st = ctx.exec_stats()
     gbs = BYTES_PER_CELL * rows * cols / (ms / 1e3) / 1e9
-    out = {"workload": f"heat2d {rows}x{cols} f32, 4 chunks (stencil_dist halo [1,0]), {iters} iterations, one launch per iteration",
+    out = {"workload": f"heat2d {rows}x{cols} f32, 4 chunks (stencil_dist halo [1,0]), {iters} iterations, one launch per iteration, "
+                       f"handed to the executor every {C1_PER_FLUSH} launches",
            "value": rows * cols / (ms / 1e3), "unit": "cell-updates/s", "ms_per_iter": ms,
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                         "note": "step time incl. planning, halo copies and graph launch; small grid: issue-bound"},

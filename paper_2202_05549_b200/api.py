@@ -249,6 +249,7 @@ class Context:
         self._arrays: dict[int, tuple] = {}
         self._inflight: list = []  # host buffers of queued async transfers
         self._work_cache: dict = {}
+        self._call_cache: dict = {}
 
     def close(self):
         if self.h:
@@ -295,6 +296,27 @@ class Context:
         return _chunks_out(self.lib, self.lib.array_chunks, self.h, array_id)
 
     def launch(self, kernel: str, grid, block, work: Sequence[Superblock], args: Iterable, annotation: str):
+        args = list(args)
+        # iterative launches repeat one call: its ctypes structures are converted once (the type
+        # is part of the key so that 1, 1.0 and True stay distinct arguments)
+        try:
+            ckey = (kernel, tuple(grid) if not isinstance(grid, capi.Rect) else None, tuple(block), tuple(work),
+                    tuple((type(a), a) for a in args), annotation)
+            hit = self._call_cache.get(ckey) if ckey[1] is not None else None
+        except TypeError:  # unhashable argument: convert without caching
+            ckey, hit = None, None
+        if hit is None:
+            hit = self._convert_launch(kernel, grid, block, work, args, annotation)
+            if ckey is not None and ckey[1] is not None:
+                if len(self._call_cache) > 64:
+                    self._call_cache.clear()
+                self._call_cache[ckey] = hit
+        kb, g, b, w, nw, la, na, ab = hit
+        first, last = C.c_int64(0), C.c_int64(0)
+        self.lib.check(self.lib.launch(self.h, kb, C.byref(g), b, w, nw, la, na, ab, C.byref(first), C.byref(last)))
+        return first.value, last.value
+
+    def _convert_launch(self, kernel, grid, block, work, args, annotation):
         g = _domain(grid)
         b = (C.c_int64 * 3)(*block)
         key = tuple(work)  # iterative launches reuse one decomposition: convert it once
@@ -307,7 +329,6 @@ class Context:
             if len(self._work_cache) > 64:
                 self._work_cache.clear()
             self._work_cache[key] = w
-        args = list(args)
         la = (capi.LaunchArg * max(1, len(args)))()
         for i, a in enumerate(args):
             if isinstance(a, Arr):
@@ -318,10 +339,7 @@ class Context:
                 la[i].kind, la[i].f = capi.LARG_FLOAT, float(a)
             else:
                 raise ValidationError(f"unsupported launch argument {a!r}")
-        first, last = C.c_int64(0), C.c_int64(0)
-        self.lib.check(self.lib.launch(self.h, kernel.encode(), C.byref(g), b, w, len(work), la, len(args), annotation.encode(),
-                                       C.byref(first), C.byref(last)))
-        return first.value, last.value
+        return kernel.encode(), g, b, w, len(work), la, len(args), annotation.encode()
 
     def flush(self):
         self.lib.check(self.lib.flush(self.h))

@@ -566,7 +566,7 @@ bool executor::graph_eligible(const std::vector<task>& b, int* gpu) const {
 	// between submissions that the multi-stream path keeps for large superblocks.
 	static const double max_threads = [] {
 		const char* e = std::getenv("MTB_GRAPH_MAX_THREADS");
-		return e ? std::atof(e) : 33554432.0;
+		return e ? std::atof(e) : 268435456.0; // 2^28: e.g. ten 4096^2 launches in one flush
 	}();
 	double threads = 0;
 	for(const auto& t : b)
