@@ -131,3 +131,37 @@ def test_fuzz_scenarios_with_repeats_match_the_reference(ref):
         assert coherent and S.compare(got, want, 1e-6) == [], seed
         checked += 1
     assert checked >= 30 and replays > 0
+
+
+@pytest.mark.parametrize("per_flush", [4, 10])
+def test_multi_launch_submissions_replay_bit_exact(okern, per_flush):
+    """several launches handed to the executor in one flush (the bench's C1 pattern): the batch
+    is one graph whose edges run across iterations; a trailing partial batch and a batch with a
+    second kernel (scale by a different alpha) are replayed or issued eagerly. Bit-exact against
+    the oracle either way"""
+    rows, cols, iters = 384, 640, 47
+    x = np.random.default_rng(per_flush).standard_normal((rows, cols)).astype(np.float32)
+    alphas = [0.1 if i % 9 else 0.25 for i in range(iters)]
+    with mb.context(workers=1, devices=4, num_gpus=1) as ctx:
+        devs = ctx.devices
+        d = lambda: ctx.dist.stencil([rows, cols], [rows // 4, cols], [1, 0], devs)  # noqa: E731
+        a = ctx.create_array([rows, cols], "f32", d(), 0)
+        b = ctx.create_array([rows, cols], "f32", d(), 0)
+        ctx.write(a, x)
+        w = ctx.dist.block_work([rows, cols], [16, 16], [rows // 4, cols], devs)
+        for rep in range(3):  # the same sequence three times: batches repeat and get replayed
+            for i, al in enumerate(alphas):
+                ctx.launch("heat2d", [rows, cols], [16, 16], w, [rows, cols, al, Arr(b), Arr(a)], HEAT)
+                if (i + 1) % per_flush == 0:
+                    ctx.flush()
+                a, b = b, a
+            ctx.flush()
+        got = ctx.read(a)
+        st = ctx.exec_stats()
+    assert st["graph_replays"] > 0
+    cur, nxt = x.copy(), np.empty_like(x)
+    for _ in range(3):
+        for al in alphas:
+            okern.oracle_heat2d(C.c_int64(rows), C.c_int64(cols), C.c_double(al), cur.ctypes.data_as(F32), nxt.ctypes.data_as(F32))
+            cur, nxt = nxt, cur
+    assert np.array_equal(got.view(np.uint32), cur.view(np.uint32))
