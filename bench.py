@@ -208,27 +208,38 @@ def bf16_ramp_row(i, n, mod):
     return u.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
-def run_contraction(ctx, n, steps, warmup):
-    """BASELINE config C3 on one GPU: C (f32) = A (bf16) x Bt^T (bf16), n^3, through the planner
-    (one superblock per GPU) and the tcgen05 kernel; TFLOP/s from device events."""
+def f32_ramp_row(i, n, mod):
+    """host restatement of ramp2d_f32 for row i"""
+    import numpy as np
+    j = np.arange(n, dtype=np.int64)
+    return (((i * 31 + j * 17 + 7) % mod).astype(np.float64) / mod).astype(np.float32).astype(np.float64)
+
+
+def run_contraction(ctx, n, steps, warmup, kind="bf16"):
+    """BASELINE config C3 on one GPU: C (f32) = A x Bt^T, n^3, through the planner (one
+    superblock per GPU) and the tcgen05 kernel; TFLOP/s from device events. kind "bf16": bf16
+    operands (kind::f16); "tf32": f32 operands multiplied as TF32 (kind::tf32), C3's fp32 form."""
     from paper_2202_05549_b200 import Arr
     dev = ctx.devices
-    A = ctx.create_array([n, n], "bf16", ctx.dist.single([n, n], dev[0]), 0)
-    B = ctx.create_array([n, n], "bf16", ctx.dist.single([n, n], dev[0]), 0)
+    kernel = f"matmul_nt_{kind}"
+    et = "bf16" if kind == "bf16" else "f32"
+    A = ctx.create_array([n, n], et, ctx.dist.single([n, n], dev[0]), 0)
+    B = ctx.create_array([n, n], et, ctx.dist.single([n, n], dev[0]), 0)
     Cm = ctx.create_array([n, n], "f32", ctx.dist.single([n, n], dev[0]), 0)
     w = ctx.dist.block_work([n, n], [16, 16], [n, n], dev)
-    ctx.launch("ramp2d_bf16", [n, n], [16, 16], w, [n, n, 1000, 0.0, 1.0, Arr(A)], "global [i, j] => write out[i,j]")
-    ctx.launch("ramp2d_bf16", [n, n], [16, 16], w, [n, n, 997, 0.0, 1.0, Arr(B)], "global [i, j] => write out[i,j]")
+    ctx.launch(f"ramp2d_{et}", [n, n], [16, 16], w, [n, n, 1000, 0.0, 1.0, Arr(A)], "global [i, j] => write out[i,j]")
+    ctx.launch(f"ramp2d_{et}", [n, n], [16, 16], w, [n, n, 997, 0.0, 1.0, Arr(B)], "global [i, j] => write out[i,j]")
     ann = "global [i, j] => write C[i,j], read A[i,:], read Bt[j,:]"
+    host_row = bf16_ramp_row if kind == "bf16" else f32_ramp_row
 
     def step():
-        ctx.launch("matmul_nt_bf16", [n, n], [16, 16], w, [n, n, n, Arr(Cm), Arr(A), Arr(B)], ann)
+        ctx.launch(kernel, [n, n], [16, 16], w, [n, n, n, Arr(Cm), Arr(A), Arr(B)], ann)
         ctx.flush()
 
     for _ in range(warmup):
         step()
     ctx.synchronize()
-    k0, ms0 = ctx.kernel_time("matmul_nt_bf16")
+    k0, ms0 = ctx.kernel_time(kernel)
     ctx.profile_kernels(True)
     ctx.mark(0)
     for _ in range(steps):
@@ -237,15 +248,15 @@ def run_contraction(ctx, n, steps, warmup):
     elapsed = ctx.elapsed_ms()
     ctx.synchronize()
     ctx.profile_kernels(False)
-    k1, ms1 = ctx.kernel_time("matmul_nt_bf16")
-    # spot check 16 elements against an fp64 host dot product of the same bf16 inputs
+    k1, ms1 = ctx.kernel_time(kernel)
+    # spot check 16 elements against an fp64 host dot product of the same inputs
     import numpy as np
     c = ctx.read(Cm)
     rng = np.random.default_rng(0)
     worst = 0.0
     for _ in range(16):
         i, j = int(rng.integers(n)), int(rng.integers(n))
-        want = float(bf16_ramp_row(i, n, 1000) @ bf16_ramp_row(j, n, 997))
+        want = float(host_row(i, n, 1000) @ host_row(j, n, 997))
         worst = max(worst, abs(float(c[i, j]) - want) / max(abs(want), 1e-30))
     del c
     for a in (A, B, Cm):
@@ -253,7 +264,7 @@ def run_contraction(ctx, n, steps, warmup):
     ctx.synchronize()
     flop = 2.0 * n ** 3
     kern_ms = (ms1 - ms0) / max(1, k1 - k0)
-    return {"workload": f"matmul_nt_bf16 {n}^3 (C f32 = A bf16 x Bt^T bf16), 1 superblock", "value": flop * steps / (elapsed / 1e3) / 1e12,
+    return {"workload": f"{kernel} {n}^3 (C f32 = A {kind} x Bt^T {kind}), 1 superblock", "value": flop * steps / (elapsed / 1e3) / 1e12,
             "unit": "TFLOP/s", "steps": steps, "ms_per_step": elapsed / steps, "kernel_ms": kern_ms,
             "max_rel_err_16_samples_vs_fp64": worst}
 
@@ -775,6 +786,15 @@ def run_b200(args):
         contraction["roofline"] = {"bound": "tensor", "achieved": kach, "peak": tburst, "unit": "TFLOP/s", "frac": kach / tburst,
                                    "peak_kind": "measured burst (cuBLAS bf16 8192^3, best of 10)", "frac_of_sustained": kach / tpeak,
                                    "kernel": "gemm_bf16_nt_kernel (tcgen05.mma cta_group::1 M128 N256, TMA, TMEM)"}
+        if args.tf32_steps > 0:
+            t32 = run_contraction(ctx, args.matmul_n, args.tf32_steps, 1, "tf32")
+            k32 = 2.0 * args.matmul_n ** 3 / (t32["kernel_ms"] / 1e3) / 1e12
+            # no measured TF32 peak on this pool: dense TF32 is half the bf16 rate (datasheet), so
+            # half the measured bf16 burst figure
+            t32["roofline"] = {"bound": "tensor", "achieved": k32, "peak": tburst / 2, "unit": "TFLOP/s", "frac": k32 / (tburst / 2),
+                               "peak_kind": "half the measured bf16 burst (TF32 = 1/2 bf16 dense rate)",
+                               "kernel": "gemm_bf16_nt_kernel<TF32> (tcgen05.mma kind::tf32 cta_group::1 M128 N256, TMA, TMEM)"}
+            contraction["tf32"] = t32
     c1 = None
     if ws == 1 and args.c1:
         c1 = run_c1(100, args.c1_ref_iters, peaks()[0], rank == 0 and args.cpu_baseline)
@@ -847,6 +867,7 @@ def main():
     p.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     p.add_argument("--matmul-n", type=int, default=32768, help="C3 contraction size (0 to skip)")
     p.add_argument("--matmul-steps", type=int, default=5)
+    p.add_argument("--tf32-steps", type=int, default=3, help="steps of the C3 fp32 (TF32) contraction leg (0 to skip)")
     p.add_argument("--no-c4", dest="c4", action="store_false", help="skip the histogram / k-means legs")
     p.add_argument("--hist-n", type=int, default=4_000_000_000)
     p.add_argument("--strip", type=int, default=128, help="N>1: rows of the halo-facing superblocks per GPU")

@@ -381,6 +381,16 @@ int mt_wrapper_source(const char* id, const mt_param_spec* params, int32_t npara
  * `cap` bytes including the NUL; *len receives the text length. */
 int mt_fuzz_scenario_json(uint64_t seed, char* buf, int64_t cap, int64_t* len);
 
+/* ---- direct contraction entry points (the kernels behind matmul_nt_bf16 / _tf32) ------- */
+/* C (f32, m x n, row pitch ldc) = A (m x k) x Bt^T (Bt: n x k), all row-major DEVICE pointers,
+ * enqueued on `stream` (a cudaStream_t, NULL = legacy default). bf16: A and Bt are bf16 bit
+ * patterns (kind::f16); tf32: f32 operands read as TF32 (kind::tf32). Row pitches in elements
+ * must make 16-byte multiples. Returns 0, or 5 (k <= 0), 6 (misaligned operands), 7 (tensor
+ * map encode failed), 1 (launch error). The reference's `matmul` (kernels.cpp:167-193) is the
+ * scalar form; these are the C3 tensor-core forms. */
+int mt_gemm_bf16_nt(const void* a, const void* bt, float* c, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, void* stream);
+int mt_gemm_tf32_nt(const float* a, const float* bt, float* c, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

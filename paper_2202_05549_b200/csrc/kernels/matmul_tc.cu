@@ -156,6 +156,15 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
 	    "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// kind::tf32: f32 operands read as TF32 (the low 13 mantissa bits are not used), K = 8 per MMA
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+	asm volatile(
+	    "{\n\t.reg .pred p;\n\t"
+	    "setp.ne.b32 p, %4, 0;\n\t"
+	    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+	    "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 // K-major operand, 128-byte swizzle: 8-row atoms of 1024 B (SBO), version 1, layout type 2
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
 	uint64_t d = 0;
@@ -170,6 +179,11 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
 // kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major, M x N = `m` x 256
 __host__ __device__ constexpr uint32_t instr_desc(int m = BM) {
 	return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+// kind::tf32 instruction descriptor: tf32 x tf32 -> f32 (formats 2), both K-major, 128 x 256
+__host__ __device__ constexpr uint32_t instr_desc_tf32() {
+	return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -205,8 +219,12 @@ __device__ __forceinline__ void tile_coords(int t, const gemm_args& p, int& mb, 
 	nb = r / rows;
 }
 
+// TF32: f32 operands (kind::tf32). A stage is still one 128-byte swizzle row per operand row,
+// i.e. 32 f32 instead of 64 bf16 of K, and each of its 4 MMAs covers 32 bytes of K (8 f32).
+template <bool TF32>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_nt_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, gemm_args p) {
+	constexpr int BKE = TF32 ? BK / 2 : BK; // K elements per stage
 	extern __shared__ uint8_t smem_raw[];
 	uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
 	uint8_t* a_smem = smem;
@@ -257,8 +275,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 				for(int kb = 0; kb < p.k_blocks; ++kb) {
 					mbar_wait(&empty[stage], phase ^ 1);
 					mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-					tma_load_2d(a_smem + stage * A_STAGE_BYTES, &tmap_a, &full[stage], kb * BK, arow);
-					tma_load_2d(b_smem + stage * B_STAGE_BYTES, &tmap_b, &full[stage], kb * BK, brow);
+					tma_load_2d(a_smem + stage * A_STAGE_BYTES, &tmap_a, &full[stage], kb * BKE, arow);
+					tma_load_2d(b_smem + stage * B_STAGE_BYTES, &tmap_b, &full[stage], kb * BKE, brow);
 					if(++stage == STAGES) {
 						stage = 0;
 						phase ^= 1;
@@ -269,7 +287,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	} else if(warp == 1) {
 		if(lane == 0) {
 			// ---- MMA issuer ----
-			constexpr uint32_t idesc = instr_desc();
+			constexpr uint32_t idesc = TF32 ? instr_desc_tf32() : instr_desc();
 			int stage = 0;
 			uint32_t phase = 0;
 			int local = 0;
@@ -284,8 +302,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 					const uint32_t a0 = smem_u32(a_smem + stage * A_STAGE_BYTES);
 					const uint32_t b0 = smem_u32(b_smem + stage * B_STAGE_BYTES);
 #pragma unroll
-					for(int k = 0; k < BK / UMMA_K; ++k)
-						tc_mma(d, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+					for(int k = 0; k < BK / UMMA_K; ++k) {
+						if constexpr(TF32)
+							tc_mma_tf32(d, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+						else
+							tc_mma(d, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+					}
 					tc_commit(&empty[stage]);
 					if(++stage == STAGES) {
 						stage = 0;
@@ -507,15 +529,16 @@ encode_fn get_encode() {
 	return fn;
 }
 
-// 2D bf16 K-major operand: `rows` x `cols` (cols contiguous), row pitch `ld` elements
-bool make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_rows) {
+// 2D K-major operand (bf16, or f32 for TF32): `rows` x `cols` (cols contiguous), row pitch `ld`
+// elements; boxes of one 128-byte row of K
+bool make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_rows, bool f32 = false) {
 	encode_fn enc = get_encode();
 	if(!enc) return false;
 	const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-	const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-	const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), box_rows};
+	const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * (f32 ? 4 : 2)};
+	const cuuint32_t box[2] = {static_cast<cuuint32_t>(f32 ? BK / 2 : BK), box_rows};
 	const cuuint32_t estride[2] = {1, 1};
-	return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+	return enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
 	           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
 	       == CUDA_SUCCESS;
 }
@@ -529,10 +552,11 @@ int num_sms() {
 
 // a: rows [a_row0, a_row0 + m) of an (a_rows x k) matrix; bt likewise for n.
 int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const void* bt, int64_t b_rows, int64_t ldb, int64_t b_row0, float* c,
-    int64_t ldc, int64_t m, int64_t n, int64_t k, cudaStream_t s) {
+    int64_t ldc, int64_t m, int64_t n, int64_t k, cudaStream_t s, bool tf32 = false) {
 	if(m <= 0 || n <= 0) return 0;
 	if(k <= 0) return 5;
-	if((lda * 2) % 16 || (ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(a) % 16) || (reinterpret_cast<uintptr_t>(bt) % 16)) return 6;
+	const int64_t es = tf32 ? 4 : 2;
+	if((lda * es) % 16 || (ldb * es) % 16 || (reinterpret_cast<uintptr_t>(a) % 16) || (reinterpret_cast<uintptr_t>(bt) % 16)) return 6;
 	gemm_args p{};
 	p.c = c;
 	p.ldc = ldc;
@@ -543,7 +567,8 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	p.b_row0 = b_row0;
 	p.m_blocks = static_cast<int>((m + BM - 1) / BM);
 	p.n_blocks = static_cast<int>((n + BN - 1) / BN);
-	p.k_blocks = static_cast<int>((k + BK - 1) / BK);
+	const int64_t bke = tf32 ? BK / 2 : BK;
+	p.k_blocks = static_cast<int>((k + bke - 1) / bke);
 	const int sms = num_sms();
 	p.group_m = GROUP_M;
 	if(const char* e = std::getenv("MTB_GEMM_GROUP")) p.group_m = std::max(1, std::atoi(e));
@@ -559,13 +584,18 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	p.no_store = std::getenv("MTB_GEMM_NOSTORE") != nullptr;
 	p.n_major = std::getenv("MTB_GEMM_NMAJOR") != nullptr;
 	const bool force_pair = std::getenv("MTB_GEMM_FORCE_PAIR") != nullptr;
-	const bool pair = p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && (!big || force_pair) && std::getenv("MTB_GEMM_NO_PAIR") == nullptr;
+	const bool pair = !tf32 && p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && (!big || force_pair) && std::getenv("MTB_GEMM_NO_PAIR") == nullptr;
 	CUtensorMap ma, mb;
-	if(!make_map(&ma, a, a_rows, k, lda, BM) || !make_map(&mb, bt, b_rows, k, ldb, pair ? BN / 2 : BN)) return 7;
+	if(!make_map(&ma, a, a_rows, k, lda, BM, tf32) || !make_map(&mb, bt, b_rows, k, ldb, pair ? BN / 2 : BN, tf32)) return 7;
 	if(!pair) {
-		kern::ensure_smem(gemm_bf16_nt_kernel, static_cast<int>(SMEM_BYTES));
 		const int grid = std::min(p.m_blocks * p.n_blocks, sms);
-		gemm_bf16_nt_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+		if(tf32) {
+			kern::ensure_smem(gemm_bf16_nt_kernel<true>, static_cast<int>(SMEM_BYTES));
+			gemm_bf16_nt_kernel<true><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+		} else {
+			kern::ensure_smem(gemm_bf16_nt_kernel<false>, static_cast<int>(SMEM_BYTES));
+			gemm_bf16_nt_kernel<false><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+		}
 		return cudaGetLastError() == cudaSuccess ? 0 : 1;
 	}
 	kern::ensure_smem(gemm_bf16_nt_2sm_kernel, static_cast<int>(SMEM2_BYTES));
@@ -598,7 +628,7 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 
 } // namespace tc
 
-int launch_matmul_nt_bf16(const mt_launch_ctx* c, void* stream) {
+static int launch_matmul_nt(const mt_launch_ctx* c, void* stream, bool tf32) {
 	const int64_t m = c->scalars_int[0], n = c->scalars_int[1], k = c->scalars_int[2];
 	const int64_t r0 = c->threads_lo[0], r1 = std::min(c->threads_hi[0], m);
 	const int64_t c0 = c->threads_lo[1], c1 = std::min(c->threads_hi[1], n);
@@ -610,14 +640,22 @@ int launch_matmul_nt_bf16(const mt_launch_ctx* c, void* stream) {
 	if(va.offset[1] != 0 || vb.offset[1] != 0 || va.extent[1] < k || vb.extent[1] < k) return 3; // whole K rows staged
 	float* cp = static_cast<float*>(vc.base) + (r0 - vc.offset[0]) * vc.stride[0] + (c0 - vc.offset[1]) * vc.stride[1];
 	return tc::run_gemm(va.base, va.extent[0], va.stride[0], r0 - va.offset[0], vb.base, vb.extent[0], vb.stride[0], c0 - vb.offset[0], cp, vc.stride[0],
-	    r1 - r0, c1 - c0, k, static_cast<cudaStream_t>(stream));
+	    r1 - r0, c1 - c0, k, static_cast<cudaStream_t>(stream), tf32);
 }
+
+int launch_matmul_nt_bf16(const mt_launch_ctx* c, void* stream) { return launch_matmul_nt(c, stream, false); }
+int launch_matmul_nt_tf32(const mt_launch_ctx* c, void* stream) { return launch_matmul_nt(c, stream, true); }
 
 void register_matmul_kernels(kernel_table& t) {
 	t.add({"matmul_nt_bf16",
 	    {param_sig{"m", false, dtype::i64, 0, false}, param_sig{"n", false, dtype::i64, 0, false}, param_sig{"k", false, dtype::i64, 0, false},
 	        param_sig{"C", true, dtype::f32, 2, true}, param_sig{"A", true, dtype::bf16, 2, false}, param_sig{"Bt", true, dtype::bf16, 2, false}},
 	    launch_matmul_nt_bf16});
+	// the fp32 form of C3 on the tensor cores: f32 operands multiplied as TF32, f32 accumulation
+	t.add({"matmul_nt_tf32",
+	    {param_sig{"m", false, dtype::i64, 0, false}, param_sig{"n", false, dtype::i64, 0, false}, param_sig{"k", false, dtype::i64, 0, false},
+	        param_sig{"C", true, dtype::f32, 2, true}, param_sig{"A", true, dtype::f32, 2, false}, param_sig{"Bt", true, dtype::f32, 2, false}},
+	    launch_matmul_nt_tf32});
 }
 
 } // namespace mtb
@@ -625,4 +663,8 @@ void register_matmul_kernels(kernel_table& t) {
 // direct entry for tests and the bench's contraction line (device pointers, row-major)
 extern "C" int mt_gemm_bf16_nt(const void* a, const void* bt, float* c, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, void* stream) {
 	return mtb::tc::run_gemm(a, m, lda, 0, bt, n, ldb, 0, c, ldc, m, n, k, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int mt_gemm_tf32_nt(const float* a, const float* bt, float* c, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, void* stream) {
+	return mtb::tc::run_gemm(a, m, lda, 0, bt, n, ldb, 0, c, ldc, m, n, k, static_cast<cudaStream_t>(stream), true);
 }

@@ -80,3 +80,59 @@ def test_matmul_nt_bf16_through_the_planner():
     rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
     assert rel.max() <= REL
     assert kinds.count("execute") == 4 and kinds.count("send") > 0
+
+
+def _tf32_fn():
+    fn = mb.lib().dll.mt_gemm_tf32_nt
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]
+    return fn
+
+
+def tf32_trunc(x: np.ndarray) -> np.ndarray:
+    """f32 with the 13 low mantissa bits cleared: the operand value kind::tf32 multiplies"""
+    return (x.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 32), (300, 520, 136), (1024, 768, 1000), (2048, 2048, 4096), (3000, 4100, 1000)])
+def test_gemm_tf32_matches_fp64(m, n, k):
+    """the fp32 form of C3 (kind::tf32, f32 accumulation) within 1e-3 of the fp64 product of the
+    f32 inputs; and within 1e-4 of the fp64 product of the TF32-truncated inputs, which pins
+    the operand conversion (the low 13 mantissa bits are ignored: against the f32 inputs the
+    error is a bias of about -7e-4, against the truncated ones about 3e-5 at k = 4096, the
+    tensor core's own accumulation)"""
+    import torch
+    rng = np.random.default_rng(m + n + k)
+    a = pattern(m, k, 1000, 7) if k % 2 else rng.random((m, k), dtype=np.float32)
+    bt = pattern(n, k, 997, 3)
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(bt).cuda()
+    dc = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+    assert _tf32_fn()(da.data_ptr(), db.data_ptr(), dc.data_ptr(), m, n, k, k, k, n, torch.cuda.current_stream().cuda_stream) == 0
+    torch.cuda.synchronize()
+    got = dc.cpu().numpy().astype(np.float64)
+    assert np.isfinite(got).all()
+    want = a.astype(np.float64) @ bt.astype(np.float64).T
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+    assert rel.max() <= REL, rel.max()
+    want_t = tf32_trunc(a).astype(np.float64) @ tf32_trunc(bt).astype(np.float64).T
+    rel_t = np.abs(got - want_t) / np.maximum(np.abs(want_t), 1e-30)
+    assert rel_t.max() <= 1e-4, (rel_t.max(), rel.max())
+
+
+def test_matmul_nt_tf32_through_the_planner():
+    m, n, k = 512, 768, 320
+    a = pattern(m, k, 1000, 7)
+    bt = pattern(n, k, 997, 3)
+    with mb.context(workers=1, devices=4, num_gpus=1) as ctx:
+        devs = ctx.devices
+        A = ctx.create_array([m, k], "f32", ctx.dist.row([m, k], 128, devs), 0)
+        B = ctx.create_array([n, k], "f32", ctx.dist.row([n, k], 192, devs), 0)
+        Cm = ctx.create_array([m, n], "f32", ctx.dist.tile([m, n], [256, 384], devs), 0)
+        ctx.write(A, a)
+        ctx.write(B, bt)
+        work = ctx.dist.block_work([m, n], [16, 16], [256, 384], devs)
+        ctx.launch("matmul_nt_tf32", [m, n], [16, 16], work, [m, n, k, Arr(Cm), Arr(A), Arr(B)],
+                   "global [i, j] => write C[i,j], read A[i,:], read Bt[j,:]")
+        got = ctx.read(Cm).astype(np.float64)
+    want = a.astype(np.float64) @ bt.astype(np.float64).T
+    assert (np.abs(got - want) / np.maximum(np.abs(want), 1e-30)).max() <= REL
