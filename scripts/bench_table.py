@@ -17,6 +17,11 @@ rows = [
     ("C3 contraction 32768³ bf16 (tcgen05)", f"{d['contraction']['value']:.0f} TFLOP/s",
      f"{d['contraction']['roofline']['frac']:.2f} of burst cuBLAS ({d['contraction']['roofline']['peak']:.0f}); "
      f"{d['contraction']['roofline']['frac_of_sustained']:.2f} of sustained"),
+] + ([
+    ("C3 contraction 32768³ fp32 operands as TF32 (tcgen05)", f"{d['contraction']['tf32']['value']:.0f} TFLOP/s",
+     f"{d['contraction']['tf32']['roofline']['frac']:.2f} of half the bf16 burst; max rel. err vs fp64 "
+     f"{d['contraction']['tf32']['max_rel_err_16_samples_vs_fp64']:.1e}"),
+] if 'tf32' in d['contraction'] else []) + [
     ("C4 histogram 4e9 → 256 bins", f"{h[0]['value']/1e12:.2f} T elements/s", f"{h[0]['roofline']['frac']:.2f} of copy peak (read-only stream)"),
     ("C4 histogram 4e9 → 65536 bins", f"{h[1]['value']/1e12:.2f} T elements/s", f"{h[1]['roofline']['frac']:.2f} (shared-atomic bank conflicts)"),
     ("C4 k-means assign 1e9×16, k=256", f"{km['assign']['ms']:.0f} ms",
