@@ -114,6 +114,14 @@ __device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_
 	    "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ void tc_mma2_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+	asm volatile(
+	    "{\n\t.reg .pred p;\n\t"
+	    "setp.ne.b32 p, %4, 0;\n\t"
+	    "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+	    "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void tc_commit2_mc(uint64_t* bar, uint16_t mask) {
 	asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
 	    : "memory");
@@ -182,8 +190,8 @@ __host__ __device__ constexpr uint32_t instr_desc(int m = BM) {
 }
 
 // kind::tf32 instruction descriptor: tf32 x tf32 -> f32 (formats 2), both K-major, 128 x 256
-__host__ __device__ constexpr uint32_t instr_desc_tf32() {
-	return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
+__host__ __device__ constexpr uint32_t instr_desc_tf32(int m = BM) {
+	return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -370,8 +378,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // the leader for both); the leader's MMA commit frees the stage in both CTAs and signals both
 // CTAs' `tmem_full`; both CTAs' epilogue warps release the accumulator on the leader's
 // `tmem_empty` (count 8).
+template <bool TF32>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_nt_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, gemm_args p) {
+	constexpr int BKE = TF32 ? BK / 2 : BK; // K elements per stage
 	extern __shared__ uint8_t smem_raw[];
 	uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
 	uint8_t* a_smem = smem;
@@ -429,8 +439,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 				for(int kb = 0; kb < p.k_blocks; ++kb) {
 					mbar_wait(&empty[stage], phase ^ 1);
 					if(leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE2_BYTES);
-					tma_load_2d_2sm(a_smem + stage * A_STAGE_BYTES, &tmap_a, &full[stage], kb * BK, arow, p.hint_a);
-					tma_load_2d_2sm(b_smem + stage * B2_STAGE_BYTES, &tmap_b, &full[stage], kb * BK, brow, p.hint_b);
+					tma_load_2d_2sm(a_smem + stage * A_STAGE_BYTES, &tmap_a, &full[stage], kb * BKE, arow, p.hint_a);
+					tma_load_2d_2sm(b_smem + stage * B2_STAGE_BYTES, &tmap_b, &full[stage], kb * BKE, brow, p.hint_b);
 					if(++stage == STAGES2) {
 						stage = 0;
 						phase ^= 1;
@@ -441,7 +451,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	} else if(warp == 1) {
 		if(lane == 0 && leader) {
 			// ---- MMA issuer (leader only) ----
-			constexpr uint32_t idesc = instr_desc(2 * BM);
+			constexpr uint32_t idesc = TF32 ? instr_desc_tf32(2 * BM) : instr_desc(2 * BM);
 			int stage = 0;
 			uint32_t phase = 0;
 			int local = 0;
@@ -456,8 +466,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 					const uint32_t a0 = smem_u32(a_smem + stage * A_STAGE_BYTES);
 					const uint32_t b0 = smem_u32(b_smem + stage * B2_STAGE_BYTES);
 #pragma unroll
-					for(int k = 0; k < BK / UMMA_K; ++k)
-						tc_mma2(d, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+					for(int k = 0; k < BK / UMMA_K; ++k) {
+						if constexpr(TF32)
+							tc_mma2_tf32(d, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+						else
+							tc_mma2(d, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+					}
 					tc_commit2_mc(&empty[stage], kPair);
 					if(++stage == STAGES2) {
 						stage = 0;
@@ -580,11 +594,13 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	// pairs are 5-12% faster from 4096^3 to 16384^2 x 32768, but at M = N = K = 32768 they read
 	// ~4x the DRAM bytes of the single-CTA kernel (L2 reuse across the wave is lost; the cause is
 	// not understood yet), so problems with both M*N > 16384^2 and K > 16384 stay on single CTAs.
-	const bool big = static_cast<double>(m) * static_cast<double>(n) > 16384.0 * 16384.0 && k > 16384;
+	// TF32 (twice the operand bytes per K): pairs win at 8192^3 (830 vs 767 TFLOP/s) and lose from
+	// 16384^3 (677 vs 747), so f32 operands keep single CTAs once K exceeds 8192
+	const bool big = tf32 ? k > 8192 : static_cast<double>(m) * static_cast<double>(n) > 16384.0 * 16384.0 && k > 16384;
 	p.no_store = std::getenv("MTB_GEMM_NOSTORE") != nullptr;
 	p.n_major = std::getenv("MTB_GEMM_NMAJOR") != nullptr;
 	const bool force_pair = std::getenv("MTB_GEMM_FORCE_PAIR") != nullptr;
-	const bool pair = !tf32 && p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && (!big || force_pair) && std::getenv("MTB_GEMM_NO_PAIR") == nullptr;
+	const bool pair = p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && (!big || force_pair) && std::getenv("MTB_GEMM_NO_PAIR") == nullptr;
 	CUtensorMap ma, mb;
 	if(!make_map(&ma, a, a_rows, k, lda, BM, tf32) || !make_map(&mb, bt, b_rows, k, ldb, pair ? BN / 2 : BN, tf32)) return 7;
 	if(!pair) {
@@ -598,7 +614,8 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 		}
 		return cudaGetLastError() == cudaSuccess ? 0 : 1;
 	}
-	kern::ensure_smem(gemm_bf16_nt_2sm_kernel, static_cast<int>(SMEM2_BYTES));
+	const auto pair_kernel = tf32 ? gemm_bf16_nt_2sm_kernel<true> : gemm_bf16_nt_2sm_kernel<false>;
+	kern::ensure_smem(pair_kernel, static_cast<int>(SMEM2_BYTES));
 	cudaLaunchConfig_t cfg{};
 	cudaLaunchAttribute attr[1];
 	attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -610,11 +627,12 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	cfg.stream = s;
 	cfg.attrs = attr;
 	cfg.numAttrs = 1;
-	static int max_clusters = 0;
+	static int max_clusters_by_kind[2] = {0, 0};
+	int& max_clusters = max_clusters_by_kind[tf32 ? 1 : 0];
 	if(max_clusters == 0) {
 		cfg.gridDim = dim3(static_cast<unsigned>(sms & ~1));
 		int n_cl = 0;
-		if(cudaOccupancyMaxActiveClusters(&n_cl, gemm_bf16_nt_2sm_kernel, &cfg) != cudaSuccess || n_cl <= 0) n_cl = sms / 2;
+		if(cudaOccupancyMaxActiveClusters(&n_cl, pair_kernel, &cfg) != cudaSuccess || n_cl <= 0) n_cl = sms / 2;
 		cudaGetLastError();
 		max_clusters = n_cl;
 		if(const char* e = std::getenv("MTB_GEMM_CLUSTERS")) max_clusters = std::max(1, std::atoi(e));
@@ -622,7 +640,7 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	}
 	const int units = ((p.m_blocks + 1) / 2) * p.n_blocks;
 	cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(units, max_clusters)));
-	if(cudaLaunchKernelEx(&cfg, gemm_bf16_nt_2sm_kernel, ma, mb, p) != cudaSuccess) return 1;
+	if(cudaLaunchKernelEx(&cfg, pair_kernel, ma, mb, p) != cudaSuccess) return 1;
 	return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

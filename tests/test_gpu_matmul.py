@@ -94,7 +94,9 @@ def tf32_trunc(x: np.ndarray) -> np.ndarray:
     return (x.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
 
 
-@pytest.mark.parametrize("m,n,k", [(128, 256, 32), (300, 520, 136), (1024, 768, 1000), (2048, 2048, 4096), (3000, 4100, 1000)])
+@pytest.mark.parametrize("m,n,k", [(128, 256, 32), (300, 520, 136), (1024, 768, 1000), (2048, 2048, 4096),
+                                   # CTA-pair kernel: odd M-block count, ragged N and K
+                                   (4224, 4096, 512), (3000, 4100, 1000)])
 def test_gemm_tf32_matches_fp64(m, n, k):
     """the fp32 form of C3 (kind::tf32, f32 accumulation) within 1e-3 of the fp64 product of the
     f32 inputs; and within 1e-4 of the fp64 product of the TF32-truncated inputs, which pins
