@@ -90,11 +90,14 @@ void dep_tracker::read(int64_t chunk, int64_t task, const box& region_in, std::v
 	state& s = get(chunk);
 	const box region = compat_ ? s.region : intersect(region_in, s.region);
 	if(region.is_empty()) return;
-	std::vector<cell> keep, inside;
-	keep.reserve(s.cells.size() + 4);
-	for(const auto& c : s.cells) {
+	// scratch lists reused across calls (the planner is single-threaded per context; thread_local
+	// keeps contexts on different threads apart); untouched cells are moved, not copied
+	static thread_local std::vector<cell> keep, inside;
+	keep.clear();
+	inside.clear();
+	for(auto& c : s.cells) {
 		if(!overlaps(c.region, region)) {
-			keep.push_back(c);
+			keep.push_back(std::move(c));
 			continue;
 		}
 		if(c.writer >= 0) deps.push_back(c.writer);
@@ -105,7 +108,8 @@ void dep_tracker::read(int64_t chunk, int64_t task, const box& region_in, std::v
 		if(it == c.readers.end() || *it != task) c.readers.insert(it, task);
 		keep.push_back(std::move(c));
 	}
-	s.cells = std::move(keep);
+	s.cells.swap(keep);
+	keep.clear();
 	coalesce(s.cells);
 }
 
@@ -113,11 +117,12 @@ void dep_tracker::write(int64_t chunk, int64_t task, const box& region_in, std::
 	state& s = get(chunk);
 	const box region = compat_ ? s.region : intersect(region_in, s.region);
 	if(region.is_empty()) return;
-	std::vector<cell> keep, inside;
-	keep.reserve(s.cells.size() + 4);
-	for(const auto& c : s.cells) {
+	static thread_local std::vector<cell> keep, inside;
+	keep.clear();
+	inside.clear();
+	for(auto& c : s.cells) {
 		if(!overlaps(c.region, region)) {
-			keep.push_back(c);
+			keep.push_back(std::move(c));
 			continue;
 		}
 		if(c.writer >= 0) deps.push_back(c.writer);
@@ -126,7 +131,8 @@ void dep_tracker::write(int64_t chunk, int64_t task, const box& region_in, std::
 		split(c, region, inside, keep);
 	}
 	keep.push_back(cell{region, task, {}});
-	s.cells = std::move(keep);
+	s.cells.swap(keep);
+	keep.clear();
 	s.filled = true;
 	coalesce(s.cells);
 }
