@@ -11,9 +11,18 @@
 //   * region mode emits a subset of those edges whose transitive closure still orders every
 //     pair of conflicting accesses (each dropped edge is to a task whose cells were
 //     overwritten, and the overwriting task is itself ordered after it).
+//
+// Cost. The reference's registry is O(1) per access (array_registry.cpp:41-60). Cells of a
+// chunk are kept in an ordered map keyed by their low corner along one index axis (the axis
+// the accesses split, chosen and re-chosen from the cells' shapes), with a count of cell
+// extents along that axis: an access visits only cells whose low corner lies within
+// (max extent) of its box, and coalesces only the cells around the box it touched. Band
+// accesses of one chunk by S superblocks cost O(log S) each instead of O(S^2).
 #pragma once
 
+#include <array>
 #include <cstdint>
+#include <map>
 #include <unordered_map>
 #include <vector>
 
@@ -32,6 +41,8 @@ class dep_tracker {
 	// Create task: `creator` becomes the writer of the whole chunk (array_registry.cpp:24-28)
 	void mark_created(int64_t chunk, int64_t creator, bool filled);
 	bool filled(int64_t chunk) const;
+	// host upload outside the plan (mt_array_write): the chunk holds defined data from now on
+	void mark_filled(int64_t chunk);
 
 	// Records an access over `region` (clipped to the chunk) and appends the tasks the
 	// accessor must wait for to `deps` (unsorted, may contain duplicates).
@@ -39,6 +50,7 @@ class dep_tracker {
 	void write(int64_t chunk, int64_t task, const box& region, std::vector<int64_t>& deps);
 
 	size_t cell_count(int64_t chunk) const;
+	int index_axis(int64_t chunk) const;
 
   private:
 	struct cell {
@@ -46,10 +58,14 @@ class dep_tracker {
 		int64_t writer = -1;
 		std::vector<int64_t> readers; // ascending
 	};
+	using key = std::array<int64_t, kMaxRank>; // low corner, index axis first
 	struct state {
 		box region;
 		bool filled = false;
-		std::vector<cell> cells; // disjoint, covering `region`
+		int axis = 0;                        // index axis
+		std::map<key, cell> cells;           // disjoint, covering `region`
+		std::map<int64_t, int64_t> extents;  // cell extent along `axis` -> count
+		int64_t probes = 0, hits = 0;        // scan efficiency since the last axis check
 	};
 
 	bool compat_;
@@ -57,8 +73,14 @@ class dep_tracker {
 
 	state& get(int64_t chunk);
 	const state& get(int64_t chunk) const;
-	static void split(const cell& c, const box& cut, std::vector<cell>& out_inside, std::vector<cell>& out_outside);
-	static void coalesce(std::vector<cell>& cells);
+	static key key_of(const state& s, const box& b);
+	static void insert(state& s, cell&& c);
+	static cell take(state& s, std::map<key, cell>::iterator it);
+	// moves every cell overlapping `q` out of the map into `out`
+	static void extract(state& s, const box& q, std::vector<cell>& out);
+	static void reindex(state& s);
+	static void split(cell&& c, const box& cut, std::vector<cell>& inside, std::vector<cell>& outside);
+	void settle(state& s, const box& touched);
 };
 
 } // namespace mtb
