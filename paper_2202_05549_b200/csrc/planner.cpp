@@ -80,12 +80,18 @@ int64_t planner::emit_create(int worker, device_id dev, int64_t chunk_id, fill_k
 void planner::record(int64_t c, int64_t t, bool write, const box& region, bool check_filled, std::vector<int64_t>& out) {
 	if(check_filled && !deps_.filled(c))
 		throw plan_error("chunk " + std::to_string(c) + " is read before any fill or write; its contents would be undefined");
-	std::vector<int64_t> d;
-	if(write)
-		deps_.write(c, t, region, d);
-	else
-		deps_.read(c, t, region, d);
-	if(!cfg_.suppress_conflict_deps) out.insert(out.end(), d.begin(), d.end());
+	if(cfg_.suppress_conflict_deps) {
+		static thread_local std::vector<int64_t> discard;
+		discard.clear();
+		if(write)
+			deps_.write(c, t, region, discard);
+		else
+			deps_.read(c, t, region, discard);
+	} else if(write) {
+		deps_.write(c, t, region, out);
+	} else {
+		deps_.read(c, t, region, out);
+	}
 	if(cfg_.record_accesses) accesses_.push_back({t, c, region, write});
 }
 
@@ -318,27 +324,33 @@ std::pair<int64_t, int64_t> planner::launch(const std::string& kernel, const box
 	std::vector<std::vector<partial>> partials(A);
 	std::vector<int> cand;
 
+	struct rec_t {
+		int64_t chunk;
+		bool write;
+		bool check;
+		box region;
+	};
+	struct write_t {
+		size_t access;
+		box region;
+		int64_t source;
+		bool temp;
+	};
+	// per-superblock scratch, reused
+	std::vector<rec_t> recs;
+	std::vector<write_t> writes;
+	std::vector<int64_t> dead;
+	std::vector<std::pair<size_t, int64_t>> sb_partials;
 	for(size_t s = 0; s < S; ++s) {
 		const device_id dev = work[s].device;
 		const int worker = dev.worker;
 		std::vector<arg_bind> binds(np);
 		std::vector<int64_t> exec_deps;
-		struct rec_t {
-			int64_t chunk;
-			bool write;
-			bool check;
-			box region;
-		};
-		std::vector<rec_t> recs;
-		struct write_t {
-			size_t access;
-			box region;
-			int64_t source;
-			bool temp;
-		};
-		std::vector<write_t> writes;
-		std::vector<int64_t> dead;
-		std::vector<std::pair<size_t, int64_t>> sb_partials;
+		exec_deps.reserve(8);
+		recs.clear();
+		writes.clear();
+		dead.clear();
+		sb_partials.clear();
 
 		for(size_t i = 0; i < np; ++i) {
 			const auto& p = def.params[i];
@@ -420,9 +432,9 @@ std::pair<int64_t, int64_t> planner::launch(const std::string& kernel, const box
 		e.sb_blocks = work[s].blocks;
 		e.sb_threads = sb_threads[s];
 		e.block_size = block;
-		e.args = binds;
+		e.args = std::move(binds);
 		const int64_t exec_id = emit(std::move(e));
-		for(const auto& b : binds)
+		for(const auto& b : plan_.back().args)
 			if(b.kind == arg_kind::chunk && chunk(b.chunk).temp) touch(b.chunk, exec_id);
 		for(const auto& [a, part] : sb_partials) partials[a].push_back({part, exec_id});
 
