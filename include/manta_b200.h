@@ -184,6 +184,10 @@ typedef struct mt_config {
 	                                   of evicted chunks move to a spill file when the host tier is full;
 	                                   0 = no disk tier */
 	const char* spill_dir;          /* directory of the spill file (NULL: the system temp directory) */
+	uint64_t schedule_seed;         /* 0: deterministic stream choice; else every task goes to a compute stream
+	                                   drawn from a generator seeded with it, behind a random on-device delay,
+	                                   and graph replay is off: the GPU analogue of the reference's seeded
+	                                   ready-task choice (runtime.cpp:313-319, run_overrides::ready_seed) */
 } mt_config;
 
 /* One planned chunk access (a create counts as a write of the whole chunk). */

@@ -523,6 +523,7 @@ system_config make_system_config(const mt_config& c) {
 	if(c.staging_threshold) sys.memory.staging_threshold = c.staging_threshold;
 	if(c.disk_capacity) sys.memory.disk_capacity = c.disk_capacity;
 	sys.memory.disk_in_memory = true;
+	if(c.schedule_seed) sys.ready_seed = c.schedule_seed;
 	sys.progress_timeout = std::chrono::milliseconds(600000);
 	return sys;
 }

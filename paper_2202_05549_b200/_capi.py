@@ -92,6 +92,7 @@ class Config(C.Structure):
         ("device_capacity", C.c_uint64), ("host_capacity", C.c_uint64), ("staging_threshold", C.c_uint64),
         ("record_accesses", C.c_int32), ("lookahead_tasks", C.c_int32),
         ("worker_rank", C.c_int32), ("gpu_base", C.c_int32), ("collective_reduce", C.c_int32), ("drop_executed_tasks", C.c_int32), ("disk_capacity", C.c_uint64), ("spill_dir", C.c_char_p),
+        ("schedule_seed", C.c_uint64),
     ]
 
 

@@ -218,7 +218,7 @@ class Context:
     def __init__(self, lib: capi.Lib, workers=1, devices=1, execute=True, compat_deps=False, suppress_conflict_deps=False,
                  num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0, record_accesses=False,
                  lookahead_tasks=0, worker_rank=None, gpu_base=0, collective_reduce=False, retain_plan=True, disk_capacity=0,
-                 spill_dir=None):
+                 spill_dir=None, schedule_seed=0):
         self.lib = lib
         self.dist = Distributions(lib)
         cfg = capi.Config()
@@ -238,6 +238,7 @@ class Context:
         cfg.disk_capacity = int(disk_capacity)
         self._spill_dir = spill_dir.encode() if spill_dir else None
         cfg.spill_dir = self._spill_dir
+        cfg.schedule_seed = int(schedule_seed)
         if worker_rank is not None:  # one process per worker
             cfg.single_worker, cfg.worker_rank, cfg.gpu_base = 1, int(worker_rank), int(gpu_base)
         self.single_worker = worker_rank is not None
@@ -409,6 +410,11 @@ class Context:
         # torch tensor (e.g. pinned host memory)
         if buf.is_cuda or not buf.is_contiguous() or list(buf.shape) != list(shape):
             raise ValidationError("host buffer must be a contiguous host tensor with the array's (or the box's) shape")
+        import torch
+        want = {I32: (torch.int32,), I64: (torch.int64,), F32: (torch.float32,), F64: (torch.float64,),
+                BF16: (torch.bfloat16, torch.uint16, torch.int16)}[t]
+        if buf.dtype not in want:
+            raise ValidationError(f"host tensor dtype {buf.dtype} does not match the array's element type { {v: k for k, v in capi.DTYPE_NAMES.items()}.get(t, t)}")
         return buf.data_ptr(), buf.numel() * buf.element_size()
 
     def replicas_coherent(self, array_id: int) -> bool:

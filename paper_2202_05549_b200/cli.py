@@ -14,8 +14,10 @@ incoherent replicas, 3 internal error; manta.cpp:15-18, 166-178).
 
 System flags follow add_system_flags (manta.cpp:46-54). On the GPU executor `--throttle` is
 informational, `--disk-capacity` sizes the spill file below the pinned-host tier, and
-`--seed` (randomised ready-task choice in the reference's host scheduler) has no counterpart:
-tasks run as soon as their CUDA events allow, concurrently over `--streams` streams per device.
+`--seed` randomises the schedule like the reference's seeded ready-task choice
+(runtime.cpp:313-319): every task goes to a compute stream drawn from the seeded generator,
+behind a random on-device delay (mt_config.schedule_seed); without it tasks run as soon as
+their CUDA events allow, concurrently over `--streams` streams per device.
 """
 from __future__ import annotations
 
@@ -88,6 +90,8 @@ def system_of(sc: dict, flags) -> dict:
             s[key] = v
     if flags is not None and getattr(flags, "throttle", None) is not None:
         s["staging_threshold"] = flags.throttle
+    if flags is not None and getattr(flags, "seed", None) is not None and flags.cmd != "fuzz":
+        s["ready_seed"] = flags.seed
     s.setdefault("workers", 1)
     s.setdefault("devices", 1)
     if s["workers"] < 1 or s["devices"] < 1:
@@ -107,7 +111,8 @@ def make_context(sysd: dict, execute: bool, oracle_mode=False, suppress=False, s
     disk = int(sysd.get("disk_capacity", 0)) if spill else 0
     return context(workers=workers, devices=devices, execute=execute, num_gpus=1 if execute else 0, suppress_conflict_deps=suppress, compat_deps=compat,
                    streams_per_device=streams, device_capacity=cap if spill else 0, host_capacity=max(host, cap) if spill else 0,
-                   staging_threshold=int(sysd.get("staging_threshold", 0)), disk_capacity=disk)
+                   staging_threshold=int(sysd.get("staging_threshold", 0)), disk_capacity=disk,
+                   schedule_seed=0 if oracle_mode else int(sysd.get("ready_seed", 0) or 0))
 
 
 def run_scenario(sc: dict, sysd: dict, oracle_mode=False, suppress=False, streams=0, compat=False, trace=False):
@@ -295,7 +300,7 @@ def _system_flags(p: argparse.ArgumentParser):
     p.add_argument("--host-capacity", dest="host_capacity", type=int, help="Host memory capacity in bytes")
     p.add_argument("--disk-capacity", dest="disk_capacity", type=int, help="Disk tier capacity in bytes")
     p.add_argument("--throttle", type=int, help="Staging throttle threshold in bytes (informational)")
-    p.add_argument("--seed", type=int, help="Accepted for compatibility; GPU tasks run as their events allow")
+    p.add_argument("--seed", type=int, help="Randomise the schedule: seeded stream choice and on-device delays per task")
     p.add_argument("--streams", type=int, default=0, help="Compute streams per device (0 = 4)")
     p.add_argument("--no-conflict-deps", dest="no_conflict_deps", action="store_true", help=argparse.SUPPRESS)
     p.add_argument("--compat-deps", dest="compat_deps", action="store_true",

@@ -230,6 +230,7 @@ executor_config exec_cfg(const mt_config& c) {
 	e.lookahead = c.lookahead_tasks > 0 ? c.lookahead_tasks : 512;
 	e.disk_capacity = c.disk_capacity;
 	if(c.spill_dir) e.spill_dir = c.spill_dir;
+	e.schedule_seed = c.schedule_seed;
 	if(c.single_worker) {
 		// one process per worker: this process executes worker_rank only, on GPU ordinal
 		// gpu_base (+ device index); every rank plans the identical full plan
@@ -419,10 +420,16 @@ int mt_array_read(mt_ctx* ctx, int64_t id, void* host, uint64_t bytes) {
 int mt_array_write(mt_ctx* ctx, int64_t id, const void* host, uint64_t bytes) {
 	return guarded([&] {
 		mt_exec& e = need_exec(ctx);
-		flush(ctx);
 		const array_rec& a = ctx->plan->array(id);
 		if(bytes < static_cast<uint64_t>(a.domain.volume()) * dtype_size(a.type)) throw validation_error("host buffer too small");
-		for(const auto& c : a.chunks) e.ex->upload(c.id, host, a.domain);
+		// synchronous upload outside the plan: every queued task (a copy on another GPU may
+		// still read these chunks) completes first
+		flush(ctx);
+		e.ex->sync();
+		for(const auto& c : a.chunks)
+			if(e.ex->has_chunk(c.id)) e.ex->upload(c.id, host, a.domain); // single_worker: local chunks only
+		// the chunks now hold defined data: later launches may read them
+		ctx->plan->mark_filled(id);
 	});
 }
 

@@ -281,7 +281,7 @@ void copy_box(const void* src_base, const box& src_chunk, int src_gpu, void* dst
 
 // ---- executor ------------------------------------------------------------------------------
 
-executor::executor(const executor_config& cfg) : cfg_(cfg) {
+executor::executor(const executor_config& cfg) : cfg_(cfg), rng_state_(cfg.schedule_seed) {
 	int n = 0;
 	const cudaError_t e = cudaGetDeviceCount(&n);
 	if(e != cudaSuccess || n == 0) throw execution_error("no CUDA device available for the B200 executor (" + std::string(cudaGetErrorString(e)) + ")");
@@ -465,7 +465,46 @@ void executor::set_trace(bool on) {
 	trace_ = on;
 }
 
+namespace {
+__global__ void delay_kernel(uint32_t ns) {
+	const uint64_t until = [] {
+		uint64_t t;
+		asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+		return t;
+	}() + ns;
+	for(;;) {
+		uint64_t now;
+		asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+		if(now >= until) break;
+		__nanosleep(256);
+	}
+}
+} // namespace
+
+uint64_t executor::next_random() { // splitmix64
+	uint64_t z = (rng_state_ += 0x9e3779b97f4a7c15ull);
+	z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+	z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+	return z ^ (z >> 31);
+}
+
+// Seeded schedule perturbation: half of the tasks wait 0-40 us on the device before they
+// start, so ready work on different streams and devices completes in a different order per
+// seed (the reference picks a random ready task per step, runtime.cpp:313-319).
+void executor::perturb(cudaStream_t s) {
+	if(!cfg_.schedule_seed) return;
+	const uint64_t r = next_random();
+	if(r & 1) return;
+	delay_kernel<<<1, 1, 0, s>>>(static_cast<uint32_t>((r >> 8) % 40000));
+	check_cuda(cudaGetLastError(), "delay kernel");
+}
+
 cudaStream_t executor::pick_compute(const task& t, ldev& L) {
+	if(cfg_.schedule_seed) {
+		cudaStream_t s = L.compute[next_random() % L.compute.size()];
+		perturb(s);
+		return s;
+	}
 	int64_t best = -1;
 	cudaStream_t chosen = nullptr;
 	for(const auto d : t.deps) {
@@ -560,7 +599,7 @@ void executor::issue_batch() {
 }
 
 bool executor::graph_eligible(const std::vector<task>& b, int* gpu) const {
-	if(spill_ || trace_ || profile_) return false;
+	if(spill_ || trace_ || profile_ || cfg_.schedule_seed) return false;
 	// Only submissions whose GPU work is short enough that issuing them costs as much as running
 	// them: consecutive replays run back to back on one stream, which gives up the overlap
 	// between submissions that the multi-stream path keeps for large superblocks.
@@ -1346,6 +1385,7 @@ void executor::run_copy(const task& t) {
 	if(src.type != dst.type) throw execution_error("copy between chunks of different element types");
 	ldev& L = dev(t.resource);
 	cudaStream_t s = L.copy;
+	perturb(s);
 	wait_deps(t, s);
 	copy_box(src.ptr, src.region, ord(src.gpu), dst.ptr, dst.region, ord(dst.gpu), t.dst_region, dtype_size(src.type), s);
 	++ctr_.copies;

@@ -52,6 +52,7 @@ struct executor_config {
 	int local_workers = -1;       // -1: all workers
 	uint64_t disk_capacity = 0;   // disk tier below the host tier (0: none)
 	std::string spill_dir;        // spill file directory ("" = system temp directory)
+	uint64_t schedule_seed = 0;   // != 0: randomised stream choice + delays (reference ready_seed)
 };
 
 struct exec_counters {
@@ -269,6 +270,10 @@ class executor {
 	cudaEvent_t take_event(int gpu);
 	void wait_deps(const task& t, cudaStream_t s);
 	cudaStream_t pick_compute(const task& t, ldev& L);
+	// schedule perturbation (cfg.schedule_seed): a random on-device delay before a task
+	uint64_t rng_state_ = 0;
+	uint64_t next_random();
+	void perturb(cudaStream_t s);
 	void finish(const task& t, cudaStream_t s);
 	void retire_completed();
 	buffer& buf(int64_t chunk);

@@ -195,6 +195,10 @@ void planner::delete_array(int64_t id) {
 	arrays_.erase(id);
 }
 
+void planner::mark_filled(int64_t id) {
+	for(const auto& c : array(id).chunks) deps_.mark_filled(c.id);
+}
+
 namespace {
 
 struct bound_param {

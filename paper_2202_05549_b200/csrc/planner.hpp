@@ -61,6 +61,8 @@ class planner {
 
 	const array_rec& create_array(const box& domain, dtype type, std::vector<chunk_desc> chunks, fill_kind fill);
 	void delete_array(int64_t id);
+	// the array's chunks were filled outside the plan (mt_array_write's synchronous upload)
+	void mark_filled(int64_t id);
 	std::pair<int64_t, int64_t> launch(const std::string& kernel, const box& grid, const point& block, const std::vector<superblock>& work,
 	    const std::vector<launch_arg>& args, const annotation& ann);
 

@@ -1,0 +1,146 @@
+"""The reference's acceptance criteria that pin this path, run on the B200 executor
+(proj/tests/acceptance/acceptance.cpp). Expected outputs come from the reference itself
+(oracle/_ref: its oracle_run, i.e. every array on one device of the CPU executor).
+
+* c3 (acceptance.cpp:158-180): every bundled scenario on the four system shapes
+  {1x1, 1x4, 2x2, 4x1} equals the oracle run within 1e-6 (compare_results), replicas coherent.
+* c4 (acceptance.cpp:182-237): device capacity a quarter of the largest per-device working set
+  (max_device_working_set, acceptance.cpp:63-78): the stencil on 1x2 evicts and stays exact,
+  then with the host tier capped at half the working set spills cascade to disk; the matmul
+  chain on 1x1 at a quarter capacity evicts and stays exact -- the case that stalls the
+  reference's first-fit pool (memory.cpp:18-31). The executor caps memory per
+  physical GPU; the logical devices of one system share the test GPU, so the cap is the sum
+  of the per-device caps (2 x ws/4 on 1x2).
+* c7 (acceptance.cpp:289-311): the stencil on 2x2 is byte-identical across schedules. The
+  reference reorders its ready queue with a seed (runtime.cpp:313-319); here the seed draws
+  every task's compute stream and a random on-device delay (mt_config.schedule_seed), and the
+  schedule also varies with 1/2/4/16 streams per device and with graph replay on/off.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2202_05549_b200 as mb
+from paper_2202_05549_b200 import scenario as S
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(1, 1), (1, 4), (2, 2), (4, 1)]
+NAMES = ["compute_only", "correlator_like", "map", "matmul", "nbody_like", "reduction", "spmv", "stencil"]
+
+
+@pytest.fixture(scope="module")
+def oracle_out(ref, scenarios):
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            cache[name] = S.reference_run(ref, scenarios[name], oracle_mode=True)[0]
+        return cache[name]
+    return get
+
+
+def run_product(sc, workers, devices, **kw):
+    with mb.context(workers=workers, devices=devices, num_gpus=1, **kw) as ctx:
+        S.register_gather_kernels(ctx, sc)
+        got, coherent = S.run(ctx, sc)
+        stats = ctx.exec_stats()
+    return got, coherent, stats
+
+
+def max_device_working_set(sc, workers, devices):
+    """acceptance.cpp:63-78: non-temporary create bytes per device, 4 KiB rounded; the max"""
+    with mb.context(workers=workers, devices=devices, execute=False) as ctx:
+        S.register_gather_kernels(ctx, sc)
+        S.apply(ctx, sc, flush=False)
+        per = {}
+        for t in ctx.plan():
+            if t["kind"] != "create" or ctx.chunk_meta(t["chunk"])[2]:
+                continue
+            lo, hi = t["region"]
+            nbytes = int(np.prod([h - l for l, h in zip(lo, hi)])) * mb._capi.DTYPE_SIZE[t["dtype"]]
+            per[t["home"]] = per.get(t["home"], 0) + (nbytes + 4095) // 4096 * 4096
+    return max(per.values())
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=[f"{w}x{d}" for w, d in SHAPES])
+@pytest.mark.parametrize("name", NAMES)
+def test_c3_scenario_on_four_shapes(name, shape, scenarios, oracle_out):
+    sc = scenarios[name]
+    got, coherent, _ = run_product(sc, *shape)
+    assert coherent, f"{name} on {shape}: replicas disagree"
+    assert S.compare(got, oracle_out(name), 1e-6) == []
+
+
+def test_c4_stencil_quarter_capacity_and_disk_cascade(scenarios, oracle_out, tmp_path):
+    sc = scenarios["stencil"]
+    ws = max_device_working_set(sc, 1, 2)
+    cap = 2 * (ws // 4)
+    got, coherent, st = run_product(sc, 1, 2, device_capacity=cap, host_capacity=1 << 30)
+    assert coherent and st["evictions"] > 0
+    assert st["peak_device_bytes"] <= cap
+    assert S.compare(got, oracle_out("stencil"), 1e-6) == []
+    # the host tier capped at half the working set: evicted copies move on to disk
+    got, coherent, st = run_product(sc, 1, 2, device_capacity=cap, host_capacity=ws // 2, disk_capacity=8 * ws, spill_dir=str(tmp_path))
+    assert coherent and st["evictions"] > 0
+    assert st["bytes_host_to_disk"] > 0
+    assert S.compare(got, oracle_out("stencil"), 1e-6) == []
+
+
+@pytest.mark.parametrize("fraction", [4, 3, 2])
+def test_c4_matmul_chain_quarter_capacity(scenarios, oracle_out, fraction):
+    """The reference stalls here at ws/4 (first-fit fragmentation); the stream-ordered
+    pool with Belady eviction over the lookahead must complete it exactly."""
+    sc = scenarios["matmul"]
+    ws = max_device_working_set(sc, 1, 1)
+    cap = ws // fraction
+    got, coherent, st = run_product(sc, 1, 1, device_capacity=cap, host_capacity=1 << 30)
+    assert coherent and st["evictions"] > 0
+    assert st["peak_device_bytes"] <= cap
+    assert S.compare(got, oracle_out("matmul"), 1e-6) == []
+
+
+def _stencil_bytes(sc, **kw):
+    got, coherent, _ = run_product(sc, 2, 2, **kw)
+    assert coherent
+    return {k: v.tobytes() for k, v in got.items()}
+
+
+def test_c7_seeded_schedules_are_byte_identical(scenarios, oracle_out):
+    sc = scenarios["stencil"]
+    base = _stencil_bytes(sc)
+    assert S.compare({k: np.frombuffer(v, np.float32) for k, v in base.items()},
+                     {k: v.ravel() for k, v in oracle_out("stencil").items()}, 1e-6) == []
+    for seed in range(1, 33):
+        assert _stencil_bytes(sc, schedule_seed=seed) == base, f"seed {seed} diverged"
+
+
+@pytest.mark.parametrize("streams", [1, 2, 4, 16])
+@pytest.mark.parametrize("graphs", [True, False])
+def test_c7_streams_and_graphs_are_byte_identical(scenarios, streams, graphs):
+    sc = scenarios["stencil"]
+    base = _stencil_bytes(sc)
+    old = os.environ.pop("MTB_NO_GRAPHS", None)
+    try:
+        if not graphs:
+            os.environ["MTB_NO_GRAPHS"] = "1"
+        assert _stencil_bytes(sc, streams_per_device=streams) == base
+        assert _stencil_bytes(sc, streams_per_device=streams, schedule_seed=1000 + streams) == base
+    finally:
+        os.environ.pop("MTB_NO_GRAPHS", None)
+        if old is not None:
+            os.environ["MTB_NO_GRAPHS"] = old
+
+
+def test_cli_seed_flag_randomises_and_matches(tmp_path, scenarios):
+    import json
+    import subprocess
+    import sys
+    path = tmp_path / "stencil.json"
+    path.write_text(json.dumps(scenarios["stencil"]))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "paper_2202_05549_b200", "run", str(path), "--oracle", "--seed", "7"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "oracle: PASS" in r.stdout or "PASS" in r.stdout
