@@ -171,9 +171,36 @@ def sample_rows(want: int, devices: int, block: int = 16) -> int:
     return per * max(1, round(want / per))
 
 
-def cpu_reference_rate(rows, cols, iters, devices, bounds_check=True) -> tuple[float, float]:
-    """Reference CPU executor (oracle/_ref) on a rows x cols sample: (cell-updates/s, seconds).
-    bounds_check: the reference's array_view index checks (memory.hpp:54, default on)."""
+def host_cpu() -> dict:
+    """the CPU model and thread counts the CPU baselines ran on"""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        affinity = len(os.sched_getaffinity(0))
+    except AttributeError:
+        affinity = os.cpu_count()
+    return {"model": model, "nproc": affinity, "cpu_count": os.cpu_count()}
+
+
+# One sampling protocol for the heat2d CPU baseline, shared by the main arm's cpu_baseline and
+# `--impl reference`: a CPU_ROWS-row band of the full-width grid, one chunk (and device thread)
+# per host thread, CPU_WARMUP untimed launches, then timed launches in the same context. The
+# reference pipelines consecutive launches across chunks (SURVEY A.4), so its rate climbs over
+# the first few launches; timing after the warm-up gives the steady-state rate either arm sees.
+CPU_ROWS, CPU_WARMUP, CPU_ITERS = 512, 3, 20
+
+
+def cpu_reference_rate(rows, cols, iters, devices, bounds_check=True, warmup=CPU_WARMUP) -> tuple[float, float]:
+    """Reference CPU executor (oracle/_ref) on a rows x cols sample: (cell-updates/s, seconds of
+    the timed launches). bounds_check: the reference's array_view index checks (memory.hpp:54,
+    default on)."""
     import oracle
     from paper_2202_05549_b200 import Arr
     ref = oracle.reference()
@@ -184,13 +211,18 @@ def cpu_reference_rate(rows, cols, iters, devices, bounds_check=True) -> tuple[f
         raise RuntimeError("reference build lacks mr_set_bounds_check")
     ctx = oracle.reference_context(workers=1, devices=devices, execute=True)
     a, b, work = setup_heat(ctx, rows, cols, devices)
-    ctx.synchronize()
+
+    def run(n):
+        nonlocal a, b
+        for _ in range(n):
+            ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN)
+            ctx.flush()
+            a, b = b, a
+        ctx.synchronize()
+
+    run(warmup)
     t0 = time.perf_counter()
-    for _ in range(iters):
-        ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN)
-        ctx.flush()
-        a, b = b, a
-    ctx.synchronize()
+    run(iters)
     dt = time.perf_counter() - t0
     ctx.close()
     if toggle is not None:
@@ -198,21 +230,121 @@ def cpu_reference_rate(rows, cols, iters, devices, bounds_check=True) -> tuple[f
     return rows * cols * iters / dt, dt
 
 
-def bf16_ramp_row(i, n, mod):
-    """host restatement of ramp2d_bf16 for row i (f32 ramp, round-to-nearest-even to bf16)"""
-    import numpy as np
-    j = np.arange(n, dtype=np.int64)
-    v = (((i * 31 + j * 17 + 7) % mod).astype(np.float64) / mod).astype(np.float32)
-    u = v.view(np.uint32).astype(np.uint64)
-    u = ((u + (((u >> 16) & 1) + 0x7FFF)) >> 16) << 16
-    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+def cpu_heat_baseline(cols, iters=CPU_ITERS, bounds_off=True) -> dict:
+    """the heat2d CPU baseline under the shared protocol, plus its sensitivity to the sample
+    height (half the rows)"""
+    import oracle
+    threads = oracle.reference().host_threads()
+    devices = max(1, min(threads, 64))
+    rows = sample_rows(CPU_ROWS, devices)
+    rate, dt = cpu_reference_rate(rows, cols, iters, devices)
+    half = sample_rows(CPU_ROWS // 2, devices)
+    rate_half, _ = cpu_reference_rate(half, cols, iters, devices)
+    out = {"value": rate, "unit": "cell-updates/s", "cores": devices, "kind": "reference",
+           "sample": f"{rows}x{cols} band of the grid, {devices} chunks (stencil_dist halo [1,0]), 1 worker x {devices} device threads, "
+                     f"{CPU_WARMUP} warm-up + {iters} timed launches ({dt:.1f} s)",
+           "bounds_check": "on (the reference default, memory.hpp:54)", "host": host_cpu(),
+           "sensitivity": {"rows": half, "value": rate_half, "ratio": rate_half / rate}}
+    if bounds_off:
+        try:
+            rate_off, dt_off = cpu_reference_rate(rows, cols, iters, devices, bounds_check=False)
+            out["bounds_check_off"] = {"value": rate_off, "seconds": dt_off}
+        except Exception as e:  # noqa: BLE001
+            out["bounds_check_off"] = {"unavailable": str(e)}
+    return out
 
 
-def f32_ramp_row(i, n, mod):
-    """host restatement of ramp2d_f32 for row i"""
+def cpu_matmul_baseline(sizes=(1024, 2048)) -> dict:
+    """the reference `matmul` kernel (kernels.cpp:167-193: scalar f32 dot in l order) on the
+    reference CPU executor with every host thread: A and C row blocks, B replicated (the
+    replicated-input form of C3), inputs the C3 ramp patterns; FLOP/s = 2 n^3 / launch time.
+    At the smallest size every element is checked against an fp64 product of the same inputs."""
     import numpy as np
-    j = np.arange(n, dtype=np.int64)
-    return (((i * 31 + j * 17 + 7) % mod).astype(np.float64) / mod).astype(np.float32).astype(np.float64)
+
+    import oracle
+    from paper_2202_05549_b200 import Arr
+    threads = oracle.reference().host_threads()
+    dv = max(1, min(threads, 64))
+    runs = []
+    for n in sizes:
+        ctx = oracle.reference_context(workers=1, devices=dv, execute=True)
+        devs = ctx.devices
+        per = (n + dv - 1) // dv
+        per = (per + 15) // 16 * 16
+        A = ctx.create_array([n, n], "f32", ctx.dist.row([n, n], per, devs), 0)
+        B = ctx.create_array([n, n], "f32", ctx.dist.replicated([n, n], devs), 0)
+        Cm = ctx.create_array([n, n], "f32", ctx.dist.row([n, n], per, devs), 0)
+        w = ctx.dist.block_work([n, n], [16, 16], [per, n], devs)
+        ctx.launch("ramp2d_f32", [n, n], [16, 16], w, [n, n, 1000, 0.0, 1.0, Arr(A)], "global [i, j] => write out[i,j]")
+        ctx.launch("ramp2d_f32", [n, n], [16, 16], ctx.dist.block_work([n, n], [16, 16], [n, n], devs[:1]), [n, n, 997, 0.0, 1.0, Arr(B)],
+                   "global [i, j] => write out[i,j]")
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        ctx.launch("matmul", [n, n], [16, 16], w, [n, n, n, Arr(Cm), Arr(A), Arr(B)], "global [i, j] => write C[i,j], read A[i,:], read B[:,j]")
+        ctx.synchronize()
+        dt = time.perf_counter() - t0
+        r = {"n": n, "value": 2.0 * n ** 3 / dt / 1e12, "seconds": dt}
+        if n == min(sizes):
+            c = ctx.read(Cm).astype(np.float64)
+            want = ctx.read(A).astype(np.float64) @ ctx.read(B).astype(np.float64)
+            r["max_rel_err_vs_fp64_all_elements"] = float(np.max(np.abs(c - want) / np.abs(want)))
+        ctx.close()
+        runs.append(r)
+    best = max(runs, key=lambda r: r["value"])
+    return {"value": best["value"], "unit": "TFLOP/s", "cores": dv, "kind": "reference",
+            "sample": "reference `matmul` kernel (f32, kernels.cpp:167-193) at " + ", ".join(f"{r['n']}^3 ({r['seconds']:.1f} s)" for r in runs)
+                      + f", 1 worker x {dv} device threads; value = the faster size",
+            "sizes": runs, "host": host_cpu()}
+
+
+def cpu_ooc_baseline(rows=2048, cols=8192, iters=4) -> dict:
+    """the reference's out-of-core path (memory.cpp:245-377) at a reduced size: heat2d over two
+    rows x cols f32 arrays in chunk_rows-row chunks, with every device's capacity a quarter of its
+    working set (acceptance c4's squeeze), all host threads; cell-updates/s over timed launches
+    after one warm-up launch, and the reference's own eviction counts"""
+    import json as _json
+
+    import oracle
+    from paper_2202_05549_b200 import Arr
+    threads = oracle.reference().host_threads()
+    dv = max(1, min(threads, 64))
+    # eight chunks per device: one task's footprint (its input chunk with halo rows plus its
+    # output chunk) must fit the quarter capacity, which the reference checks (memory.cpp:278-287)
+    chunk_rows = max(16, rows // (8 * dv) // 16 * 16)
+    dv = max(1, min(dv, rows // chunk_rows // 8))
+    per_dev_ws = 2 * rows * cols * 4 // dv
+    cap = per_dev_ws // 4
+    ctx = oracle.reference_context(workers=1, devices=dv, execute=True, device_capacity=cap, host_capacity=4 * 2 * rows * cols * 4)
+    devs = ctx.devices
+    dist = lambda: ctx.dist.stencil([rows, cols], [chunk_rows, cols], [1, 0], devs)  # noqa: E731
+    a = ctx.create_array([rows, cols], "f32", dist(), 0)
+    b = ctx.create_array([rows, cols], "f32", dist(), 0)
+    work = ctx.dist.block_work([rows, cols], [16, 16], [chunk_rows, cols], devs)
+    ctx.launch("ramp2d_f32", [rows, cols], [16, 16], work, [rows, cols, 1000, 0.0, 1.0, Arr(a)], "global [i, j] => write out[i,j]")
+    ctx.synchronize()
+
+    def run(n):
+        nonlocal a, b
+        for _ in range(n):
+            ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN)
+            ctx.flush()
+            a, b = b, a
+        ctx.synchronize()
+
+    run(1)
+    t0 = time.perf_counter()
+    run(iters)
+    dt = time.perf_counter() - t0
+    try:
+        rep = _json.loads(ctx.report_json())
+        evictions = sum(int(w.get("evictions", 0)) for w in rep.get("workers", []))
+    except Exception:  # noqa: BLE001
+        evictions = None
+    ctx.close()
+    return {"value": rows * cols * iters / dt, "unit": "cell-updates/s", "cores": dv, "kind": "reference",
+            "sample": f"heat2d {rows}x{cols} f32 x2 arrays, {chunk_rows}-row chunks over {dv} devices, device capacity "
+                      f"{cap} B = 1/4 of each device's working set (acceptance c4), 1 warm-up + {iters} timed launches ({dt:.1f} s)",
+            "evictions": evictions, "host": host_cpu()}
 
 
 def run_contraction(ctx, n, steps, warmup, kind="bf16"):
@@ -230,7 +362,6 @@ def run_contraction(ctx, n, steps, warmup, kind="bf16"):
     ctx.launch(f"ramp2d_{et}", [n, n], [16, 16], w, [n, n, 1000, 0.0, 1.0, Arr(A)], "global [i, j] => write out[i,j]")
     ctx.launch(f"ramp2d_{et}", [n, n], [16, 16], w, [n, n, 997, 0.0, 1.0, Arr(B)], "global [i, j] => write out[i,j]")
     ann = "global [i, j] => write C[i,j], read A[i,:], read Bt[j,:]"
-    host_row = bf16_ramp_row if kind == "bf16" else f32_ramp_row
 
     def step():
         ctx.launch(kernel, [n, n], [16, 16], w, [n, n, n, Arr(Cm), Arr(A), Arr(B)], ann)
@@ -249,24 +380,72 @@ def run_contraction(ctx, n, steps, warmup, kind="bf16"):
     ctx.synchronize()
     ctx.profile_kernels(False)
     k1, ms1 = ctx.kernel_time(kernel)
-    # spot check 16 elements against an fp64 host dot product of the same inputs
-    import numpy as np
-    c = ctx.read(Cm)
-    rng = np.random.default_rng(0)
-    worst = 0.0
-    for _ in range(16):
-        i, j = int(rng.integers(n)), int(rng.integers(n))
-        want = float(host_row(i, n, 1000) @ host_row(j, n, 997))
-        worst = max(worst, abs(float(c[i, j]) - want) / max(abs(want), 1e-30))
-    del c
+    err = full_check(ctx, Cm, n, kind)
     for a in (A, B, Cm):
         ctx.delete_array(a)
     ctx.synchronize()
     flop = 2.0 * n ** 3
     kern_ms = (ms1 - ms0) / max(1, k1 - k0)
     return {"workload": f"{kernel} {n}^3 (C f32 = A {kind} x Bt^T {kind}), 1 superblock", "value": flop * steps / (elapsed / 1e3) / 1e12,
-            "unit": "TFLOP/s", "steps": steps, "ms_per_step": elapsed / steps, "kernel_ms": kern_ms,
-            "max_rel_err_16_samples_vs_fp64": worst}
+            "unit": "TFLOP/s", "steps": steps, "ms_per_step": elapsed / steps, "kernel_ms": kern_ms, "check": err}
+
+
+def full_check(ctx, Cm, n, kind):
+    """every element of C against an fp64 product (cuBLAS DGEMM, torch) of the same inputs,
+    generated on the device from the ramp formula (bf16: rounded to nearest-even bf16, as the
+    ramp2d_bf16 kernel stores them; tf32: the f32 values). Returns the max and mean relative
+    error (the mean exposes a systematic bias) over all n^2 elements."""
+    import torch
+    dev = torch.device("cuda")
+
+    def ramp(mod, off):
+        i = torch.arange(n, dtype=torch.int64, device=dev)
+        v = ((i[:, None] * 31 + i[None, :] * 17 + off) % mod).to(torch.float64) / mod
+        v = v.to(torch.float32)
+        if kind == "bf16":
+            v = v.to(torch.bfloat16)
+        return v.to(torch.float64)
+
+    try:
+        a = ramp(1000, 7)
+        b = ramp(997, 7)
+        want = a @ b.T
+        del a, b
+        got = torch.from_numpy(ctx.read(Cm)).to(dev)
+        rel = (got.to(torch.float64) - want) / want.abs().clamp_min(1e-30)
+        out = {"elements": n * n, "max_rel_err_vs_fp64": float(rel.abs().max()), "mean_rel_err_vs_fp64": float(rel.mean()),
+               "reference": "fp64 cuBLAS product of the same inputs on the device"}
+        del got, want, rel
+    except Exception as e:  # noqa: BLE001
+        out = {"unavailable": str(e)}
+    torch.cuda.empty_cache()
+    return out
+
+
+def cublas_tf32_peak(n=8192, reps=10):
+    """measured dense TF32 peak of this box: torch.matmul on f32 with TF32 allowed (cuBLAS),
+    best of `reps` back-to-back launches timed with CUDA events"""
+    import torch
+    a = torch.rand(n, n, device="cuda")
+    b = torch.rand(n, n, device="cuda")
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        for _ in range(3):
+            torch.matmul(a, b)
+        best = 0.0
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            e1.synchronize()
+            best = max(best, 2.0 * n ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+    del a, b
+    torch.cuda.empty_cache()
+    return best
 
 
 def _timed(ctx, kernel, fn, steps):
@@ -423,18 +602,20 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": f"reference CPU executor not loadable: {e}"}))
         return
     devices = max(1, min(threads, 64))
-    rows = sample_rows(args.ref_rows, devices)
+    rows = sample_rows(CPU_ROWS, devices)
     cols = args.cols
-    # warmup + timed: each step = one heat iteration over the sample
-    cpu_reference_rate(rows, cols, max(1, args.warmup), devices)
-    rate, dt = cpu_reference_rate(rows, cols, args.steps, devices)
-    sample = f"{rows}x{cols} rows sample of the {args.rows}x{args.cols} grid, {devices} chunks (stencil_dist halo [1,0]), 1 worker x {devices} device threads"
+    # the shared protocol (CPU_ROWS band, warm-up launches in the same context), each step one
+    # heat iteration over the band; the step count is capped so the arm ends within minutes
+    steps = max(1, min(args.steps, 60))
+    rate, dt = cpu_reference_rate(rows, cols, steps, devices, warmup=max(CPU_WARMUP, min(args.warmup, 10)))
+    sample = (f"{rows}x{cols} band of the {args.rows}x{args.cols} grid, {devices} chunks (stencil_dist halo [1,0]), 1 worker x {devices} "
+              f"device threads, {max(CPU_WARMUP, min(args.warmup, 10))} warm-up + {steps} timed launches")
     print(json.dumps({
-        "metric": METRIC, "impl": "reference", "value": rate, "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "metric": METRIC, "impl": "reference", "value": rate, "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (ramp2d_f32 pattern)",
         "config": {"workload": "heat2d 2D 5-point stencil f32, row-block stencil distribution", "rows": rows, "cols": cols, "iterations_per_step": 1},
-        "cpu_baseline": {"value": rate, "unit": "cell-updates/s", "cores": devices, "kind": "reference", "sample": sample},
+        "cpu_baseline": {"value": rate, "unit": "cell-updates/s", "cores": devices, "kind": "reference", "sample": sample, "host": host_cpu()},
         "e2e": {"value": rate, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -567,9 +748,9 @@ def run_c1(iters, ref_iters, hbm, cpu):
            "graph_replays": st.get("graph_replays")}
     if cpu:
         try:
-            rate, dt = cpu_reference_rate(rows, cols, ref_iters, 4)
+            rate, dt = cpu_reference_rate(rows, cols, ref_iters, 4, warmup=1)
             out["cpu_baseline"] = {"value": rate, "unit": "cell-updates/s", "cores": 4, "kind": "reference",
-                                   "sample": f"the same 4096^2 grid and 4 chunks (one device thread each), {ref_iters} iterations ({dt:.1f} s)"}
+                                   "sample": f"the same 4096^2 grid and 4 chunks (one device thread each), 1 warm-up + {ref_iters} timed iterations ({dt:.1f} s)"}
         except Exception as e:  # noqa: BLE001
             out["cpu_baseline"] = {"unavailable": str(e)}
     return out
@@ -756,19 +937,7 @@ def run_b200(args):
     cpu = None
     if rank == 0 and args.cpu_baseline:
         try:
-            import oracle
-            threads = oracle.reference().host_threads()
-            devices = max(1, min(threads, 64))
-            rrows = sample_rows(args.ref_rows, devices)
-            rate, dt = cpu_reference_rate(rrows, cols, args.ref_iters, devices)
-            cpu = {"value": rate, "unit": "cell-updates/s", "cores": devices, "kind": "reference",
-                   "sample": f"{rrows}x{cols} rows x {args.ref_iters} iterations ({dt:.1f} s), {devices} chunks, 1 worker x {devices} device threads",
-                   "bounds_check": "on (the reference default, memory.hpp:54)"}
-            try:
-                rate_off, dt_off = cpu_reference_rate(rrows, cols, args.ref_iters, devices, bounds_check=False)
-                cpu["bounds_check_off"] = {"value": rate_off, "seconds": dt_off}
-            except Exception as e:  # noqa: BLE001
-                cpu["bounds_check_off"] = {"unavailable": str(e)}
+            cpu = cpu_heat_baseline(cols)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "cell-updates/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
@@ -789,12 +958,20 @@ def run_b200(args):
         if args.tf32_steps > 0:
             t32 = run_contraction(ctx, args.matmul_n, args.tf32_steps, 1, "tf32")
             k32 = 2.0 * args.matmul_n ** 3 / (t32["kernel_ms"] / 1e3) / 1e12
-            # no measured TF32 peak on this pool: dense TF32 is half the bf16 rate (datasheet), so
-            # half the measured bf16 burst figure
-            t32["roofline"] = {"bound": "tensor", "achieved": k32, "peak": tburst / 2, "unit": "TFLOP/s", "frac": k32 / (tburst / 2),
-                               "peak_kind": "half the measured bf16 burst (TF32 = 1/2 bf16 dense rate)",
-                               "kernel": "gemm_bf16_nt_kernel<TF32> (tcgen05.mma kind::tf32 cta_group::1 M128 N256, TMA, TMEM)"}
+            try:
+                p32, p32_kind = cublas_tf32_peak(), "measured here: cuBLAS TF32 (torch.matmul f32, allow_tf32) 8192^3, best of 10"
+            except Exception as e:  # noqa: BLE001
+                p32, p32_kind = tburst / 2, f"half the measured bf16 burst (cuBLAS TF32 measurement failed: {e})"
+            t32["roofline"] = {"bound": "tensor", "achieved": k32, "peak": p32, "unit": "TFLOP/s", "frac": k32 / p32, "peak_kind": p32_kind,
+                               "frac_of_half_bf16_burst": k32 / (tburst / 2),
+                               "kernel": "tf32_rne rounding pass + gemm_bf16_nt_kernel<TF32> (tcgen05.mma kind::tf32 M128 N256, TMA, TMEM); "
+                                         "kernel_ms includes the rounding pass"}
             contraction["tf32"] = t32
+        if rank == 0 and args.cpu_baseline:
+            try:
+                contraction["cpu_baseline"] = cpu_matmul_baseline()
+            except Exception as e:  # noqa: BLE001
+                contraction["cpu_baseline"] = {"unavailable": str(e)}
     c1 = None
     if ws == 1 and args.c1:
         c1 = run_c1(100, args.c1_ref_iters, peaks()[0], rank == 0 and args.cpu_baseline)
@@ -844,6 +1021,11 @@ def run_b200(args):
             out["out_of_core"] = run_ooc(rows_ooc, cols, 4096, args.ooc_cap_gib, max(8.0, args.ooc_gib - args.ooc_cap_gib + 8.0), args.ooc_iters, 2)
         except Exception as e:  # noqa: BLE001
             out["out_of_core"] = {"unavailable": str(e)}
+        if args.cpu_baseline:
+            try:
+                out["out_of_core"]["cpu_baseline"] = cpu_ooc_baseline()
+            except Exception as e:  # noqa: BLE001
+                out["out_of_core"]["cpu_baseline"] = {"unavailable": str(e)}
     if rank == 0:
         print(json.dumps(out))
     if ws > 1:
@@ -862,8 +1044,6 @@ def main():
     p.add_argument("--e2e-runs", type=int, default=2)
     p.add_argument("--e2e-pipeline", type=int, default=40, help="pipelined e2e steps (0: report the sequential e2e)")
     p.add_argument("--e2e-sets", type=int, default=3, help="array sets the pipelined e2e steps rotate over")
-    p.add_argument("--ref-rows", type=int, default=512)
-    p.add_argument("--ref-iters", type=int, default=6)
     p.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     p.add_argument("--matmul-n", type=int, default=32768, help="C3 contraction size (0 to skip)")
     p.add_argument("--matmul-steps", type=int, default=5)
@@ -879,8 +1059,6 @@ def main():
     p.add_argument("--ooc-iters", type=int, default=12)
     args = p.parse_args()
     if args.impl == "reference":
-        if args.ref_rows == 512:
-            args.ref_rows = 128
         run_reference_arm(args)
     else:
         run_b200(args)

@@ -394,6 +394,15 @@ int mt_fuzz_scenario_json(uint64_t seed, char* buf, int64_t cap, int64_t* len);
  * scalar form; these are the C3 tensor-core forms. */
 int mt_gemm_bf16_nt(const void* a, const void* bt, float* c, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, void* stream);
 int mt_gemm_tf32_nt(const float* a, const float* bt, float* c, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, void* stream);
+/* tf32 operands are first rounded to nearest-even TF32 into stream-ordered scratch (so the
+ * contraction is unbiased; MTB_TF32_TRUNCATE=1 skips it, return 8 = scratch allocation failed).
+ * _nn: B is row-major K x N (pitch ldb), the layout of the reference's `matmul`
+ * (kernels.cpp:167-193), transposed to K-major in the same pass; the builtin `matmul` takes this
+ * path for superblocks with m*n*k >= 2^30 (MTB_MATMUL_EXACT=1: always the scalar kernel). */
+int mt_gemm_tf32_nn(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, void* stream);
+/* number of tcgen05 contraction launches issued by this process so far (evidence of which path
+ * a `matmul` launch took) */
+uint64_t mt_tensor_core_launches(void);
 
 #ifdef __cplusplus
 }

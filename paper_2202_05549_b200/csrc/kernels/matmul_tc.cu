@@ -26,6 +26,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "../executor.hpp"
@@ -557,6 +558,8 @@ bool make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, in
 	       == CUDA_SUCCESS;
 }
 
+std::atomic<uint64_t> g_tc_launches{0}; // tcgen05 contraction launches in this process (mt_tensor_core_launches)
+
 int num_sms() {
 	int dev = 0, sms = 148;
 	cudaGetDevice(&dev);
@@ -603,6 +606,7 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	const bool pair = p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && (!big || force_pair) && std::getenv("MTB_GEMM_NO_PAIR") == nullptr;
 	CUtensorMap ma, mb;
 	if(!make_map(&ma, a, a_rows, k, lda, BM, tf32) || !make_map(&mb, bt, b_rows, k, ldb, pair ? BN / 2 : BN, tf32)) return 7;
+	g_tc_launches.fetch_add(1, std::memory_order_relaxed);
 	if(!pair) {
 		const int grid = std::min(p.m_blocks * p.n_blocks, sms);
 		if(tf32) {
@@ -644,7 +648,126 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+// ---- TF32 operand preparation ----------------------------------------------------------------
+//
+// kind::tf32 reads only the top 19 bits of each f32 operand, i.e. it truncates the mantissa to
+// 10 bits; on same-signed data the truncation error is one-sided and a K-long dot product
+// inherits a bias of about -2^-11 (measured -7e-4 relative at 32768^3). The operands are
+// therefore rounded to nearest-even TF32 once per launch into packed scratch (K-major, row pitch
+// a multiple of 4 elements), so the MMA sees unbiased operands: 2 reads + 2 writes of the
+// operand bytes (about 2.6 ms at 32768^3 against a 110 ms contraction). The reference-id
+// `matmul` (B row-major, K x N) is transposed in the same pass.
+
+__device__ __forceinline__ float tf32_rne(float x) {
+	uint32_t u = __float_as_uint(x);
+	if((u & 0x7f800000u) == 0x7f800000u) return x; // inf / nan
+	u += 0xfffu + ((u >> 13) & 1u);
+	return __uint_as_float(u & 0xffffe000u);
+}
+
+// dst[r][c] = rne(src[r][c]) for r < rows, c < cols; gridDim.y walks rows
+__global__ void round_rows_tf32_k(const float* __restrict__ src, int64_t ld_src, float* __restrict__ dst, int64_t ld_dst, int64_t rows, int64_t cols) {
+	for(int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+		const float* sr = src + r * ld_src;
+		float* dr = dst + r * ld_dst;
+		for(int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < cols; c += static_cast<int64_t>(gridDim.x) * blockDim.x)
+			dr[c] = tf32_rne(__ldg(sr + c));
+	}
+}
+
+// dst[j][l] = rne(src[l][j]) (src: k x n row-major with pitch ld_src; dst: n x k, pitch ld_dst)
+__global__ void transpose_round_tf32_k(const float* __restrict__ src, int64_t ld_src, float* __restrict__ dst, int64_t ld_dst, int64_t k, int64_t n) {
+	__shared__ float tile[32][33];
+	const int64_t j0 = static_cast<int64_t>(blockIdx.x) * 32, l0 = static_cast<int64_t>(blockIdx.y) * 32;
+	for(int y = threadIdx.y; y < 32; y += blockDim.y) {
+		const int64_t l = l0 + y, j = j0 + threadIdx.x;
+		tile[y][threadIdx.x] = (l < k && j < n) ? tf32_rne(__ldg(src + l * ld_src + j)) : 0.0f;
+	}
+	__syncthreads();
+	for(int y = threadIdx.y; y < 32; y += blockDim.y) {
+		const int64_t j = j0 + y, l = l0 + threadIdx.x;
+		if(j < n && l < k) dst[j * ld_dst + l] = tile[threadIdx.x][y];
+	}
+}
+
+// scratch for prepared operands: stream-ordered allocations from the device's default pool,
+// which keeps up to 32 GiB cached between launches instead of returning it at every sync
+void* scratch_alloc(size_t bytes, cudaStream_t s) {
+	static bool raised[64] = {};
+	int dev = 0;
+	cudaGetDevice(&dev);
+	if(dev < 64 && !raised[dev]) {
+		cudaMemPool_t pool;
+		if(cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+			uint64_t thr = 32ull << 30;
+			cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+		}
+		raised[dev] = true;
+	}
+	void* p = nullptr;
+	if(cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
+	return p;
+}
+
+bool tf32_truncate() {
+	static const bool on = std::getenv("MTB_TF32_TRUNCATE") != nullptr;
+	return on;
+}
+
+int64_t pad4(int64_t k) { return (k + 3) / 4 * 4; }
+
+void round_rows(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t rows, int64_t cols, cudaStream_t s) {
+	const unsigned gx = static_cast<unsigned>(std::min<int64_t>((cols + 255) / 256, 64));
+	const unsigned gy = static_cast<unsigned>(std::min<int64_t>(rows, 65535));
+	round_rows_tf32_k<<<dim3(gx, gy), 256, 0, s>>>(src, ld_src, dst, ld_dst, rows, cols);
+}
+
+// C (rows r of A x cols of Bt) with both operands f32, rounded to TF32 first (unless
+// MTB_TF32_TRUNCATE); `b_kn` true: b is K x N row-major (the reference `matmul` layout)
+int run_gemm_tf32(const float* a, int64_t lda, const float* b, int64_t ldb, bool b_kn, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k,
+    cudaStream_t s) {
+	if(m <= 0 || n <= 0) return 0;
+	if(k <= 0) return 5;
+	if(tf32_truncate() && !b_kn) return run_gemm(a, m, lda, 0, b, n, ldb, 0, c, ldc, m, n, k, s, true);
+	const int64_t kp = pad4(k);
+	float* sa = static_cast<float*>(scratch_alloc(static_cast<size_t>((m + n) * kp) * 4, s));
+	if(!sa) return 8;
+	float* sb = sa + m * kp;
+	round_rows(a, lda, sa, kp, m, k, s);
+	if(b_kn) {
+		const dim3 grid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((k + 31) / 32));
+		transpose_round_tf32_k<<<grid, dim3(32, 8), 0, s>>>(b, ldb, sb, kp, k, n);
+	} else {
+		round_rows(b, ldb, sb, kp, n, k, s);
+	}
+	const int rc = run_gemm(sa, m, kp, 0, sb, n, kp, 0, c, ldc, m, n, k, s, true);
+	cudaFreeAsync(sa, s);
+	return rc;
+}
+
 } // namespace tc
+
+// the reference-id `matmul` (kernels.cpp:167-193: C = A x B, B row-major K x N) on the tensor
+// cores: A rows and B columns of the superblock are rounded to TF32 (B transposed to K-major)
+// and contracted by the tcgen05 kernel. Returns -1 when the views do not allow it (the caller
+// falls back to the scalar reference-order kernel).
+int matmul_tc_reference(const mt_launch_ctx* c, void* stream) {
+	const int64_t m = c->scalars_int[0], n = c->scalars_int[1], k = c->scalars_int[2];
+	const int64_t r0 = c->threads_lo[0], r1 = std::min(c->threads_hi[0], m);
+	const int64_t c0 = c->threads_lo[1], c1 = std::min(c->threads_hi[1], n);
+	if(r0 >= r1 || c0 >= c1) return 0;
+	const mt_view& vc = c->views[3];
+	const mt_view& va = c->views[4];
+	const mt_view& vb = c->views[5];
+	if(!vc.base || !va.base || !vb.base) return -1;
+	if(vc.stride[1] != 1 || va.stride[1] != 1 || vb.stride[1] != 1) return -1;
+	if(va.offset[1] > 0 || va.offset[1] + va.extent[1] < k || vb.offset[0] > 0 || vb.offset[0] + vb.extent[0] < k) return -1;
+	if(r0 < va.offset[0] || r1 > va.offset[0] + va.extent[0] || c0 < vb.offset[1] || c1 > vb.offset[1] + vb.extent[1]) return -1;
+	const float* a = static_cast<const float*>(va.base) + (r0 - va.offset[0]) * va.stride[0] - va.offset[1];
+	const float* b = static_cast<const float*>(vb.base) - vb.offset[0] * vb.stride[0] + (c0 - vb.offset[1]);
+	float* cp = static_cast<float*>(vc.base) + (r0 - vc.offset[0]) * vc.stride[0] + (c0 - vc.offset[1]);
+	return tc::run_gemm_tf32(a, va.stride[0], b, vb.stride[0], true, cp, vc.stride[0], r1 - r0, c1 - c0, k, static_cast<cudaStream_t>(stream));
+}
 
 static int launch_matmul_nt(const mt_launch_ctx* c, void* stream, bool tf32) {
 	const int64_t m = c->scalars_int[0], n = c->scalars_int[1], k = c->scalars_int[2];
@@ -657,6 +780,11 @@ static int launch_matmul_nt(const mt_launch_ctx* c, void* stream, bool tf32) {
 	if(!vc.base || !va.base || !vb.base) return 2;
 	if(va.offset[1] != 0 || vb.offset[1] != 0 || va.extent[1] < k || vb.extent[1] < k) return 3; // whole K rows staged
 	float* cp = static_cast<float*>(vc.base) + (r0 - vc.offset[0]) * vc.stride[0] + (c0 - vc.offset[1]) * vc.stride[1];
+	if(tf32) {
+		const float* a = static_cast<const float*>(va.base) + (r0 - va.offset[0]) * va.stride[0];
+		const float* b = static_cast<const float*>(vb.base) + (c0 - vb.offset[0]) * vb.stride[0];
+		return tc::run_gemm_tf32(a, va.stride[0], b, vb.stride[0], false, cp, vc.stride[0], r1 - r0, c1 - c0, k, static_cast<cudaStream_t>(stream));
+	}
 	return tc::run_gemm(va.base, va.extent[0], va.stride[0], r0 - va.offset[0], vb.base, vb.extent[0], vb.stride[0], c0 - vb.offset[0], cp, vc.stride[0],
 	    r1 - r0, c1 - c0, k, static_cast<cudaStream_t>(stream), tf32);
 }
@@ -684,5 +812,12 @@ extern "C" int mt_gemm_bf16_nt(const void* a, const void* bt, float* c, int64_t 
 }
 
 extern "C" int mt_gemm_tf32_nt(const float* a, const float* bt, float* c, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, void* stream) {
-	return mtb::tc::run_gemm(a, m, lda, 0, bt, n, ldb, 0, c, ldc, m, n, k, static_cast<cudaStream_t>(stream), true);
+	return mtb::tc::run_gemm_tf32(a, lda, bt, ldb, false, c, ldc, m, n, k, static_cast<cudaStream_t>(stream));
 }
+
+// C = A x B with B row-major (K x N): the reference `matmul` layout on the tensor cores
+extern "C" int mt_gemm_tf32_nn(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, void* stream) {
+	return mtb::tc::run_gemm_tf32(a, lda, b, ldb, true, c, ldc, m, n, k, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" uint64_t mt_tensor_core_launches(void) { return mtb::tc::g_tc_launches.load(); }
