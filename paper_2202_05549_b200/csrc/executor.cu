@@ -358,6 +358,11 @@ executor::~executor() {
 	// peers must have stopped writing into our mailbox (callers barrier before teardown)
 	for(void* p : opened_) cudaIpcCloseMemHandle(p);
 	if(mbox_) cudaFree(mbox_);
+	if(link_ctr_) cudaFree(link_ctr_);
+	for(auto& l : links_) {
+		if(l.tx) cudaStreamDestroy(l.tx);
+		if(l.rx) cudaStreamDestroy(l.rx);
+	}
 	for(auto& [id, b] : bufs_) {
 		cudaSetDevice(ord(b.gpu));
 		if(b.ptr) cudaFree(b.ptr); // pool memory: cudaFree is legal on stream-ordered allocations
@@ -1803,6 +1808,8 @@ void executor::peer_import(const std::vector<std::vector<uint8_t>>& blobs) {
 	if(static_cast<int>(blobs.size()) != world_) throw validation_error("one mailbox blob per worker expected");
 	check_cuda(cudaSetDevice(ord(0)), "cudaSetDevice");
 	links_.assign(static_cast<size_t>(world_), peer_link{});
+	check_cuda(cudaMalloc(&link_ctr_, sizeof(unsigned) * 2 * static_cast<size_t>(world_)), "cudaMalloc (link counters)");
+	check_cuda(cudaMemset(link_ctr_, 0, sizeof(unsigned) * 2 * static_cast<size_t>(world_)), "cudaMemset");
 	for(int p = 0; p < world_; ++p) {
 		mbox_blob b{};
 		if(blobs[static_cast<size_t>(p)].size() != sizeof(b)) throw validation_error("bad mailbox blob");
@@ -1821,32 +1828,175 @@ void executor::peer_import(const std::vector<std::vector<uint8_t>>& blobs) {
 		l.rx_ring = mbox_ + ring_off(p);
 		l.rx_ready = reinterpret_cast<uint64_t*>(mbox_ + flag_off(world_, p));
 		l.rx_consumed = reinterpret_cast<uint64_t*>(peer + cons_off(world_, my_rank_));
+		l.tx_done = link_ctr_ + 2 * p;
+		l.rx_done = link_ctr_ + 2 * p + 1;
+		check_cuda(cudaStreamCreateWithFlags(&l.tx, cudaStreamNonBlocking), "cudaStreamCreate");
+		check_cuda(cudaStreamCreateWithFlags(&l.rx, cudaStreamNonBlocking), "cudaStreamCreate");
 	}
+	check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+}
+
+// ---- fused single-segment path --------------------------------------------------------------
+//
+// A message that fits one ring slot (every halo row: 256 KiB at C2) moves with ONE kernel per
+// side instead of staging copies, allocations and separate flag kernels:
+//   send (peer tx stream): every CTA waits for the slot to be free (only from the kSlots-th
+//        message on), copies its rows of the region straight from the chunk into the peer's
+//        slot over NVLink (st.global to the IPC-mapped peer memory), fences at system scope;
+//        the last CTA to finish release-stores the slot's ready flag in the peer's memory.
+//   recv (peer rx stream): every CTA acquire-waits on the ready flag, copies its rows from the
+//        slot (ld.global.cg: the peer's stores landed in this GPU's L2) into the chunk; the
+//        last CTA release-stores the consumption counter back into the sender's memory.
+// Larger messages keep the segmented ring below (stage, per-segment wait / copy / flag).
+
+struct box_rows {
+	char* base;          // region start inside the chunk
+	int64_t rows;        // e0 * e1 (rank 3: planes x rows; rank 2: rows; rank 1: 1)
+	int64_t per_plane;   // e1
+	int64_t pitch_plane; // bytes between planes
+	int64_t pitch_row;   // bytes between rows
+	int64_t row_bytes;   // contiguous bytes per row
+};
+
+box_rows rows_of(void* chunk_ptr, const box& chunk, const box& region, size_t elem) {
+	const int r = region.rank();
+	int64_t ext[3] = {1, 1, 1}, cext[3] = {1, 1, 1}, off[3] = {0, 0, 0};
+	for(int k = 0; k < r; ++k) {
+		ext[3 - r + k] = region.extent(k);
+		cext[3 - r + k] = chunk.extent(k);
+		off[3 - r + k] = region.lo[k] - chunk.lo[k];
+	}
+	box_rows b{};
+	const int64_t e = static_cast<int64_t>(elem);
+	b.pitch_row = cext[2] * e;
+	b.pitch_plane = cext[1] * cext[2] * e;
+	b.base = static_cast<char*>(chunk_ptr) + off[0] * b.pitch_plane + off[1] * b.pitch_row + off[2] * e;
+	b.rows = ext[0] * ext[1];
+	b.per_plane = ext[1];
+	b.row_bytes = ext[2] * e;
+	return b;
+}
+
+__device__ __forceinline__ uint64_t now_ns() {
+	uint64_t t;
+	asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+	return t;
+}
+
+__device__ void wait_flag_geq(const uint64_t* flag, uint64_t value, uint64_t timeout_ns) {
+	const uint64_t t0 = now_ns();
+	for(;;) {
+		uint64_t v;
+		asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+		if(v >= value) return;
+		__nanosleep(32);
+		if(now_ns() - t0 > timeout_ns) {
+			printf("manta-b200: peer message wait timed out (flag %p: %llu < %llu)\n", flag, static_cast<unsigned long long>(v),
+			    static_cast<unsigned long long>(value));
+			__trap();
+		}
+	}
+}
+
+// packed message (row-major region) <-> rows of a chunk; `to_packed` chooses the direction
+template <typename V, bool CG>
+__device__ void move_rows(const box_rows& b, char* packed, bool to_packed) {
+	const int64_t per = b.row_bytes / static_cast<int64_t>(sizeof(V));
+	const int64_t total = per * b.rows;
+	for(int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+		const int64_t r = i / per, c = i - r * per;
+		V* chunk = reinterpret_cast<V*>(b.base + (r / b.per_plane) * b.pitch_plane + (r % b.per_plane) * b.pitch_row) + c;
+		V* msg = reinterpret_cast<V*>(packed + r * b.row_bytes) + c;
+		if(to_packed)
+			*msg = *chunk;
+		else if constexpr(CG)
+			*chunk = __ldcg(msg);
+		else
+			*chunk = *msg;
+	}
+}
+
+template <bool CG>
+__device__ void move_any(const box_rows& b, char* packed, bool to_packed) {
+	const uintptr_t a = reinterpret_cast<uintptr_t>(b.base) | reinterpret_cast<uintptr_t>(packed) | static_cast<uintptr_t>(b.row_bytes)
+	                    | static_cast<uintptr_t>(b.pitch_row) | static_cast<uintptr_t>(b.pitch_plane);
+	if(a % 16 == 0)
+		move_rows<uint4, CG>(b, packed, to_packed);
+	else if(a % 4 == 0)
+		move_rows<unsigned, CG>(b, packed, to_packed);
+	else
+		move_rows<unsigned char, false>(b, packed, to_packed);
+}
+
+// the last CTA through `done` (after a system-scope fence) release-stores `value` to `flag`
+__device__ void last_cta_release(unsigned* done, uint64_t* flag, uint64_t value) {
+	__syncthreads();
+	if(threadIdx.x == 0) {
+		__threadfence_system();
+		if(atomicAdd(done, 1u) == gridDim.x - 1) {
+			*done = 0; // the next message on this stream starts after this kernel
+			__threadfence_system();
+			asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+		}
+	}
+}
+
+__global__ void fused_send_k(box_rows src, char* slot, const uint64_t* consumed, uint64_t need, uint64_t* ready, uint64_t value, unsigned* done,
+    uint64_t timeout_ns) {
+	if(need) {
+		if(threadIdx.x == 0) wait_flag_geq(consumed, need, timeout_ns);
+		__syncthreads();
+	}
+	move_any<false>(src, slot, true);
+	last_cta_release(done, ready, value);
+}
+
+__global__ void fused_recv_k(box_rows dst, char* slot, const uint64_t* ready, uint64_t value, uint64_t* consumed, unsigned* done, uint64_t timeout_ns) {
+	if(threadIdx.x == 0) wait_flag_geq(ready, value, timeout_ns);
+	__syncthreads();
+	move_any<true>(dst, slot, false);
+	last_cta_release(done, consumed, value);
+}
+
+unsigned fused_grid(uint64_t bytes) {
+	return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(132, (bytes + 4095) / 4096)));
 }
 
 void executor::remote_send(const task& t) {
 	if(links_.empty()) throw execution_error("send to worker " + std::to_string(t.peer) + " in another process before peer_import");
 	const buffer& src = buf(t.chunk);
 	ldev& L = dev(t.resource);
-	cudaStream_t s = L.copy;
-	wait_deps(t, s);
 	auto& link = links_.at(static_cast<size_t>(t.peer));
+	cudaStream_t s = link.tx;
+	wait_deps(t, s);
 	auto& G = gpus_[static_cast<size_t>(L.gpu)];
 	const size_t elem = dtype_size(src.type);
 	const uint64_t bytes = static_cast<uint64_t>(t.region.volume()) * elem;
-	// contiguous staging of the region (one copy when it is already contiguous in the chunk)
-	void* stage = nullptr;
-	check_cuda(cudaMallocFromPoolAsync(&stage, bytes, G.pool, s), "cudaMallocFromPoolAsync");
-	copy_box(src.ptr, src.region, ord(src.gpu), stage, t.region, ord(L.gpu), t.region, elem, s);
-	for(uint64_t off = 0; off < bytes; off += kSlotBytes) {
-		const uint64_t seg = std::min<uint64_t>(kSlotBytes, bytes - off);
+	++ctr_.messages;
+	if(bytes <= kSlotBytes) {
 		const uint64_t q = link.tx_seq++;
 		const uint64_t slot = q % kSlots;
-		if(q >= static_cast<uint64_t>(kSlots)) spin_until_geq<<<1, 1, 0, s>>>(link.tx_consumed, q + 1 - kSlots, peer_timeout_ns());
-		check_cuda(cudaMemcpyAsync(link.tx_ring + slot * kSlotBytes, static_cast<char*>(stage) + off, seg, cudaMemcpyDefault, s), "cudaMemcpyAsync (send)");
-		release_store<<<1, 1, 0, s>>>(link.tx_ready + slot, q + 1);
+		const uint64_t need = q >= static_cast<uint64_t>(kSlots) ? q + 1 - kSlots : 0;
+		fused_send_k<<<fused_grid(bytes), 256, 0, s>>>(rows_of(src.ptr, src.region, t.region, elem), link.tx_ring + slot * kSlotBytes, link.tx_consumed,
+		    need, link.tx_ready + slot, q + 1, link.tx_done, peer_timeout_ns());
+		++ctr_.message_ops;
+	} else {
+		// contiguous staging of the region, then one ring segment at a time
+		void* stage = nullptr;
+		check_cuda(cudaMallocFromPoolAsync(&stage, bytes, G.pool, s), "cudaMallocFromPoolAsync");
+		copy_box(src.ptr, src.region, ord(src.gpu), stage, t.region, ord(L.gpu), t.region, elem, s);
+		ctr_.message_ops += 3;
+		for(uint64_t off = 0; off < bytes; off += kSlotBytes) {
+			const uint64_t seg = std::min<uint64_t>(kSlotBytes, bytes - off);
+			const uint64_t q = link.tx_seq++;
+			const uint64_t slot = q % kSlots;
+			if(q >= static_cast<uint64_t>(kSlots)) spin_until_geq<<<1, 1, 0, s>>>(link.tx_consumed, q + 1 - kSlots, peer_timeout_ns());
+			check_cuda(cudaMemcpyAsync(link.tx_ring + slot * kSlotBytes, static_cast<char*>(stage) + off, seg, cudaMemcpyDefault, s), "cudaMemcpyAsync (send)");
+			release_store<<<1, 1, 0, s>>>(link.tx_ready + slot, q + 1);
+			ctr_.message_ops += q >= static_cast<uint64_t>(kSlots) ? 3 : 2;
+		}
+		check_cuda(cudaFreeAsync(stage, s), "cudaFreeAsync");
 	}
-	check_cuda(cudaFreeAsync(stage, s), "cudaFreeAsync");
 	check_cuda(cudaGetLastError(), "send kernels");
 	ctr_.bytes_sent += bytes;
 	finish(t, s);
@@ -1856,24 +2006,36 @@ void executor::remote_recv(const task& t) {
 	if(links_.empty()) throw execution_error("receive from worker " + std::to_string(t.peer) + " in another process before peer_import");
 	const buffer& dst = buf(t.chunk);
 	ldev& L = dev(t.resource);
-	cudaStream_t s = L.recv;
-	wait_deps(t, s);
 	auto& link = links_.at(static_cast<size_t>(t.peer));
+	cudaStream_t s = link.rx;
+	wait_deps(t, s);
 	auto& G = gpus_[static_cast<size_t>(L.gpu)];
 	const size_t elem = dtype_size(dst.type);
 	const uint64_t bytes = static_cast<uint64_t>(t.region.volume()) * elem;
-	void* stage = nullptr;
-	check_cuda(cudaMallocFromPoolAsync(&stage, bytes, G.pool, s), "cudaMallocFromPoolAsync");
-	for(uint64_t off = 0; off < bytes; off += kSlotBytes) {
-		const uint64_t seg = std::min<uint64_t>(kSlotBytes, bytes - off);
+	++ctr_.messages;
+	if(bytes <= kSlotBytes) {
 		const uint64_t q = link.rx_seq++;
 		const uint64_t slot = q % kSlots;
-		spin_until_geq<<<1, 1, 0, s>>>(link.rx_ready + slot, q + 1, peer_timeout_ns());
-		check_cuda(cudaMemcpyAsync(static_cast<char*>(stage) + off, link.rx_ring + slot * kSlotBytes, seg, cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync (recv)");
-		release_store<<<1, 1, 0, s>>>(link.rx_consumed, q + 1);
+		fused_recv_k<<<fused_grid(bytes), 256, 0, s>>>(rows_of(dst.ptr, dst.region, t.region, elem), link.rx_ring + slot * kSlotBytes, link.rx_ready + slot,
+		    q + 1, link.rx_consumed, link.rx_done, peer_timeout_ns());
+		++ctr_.message_ops;
+	} else {
+		void* stage = nullptr;
+		check_cuda(cudaMallocFromPoolAsync(&stage, bytes, G.pool, s), "cudaMallocFromPoolAsync");
+		ctr_.message_ops += 1;
+		for(uint64_t off = 0; off < bytes; off += kSlotBytes) {
+			const uint64_t seg = std::min<uint64_t>(kSlotBytes, bytes - off);
+			const uint64_t q = link.rx_seq++;
+			const uint64_t slot = q % kSlots;
+			spin_until_geq<<<1, 1, 0, s>>>(link.rx_ready + slot, q + 1, peer_timeout_ns());
+			check_cuda(cudaMemcpyAsync(static_cast<char*>(stage) + off, link.rx_ring + slot * kSlotBytes, seg, cudaMemcpyDeviceToDevice, s), "cudaMemcpyAsync (recv)");
+			release_store<<<1, 1, 0, s>>>(link.rx_consumed, q + 1);
+			ctr_.message_ops += 3;
+		}
+		copy_box(stage, t.region, ord(L.gpu), dst.ptr, dst.region, ord(dst.gpu), t.region, elem, s);
+		check_cuda(cudaFreeAsync(stage, s), "cudaFreeAsync");
+		ctr_.message_ops += 2;
 	}
-	copy_box(stage, t.region, ord(L.gpu), dst.ptr, dst.region, ord(dst.gpu), t.region, elem, s);
-	check_cuda(cudaFreeAsync(stage, s), "cudaFreeAsync");
 	check_cuda(cudaGetLastError(), "recv kernels");
 	ctr_.bytes_received += bytes;
 	finish(t, s);

@@ -72,6 +72,8 @@ struct exec_counters {
 	uint64_t bytes_host_in = 0, bytes_host_out = 0; // host_write / host_read tasks
 	uint64_t graph_captures = 0, graph_replays = 0;  // CUDA-graph replay of repeated submissions
 	uint64_t bytes_host_to_disk = 0, bytes_disk_to_host = 0; // disk tier
+	uint64_t messages = 0;    // inter-process send + recv tasks
+	uint64_t message_ops = 0; // stream operations (kernels, copies, allocations) they enqueued
 };
 
 class executor {
@@ -161,7 +163,12 @@ class executor {
 		uint64_t* rx_ready = nullptr;         // its ready flags (my memory)
 		uint64_t* rx_consumed = nullptr;      // my consumption of its segments (peer memory)
 		uint64_t rx_seq = 0;
+		cudaStream_t tx = nullptr, rx = nullptr; // per-peer streams: a send waiting for ring space
+		                                         // never holds up other copies or other peers
+		unsigned* tx_done = nullptr;          // CTA completion counters of the fused kernels (my memory)
+		unsigned* rx_done = nullptr;
 	};
+	unsigned* link_ctr_ = nullptr;
 	char* mbox_ = nullptr;
 	int world_ = 0;
 	int my_rank_ = -1;

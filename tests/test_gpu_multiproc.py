@@ -22,7 +22,7 @@ def _port():
     return p
 
 
-def _heat_rank(rank, world, port, rows, cols, iters, q):
+def _heat_rank(rank, world, port, rows, cols, iters, q, halo=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -31,7 +31,7 @@ def _heat_rank(rank, world, port, rows, cols, iters, q):
     ctx = mb.context(workers=world, devices=1, worker_rank=rank, gpu_base=0)
     ctx.connect_peers()
     devs = ctx.devices
-    dist_ = lambda: ctx.dist.stencil([rows, cols], [rows // world, cols], [1, 0], devs)  # noqa: E731
+    dist_ = lambda: ctx.dist.stencil([rows, cols], [rows // world, cols], [halo, 0], devs)  # noqa: E731
     a = ctx.create_array([rows, cols], "f32", dist_(), 0)
     b = ctx.create_array([rows, cols], "f32", dist_(), 0)
     work = ctx.dist.block_work([rows, cols], [16, 16], [rows // world, cols], devs)
@@ -50,14 +50,14 @@ def _heat_rank(rank, world, port, rows, cols, iters, q):
     dist.destroy_process_group()
 
 
-def test_two_process_heat_matches_single_process():
+def _two_process_heat(rows, cols, iters, halo=1):
     import paper_2202_05549_b200 as mb
     from paper_2202_05549_b200 import Arr
-    rows, cols, iters, world = 256, 512, 4, 2
+    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_heat_rank, args=(r, world, port, rows, cols, iters, q)) for r in range(world)]
+    procs = [ctx.Process(target=_heat_rank, args=(r, world, port, rows, cols, iters, q, halo)) for r in range(world)]
     for p in procs:
         p.start()
     parts = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
@@ -68,8 +68,8 @@ def test_two_process_heat_matches_single_process():
     assert all(p[2]["bytes_sent"] > 0 for p in parts)
     with mb.context(workers=1, devices=world, num_gpus=1) as c:
         devs = c.devices
-        a = c.create_array([rows, cols], "f32", c.dist.stencil([rows, cols], [rows // world, cols], [1, 0], devs), 0)
-        b = c.create_array([rows, cols], "f32", c.dist.stencil([rows, cols], [rows // world, cols], [1, 0], devs), 0)
+        a = c.create_array([rows, cols], "f32", c.dist.stencil([rows, cols], [rows // world, cols], [halo, 0], devs), 0)
+        b = c.create_array([rows, cols], "f32", c.dist.stencil([rows, cols], [rows // world, cols], [halo, 0], devs), 0)
         w = c.dist.block_work([rows, cols], [16, 16], [rows // world, cols], devs)
         c.launch("ramp2d_f32", [rows, cols], [16, 16], w, [rows, cols, 1000, 0.0, 1.0, Arr(a)], "global [i, j] => write out[i,j]")
         for _ in range(iters):
@@ -77,6 +77,25 @@ def test_two_process_heat_matches_single_process():
             a, b = b, a
         want = c.read(a)
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    return [p[2] for p in parts]
+
+
+def test_two_process_heat_matches_single_process():
+    """10 iterations: each rank sends and receives one halo row per iteration, so the 4-slot ring
+    wraps twice; every message is one fused kernel per side (exec_stats message_ops)"""
+    stats = _two_process_heat(256, 512, 10)
+    for st in stats:
+        assert st["messages"] == 22  # (ramp + 10 iterations) x (1 send + 1 receive) per rank
+        assert st["message_ops"] == st["messages"]
+
+
+def test_two_process_heat_large_halo_segments():
+    """halo [8, 0] rows of 600000 f32 = 19.2 MB per message: larger than one 16 MiB ring slot, so
+    the segmented path (stage, per-segment wait / copy / flag) moves them"""
+    stats = _two_process_heat(64, 600000, 3, halo=8)
+    for st in stats:
+        assert st["messages"] == 8  # (ramp + 3 iterations) x (1 send + 1 receive)
+        assert st["message_ops"] > st["messages"]
 
 
 def _hist_rank(rank, world, port, n, bins, q):
