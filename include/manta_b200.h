@@ -169,7 +169,10 @@ typedef struct mt_config {
 	                                   (one process per GPU; every rank plans the full plan) */
 	uint64_t device_capacity;       /* bytes per device the chunk store may use (0 = 90% of free HBM) */
 	uint64_t host_capacity;         /* pinned-host spill tier bytes (0 = no spill tier)  */
-	uint64_t staging_threshold;     /* reference throttle; informational on the GPU path */
+	uint64_t staging_threshold;     /* staging throttle (memory.cpp:290-295): per device, the bytes of chunks in use by
+	                                   issued-but-unfinished tasks stay within it (the issuing thread waits for the
+	                                   oldest in-flight tasks); a task above it alone is an execution error;
+	                                   0 = off (no waiting, graph replay allowed) */
 	int32_t record_accesses;        /* keep (task, chunk, region, write) records for mt_plan_accesses */
 	int32_t lookahead_tasks;        /* spill tier: tasks buffered ahead for Belady eviction (0 = 512) */
 	int32_t worker_rank;            /* with single_worker: the worker this process executes */

@@ -12,8 +12,10 @@ incoherent replicas, 3 internal error; manta.cpp:15-18, 166-178).
   (run_fuzz_campaign, scenario.cpp:809-846) on the GPU: the scenarios come from the product's
   restatement of make_fuzz_scenario (mt_fuzz_scenario_json), seed for seed the reference's.
 
-System flags follow add_system_flags (manta.cpp:46-54). On the GPU executor `--throttle` is
-informational, `--disk-capacity` sizes the spill file below the pinned-host tier, and
+System flags follow add_system_flags (manta.cpp:46-54). `--throttle` (default: the scenario's
+staging_threshold, 64 MiB) bounds the bytes of chunks in use by issued-but-unfinished tasks per
+device like the reference's staging throttle, with its monitor counted in the report
+(memory.cpp:290-295, 371-374); `--disk-capacity` sizes the spill file below the pinned-host tier, and
 `--seed` randomises the schedule like the reference's seeded ready-task choice
 (runtime.cpp:313-319): every task goes to a compute stream drawn from the seeded generator,
 behind a random on-device delay (mt_config.schedule_seed); without it tasks run as soon as
@@ -34,6 +36,7 @@ from . import scenario as S
 EXIT_PASS, EXIT_VALIDATION, EXIT_MISMATCH, EXIT_INTERNAL = 0, 1, 2, 3
 DEFAULT_DEVICE_CAPACITY = 256 << 20  # system_spec defaults (scenario.hpp:66-73)
 DEFAULT_HOST_CAPACITY = 1 << 30
+DEFAULT_STAGING_THRESHOLD = 64 << 20  # system_spec::staging_threshold (scenario.hpp:72)
 KINDS = ("create", "delete", "execute", "copy", "send", "recv", "reduce")
 GOLDEN = 0x9E3779B97F4A7C15
 M64 = (1 << 64) - 1
@@ -111,7 +114,7 @@ def make_context(sysd: dict, execute: bool, oracle_mode=False, suppress=False, s
     disk = int(sysd.get("disk_capacity", 0)) if spill else 0
     return context(workers=workers, devices=devices, execute=execute, num_gpus=1 if execute else 0, suppress_conflict_deps=suppress, compat_deps=compat,
                    streams_per_device=streams, device_capacity=cap if spill else 0, host_capacity=max(host, cap) if spill else 0,
-                   staging_threshold=int(sysd.get("staging_threshold", 0)), disk_capacity=disk,
+                   staging_threshold=0 if oracle_mode else int(sysd.get("staging_threshold", DEFAULT_STAGING_THRESHOLD)), disk_capacity=disk,
                    schedule_seed=0 if oracle_mode else int(sysd.get("ready_seed", 0) or 0))
 
 
@@ -299,7 +302,7 @@ def _system_flags(p: argparse.ArgumentParser):
     p.add_argument("--device-capacity", dest="device_capacity", type=int, help="Device memory capacity in bytes")
     p.add_argument("--host-capacity", dest="host_capacity", type=int, help="Host memory capacity in bytes")
     p.add_argument("--disk-capacity", dest="disk_capacity", type=int, help="Disk tier capacity in bytes")
-    p.add_argument("--throttle", type=int, help="Staging throttle threshold in bytes (informational)")
+    p.add_argument("--throttle", type=int, help="Staging throttle threshold in bytes")
     p.add_argument("--seed", type=int, help="Randomise the schedule: seeded stream choice and on-device delays per task")
     p.add_argument("--streams", type=int, default=0, help="Compute streams per device (0 = 4)")
     p.add_argument("--no-conflict-deps", dest="no_conflict_deps", action="store_true", help=argparse.SUPPRESS)

@@ -231,6 +231,7 @@ executor_config exec_cfg(const mt_config& c) {
 	e.disk_capacity = c.disk_capacity;
 	if(c.spill_dir) e.spill_dir = c.spill_dir;
 	e.schedule_seed = c.schedule_seed;
+	e.staging_threshold = c.staging_threshold;
 	if(c.single_worker) {
 		// one process per worker: this process executes worker_rank only, on GPU ordinal
 		// gpu_base (+ device index); every rank plans the identical full plan

@@ -82,6 +82,25 @@ __device__ __forceinline__ double mul_wrap(double a, double b) {
 struct bf16_t {
 	uint16_t bits;
 };
+// bf16 reduce (a B200 extension: the reference has no bf16): every combine is computed in f32
+// and rounded to nearest-even bf16; min/max compare the values (NaN compares false, as
+// std::min/max would)
+__device__ __forceinline__ float bf_to_f(bf16_t b) { return __uint_as_float(static_cast<uint32_t>(b.bits) << 16); }
+__device__ __forceinline__ bf16_t f_to_bf(float f) {
+	uint32_t u = __float_as_uint(f);
+	if((u & 0x7fffffffu) > 0x7f800000u) return bf16_t{static_cast<uint16_t>((u >> 16) | 0x40u)}; // quiet NaN
+	u += 0x7fffu + ((u >> 16) & 1u);
+	return bf16_t{static_cast<uint16_t>(u >> 16)};
+}
+__device__ __forceinline__ bool operator<(bf16_t a, bf16_t b) { return bf_to_f(a) < bf_to_f(b); }
+template <>
+__device__ __forceinline__ bf16_t add_wrap(bf16_t a, bf16_t b) {
+	return f_to_bf(__fadd_rn(bf_to_f(a), bf_to_f(b)));
+}
+template <>
+__device__ __forceinline__ bf16_t mul_wrap(bf16_t a, bf16_t b) {
+	return f_to_bf(__fmul_rn(bf_to_f(a), bf_to_f(b)));
+}
 
 template <typename T>
 __global__ void fill_kernel(T* p, uint64_t n, T v) {
@@ -200,7 +219,7 @@ void device_reduce(void* out, const void* const* inputs, int n, uint64_t count, 
 	case dtype::i64: reduce_typed<int64_t>(out, inputs, n, count, op, s); break;
 	case dtype::f32: reduce_typed<float>(out, inputs, n, count, op, s); break;
 	case dtype::f64: reduce_typed<double>(out, inputs, n, count, op, s); break;
-	case dtype::bf16: throw execution_error("bf16 reduce tasks are not supported");
+	case dtype::bf16: reduce_typed<bf16_t>(out, inputs, n, count, op, s); break;
 	}
 	check_cuda(cudaGetLastError(), "reduce kernel launch");
 }
@@ -331,6 +350,11 @@ executor::executor(const executor_config& cfg) : cfg_(cfg), rng_state_(cfg.sched
 	const int nw = cfg.workers, nd = cfg.devices_per_worker;
 	const int k = cfg.streams_per_device > 0 ? cfg.streams_per_device : 4;
 	ldevs_.resize(static_cast<size_t>(nw * nd));
+	wctr_.assign(static_cast<size_t>(nw), worker_counters{});
+	dev_used_.assign(static_cast<size_t>(nw * nd), 0);
+	dev_peak_.assign(static_cast<size_t>(nw * nd), 0);
+	pins_.assign(static_cast<size_t>(nw * nd), {});
+	pinned_bytes_.assign(static_cast<size_t>(nw * nd), 0);
 	for(int w = 0; w < nw; ++w) {
 		const bool local = cfg.local_workers < 0 || (w >= cfg.first_worker && w < cfg.first_worker + cfg.local_workers);
 		for(int d = 0; d < nd; ++d) {
@@ -604,7 +628,7 @@ void executor::issue_batch() {
 }
 
 bool executor::graph_eligible(const std::vector<task>& b, int* gpu) const {
-	if(spill_ || trace_ || profile_ || cfg_.schedule_seed) return false;
+	if(spill_ || trace_ || profile_ || cfg_.schedule_seed || cfg_.staging_threshold) return false;
 	// Only submissions whose GPU work is short enough that issuing them costs as much as running
 	// them: consecutive replays run back to back on one stream, which gives up the overlap
 	// between submissions that the multi-stream path keeps for large superblocks.
@@ -797,8 +821,96 @@ void executor::drain(bool all) {
 	}
 }
 
+void executor::charge(const buffer& b, uint64_t bytes, bool add) {
+	auto& G = gpus_[static_cast<size_t>(b.gpu)];
+	const size_t d = static_cast<size_t>(b.home.worker * cfg_.devices_per_worker + b.home.device);
+	if(add) {
+		G.used += bytes;
+		ctr_.peak_device_bytes = std::max(ctr_.peak_device_bytes, G.used);
+		dev_used_[d] += bytes;
+		dev_peak_[d] = std::max(dev_peak_[d], dev_used_[d]);
+	} else {
+		G.used -= bytes;
+		dev_used_[d] -= bytes;
+	}
+}
+
+// Staging throttle (memory.cpp:290-295) and its safety monitor (memory.cpp:371-374). The
+// reference stages a task only if the union of chunks pinned by staged-but-unfinished tasks on
+// its resource stays within the threshold; here "staged" is "issued to a stream and not yet
+// complete", and a task that would exceed it waits on the host for the oldest in-flight tasks.
+// A single task whose chunks alone exceed the threshold is the reference's fatal error
+// (memory.cpp:278-281). The monitor counts one check per admitted task and a violation for
+// every device over the threshold at that moment (by construction none).
+void executor::throttle(const task& t) {
+	const uint64_t thr = cfg_.staging_threshold;
+	std::vector<std::pair<int64_t, bool>> uses;
+	used_chunks(t, uses);
+	staged_task st{t.id, static_cast<size_t>(t.resource.worker * cfg_.devices_per_worker + t.resource.device), {}};
+	const auto add = [&](int64_t c, uint64_t bytes) {
+		for(const auto& x : st.chunks)
+			if(x.first == c) return;
+		st.chunks.emplace_back(c, bytes);
+	};
+	if(t.kind == task_kind::create) add(t.chunk, static_cast<uint64_t>(t.region.volume()) * dtype_size(t.type));
+	for(const auto& [c, w] : uses) {
+		const auto it = bufs_.find(c);
+		if(it != bufs_.end()) add(c, it->second.bytes);
+	}
+	uint64_t footprint = 0;
+	for(const auto& x : st.chunks) footprint += x.second;
+	if(footprint > thr)
+		throw execution_error("task " + std::to_string(t.id) + " footprint " + std::to_string(footprint) + " exceeds the staging threshold " + std::to_string(thr));
+	auto& pins = pins_[st.dev];
+	const auto fresh = [&] {
+		uint64_t n = 0;
+		for(const auto& [c, b] : st.chunks)
+			if(!pins.count(c)) n += b;
+		return n;
+	};
+	const auto complete = [&](int64_t id) {
+		const auto it = done_.find(id);
+		return it == done_.end() || cudaEventQuery(it->second.ev) == cudaSuccess;
+	};
+	while(!staged_.empty() && complete(staged_.front().id)) {
+		unpin(staged_.front());
+		staged_.pop_front();
+	}
+	while(pinned_bytes_[st.dev] + fresh() > thr && !staged_.empty()) {
+		const auto it = done_.find(staged_.front().id);
+		if(it != done_.end()) check_cuda(cudaEventSynchronize(it->second.ev), "cudaEventSynchronize (staging throttle)");
+		unpin(staged_.front());
+		staged_.pop_front();
+		while(!staged_.empty() && complete(staged_.front().id)) {
+			unpin(staged_.front());
+			staged_.pop_front();
+		}
+	}
+	cudaGetLastError();
+	for(const auto& [c, b] : st.chunks)
+		if(pins[c]++ == 0) pinned_bytes_[st.dev] += b;
+	auto& w = wc(t.resource.worker);
+	++w.staging_checks;
+	for(const auto bytes : pinned_bytes_)
+		if(bytes > thr) ++w.staging_violations;
+	staged_.push_back(std::move(st));
+}
+
+void executor::unpin(const staged_task& st) {
+	auto& pins = pins_[st.dev];
+	for(const auto& [c, b] : st.chunks) {
+		const auto it = pins.find(c);
+		if(it == pins.end()) continue;
+		if(--it->second == 0) {
+			pins.erase(it);
+			pinned_bytes_[st.dev] -= b;
+		}
+	}
+}
+
 void executor::issue(const task& t) {
 	nvtx3::scoped_range_in<nvtx_domain> range{task_kind_name(t.kind)};
+	if(cfg_.staging_threshold && !remote_worker(t.resource.worker)) throttle(t);
 	if(spill_) stage(t);
 	switch(t.kind) {
 	case task_kind::create: run_create(t); break;
@@ -1071,6 +1183,7 @@ void executor::disk_read(const buffer& b, void* dst) {
 		done += static_cast<uint64_t>(r);
 	}
 	ctr_.bytes_disk_to_host += b.bytes;
+	wc(b.home.worker).bytes_disk_to_host += b.bytes;
 }
 
 // The host tier is full and holds only copies of evicted chunks: write the least recently used
@@ -1095,6 +1208,7 @@ void* executor::spill_host_to_disk(uint64_t bytes, int64_t exclude) {
 		}
 		b.disk_valid = true;
 		ctr_.bytes_host_to_disk += b.bytes;
+		wc(b.home.worker).bytes_host_to_disk += b.bytes;
 	}
 	void* blk = b.host;
 	b.host = nullptr;
@@ -1121,6 +1235,7 @@ void executor::evict(int64_t chunk) {
 		check_cuda(cudaMemcpyAsync(b.host, b.ptr, b.bytes, cudaMemcpyDeviceToHost, G.d2h), "cudaMemcpyAsync D2H (evict)");
 		b.host_valid = true;
 		ctr_.bytes_device_to_host += b.bytes;
+		wc(b.home.worker).bytes_device_to_host += b.bytes;
 	}
 	check_cuda(cudaFreeAsync(b.ptr, G.d2h), "cudaFreeAsync");
 	if(!b.evicted) check_cuda(cudaEventCreateWithFlags(&b.evicted, cudaEventDisableTiming), "cudaEventCreate");
@@ -1134,8 +1249,9 @@ void executor::evict(int64_t chunk) {
 	}
 	b.ptr = nullptr;
 	b.users.clear();
-	G.used -= b.bytes;
+	charge(b, b.bytes, false);
 	++ctr_.evictions;
+	++wc(b.home.worker).evictions;
 }
 
 void executor::ensure_room(int gpu, uint64_t bytes, const std::vector<int64_t>& pinned) {
@@ -1209,8 +1325,7 @@ void executor::restore(int64_t chunk, const std::vector<int64_t>& pinned, const 
 		    task_kind_name(current.kind), needed ? 1 : 0);
 	if(!needed) {
 		// contents are overwritten before they are read: allocate only
-		G.used += b.bytes;
-		ctr_.peak_device_bytes = std::max(ctr_.peak_device_bytes, G.used);
+		charge(b, b.bytes, true);
 		if(!b.restored) check_cuda(cudaEventCreateWithFlags(&b.restored, cudaEventDisableTiming), "cudaEventCreate");
 		check_cuda(cudaEventRecord(b.restored, G.h2d), "cudaEventRecord");
 		++ctr_.dead_skips;
@@ -1228,9 +1343,9 @@ void executor::restore(int64_t chunk, const std::vector<int64_t>& pinned, const 
 	check_cuda(cudaMemcpyAsync(b.ptr, b.host, b.bytes, cudaMemcpyHostToDevice, G.h2d), "cudaMemcpyAsync H2D (restore)");
 	if(!b.restored) check_cuda(cudaEventCreateWithFlags(&b.restored, cudaEventDisableTiming), "cudaEventCreate");
 	check_cuda(cudaEventRecord(b.restored, G.h2d), "cudaEventRecord");
-	G.used += b.bytes;
-	ctr_.peak_device_bytes = std::max(ctr_.peak_device_bytes, G.used);
+	charge(b, b.bytes, true);
 	ctr_.bytes_host_to_device += b.bytes;
+	wc(b.home.worker).bytes_host_to_device += b.bytes;
 }
 
 void executor::stage(const task& t) {
@@ -1290,11 +1405,10 @@ void executor::run_create(const task& t) {
 		                      + std::to_string(G.capacity));
 	void* p = nullptr;
 	check_cuda(cudaMallocFromPoolAsync(&p, bytes, G.pool, s), "cudaMallocFromPoolAsync");
-	G.used += bytes;
-	ctr_.peak_device_bytes = std::max(ctr_.peak_device_bytes, G.used);
 	device_fill(p, count, t.type, t.fill, t.fill_op, s);
 	++ctr_.kernels;
 	bufs_[t.chunk] = buffer{p, bytes, t.region, t.type, t.home, L.gpu};
+	charge(bufs_[t.chunk], bytes, true);
 	finish(t, s);
 }
 
@@ -1305,7 +1419,7 @@ void executor::run_delete(const task& t) {
 	wait_deps(t, s);
 	if(b.ptr) {
 		check_cuda(cudaFreeAsync(b.ptr, s), "cudaFreeAsync");
-		gpus_[static_cast<size_t>(b.gpu)].used -= b.bytes;
+		charge(b, b.bytes, false);
 	}
 	if(b.host) {
 		// the pinned block is reusable once every earlier use of the chunk is done
@@ -1416,6 +1530,7 @@ void executor::run_send(const task& t) {
 	if(mailbox_.count(key)) throw execution_error("duplicate message tag");
 	mailbox_[key] = m;
 	ctr_.bytes_sent += m.bytes;
+	wc(t.worker).bytes_sent += m.bytes;
 	finish(t, s);
 }
 
@@ -1447,6 +1562,7 @@ void executor::run_recv(const task& t) {
 	free_events_[static_cast<size_t>(m.gpu)].push_back(m.ready);
 	free_events_[static_cast<size_t>(L.gpu)].push_back(unpacked);
 	ctr_.bytes_received += m.bytes;
+	wc(t.worker).bytes_received += m.bytes;
 	finish(t, s);
 }
 
@@ -1548,6 +1664,7 @@ void executor::run_allreduce(const task& t) {
 		}
 		nccl_check(g_nccl.all_reduce(out.ptr, out.ptr, count, dt, op, static_cast<ncclComm_t>(nccl_comm_), s), "ncclAllReduce");
 		ctr_.bytes_sent += count * dtype_size(out.type);
+		wc(t.worker).bytes_sent += count * dtype_size(out.type);
 		finish(t, s);
 		return;
 	}
@@ -1674,6 +1791,8 @@ void executor::sync() {
 	for(auto& [id, d] : done_) release_done_event(d.ev, d.gpu);
 	done_.clear();
 	tail_.clear();
+	for(const auto& st : staged_) unpin(st);
+	staged_.clear();
 	if(!err.empty()) throw execution_error(err);
 	if(!mailbox_.empty()) throw execution_error(std::to_string(mailbox_.size()) + " transport messages were never received (protocol violation)");
 }
@@ -1999,6 +2118,7 @@ void executor::remote_send(const task& t) {
 	}
 	check_cuda(cudaGetLastError(), "send kernels");
 	ctr_.bytes_sent += bytes;
+	wc(t.worker).bytes_sent += bytes;
 	finish(t, s);
 }
 
@@ -2038,6 +2158,7 @@ void executor::remote_recv(const task& t) {
 	}
 	check_cuda(cudaGetLastError(), "recv kernels");
 	ctr_.bytes_received += bytes;
+	wc(t.worker).bytes_received += bytes;
 	finish(t, s);
 }
 
@@ -2057,12 +2178,13 @@ std::string executor::report_json() {
 	std::ostringstream os;
 	os << "{\"workers\": [";
 	for(int w = 0; w < cfg_.workers; ++w) {
-		os << (w ? ", " : "") << "{\"worker\": " << w << ", \"evictions\": " << (w == 0 ? ctr_.evictions : 0)
-		   << ", \"bytes_device_to_host\": " << (w == 0 ? ctr_.bytes_device_to_host : 0) << ", \"bytes_host_to_disk\": " << (w == 0 ? ctr_.bytes_host_to_disk : 0)
-		   << ", \"bytes_host_to_device\": " << (w == 0 ? ctr_.bytes_host_to_device : 0) << ", \"bytes_disk_to_device\": " << (w == 0 ? ctr_.bytes_disk_to_host : 0)
-		   << ", \"bytes_sent\": " << (w == 0 ? ctr_.bytes_sent : 0) << ", \"bytes_received\": " << (w == 0 ? ctr_.bytes_received : 0)
-		   << ", \"staging_checks\": 0, \"staging_violations\": 0, \"peak_device_bytes\": [" << ctr_.peak_device_bytes << "], \"tasks\": ["
-		   << tasks[static_cast<size_t>(w)] << "]}";
+		const auto& c = wctr_[static_cast<size_t>(w)];
+		os << (w ? ", " : "") << "{\"worker\": " << w << ", \"evictions\": " << c.evictions << ", \"bytes_device_to_host\": " << c.bytes_device_to_host
+		   << ", \"bytes_host_to_disk\": " << c.bytes_host_to_disk << ", \"bytes_host_to_device\": " << c.bytes_host_to_device
+		   << ", \"bytes_disk_to_device\": " << c.bytes_disk_to_host << ", \"bytes_sent\": " << c.bytes_sent << ", \"bytes_received\": " << c.bytes_received
+		   << ", \"staging_checks\": " << c.staging_checks << ", \"staging_violations\": " << c.staging_violations << ", \"peak_device_bytes\": [";
+		for(int d = 0; d < cfg_.devices_per_worker; ++d) os << (d ? ", " : "") << dev_peak_[static_cast<size_t>(w * cfg_.devices_per_worker + d)];
+		os << "], \"tasks\": [" << tasks[static_cast<size_t>(w)] << "]}";
 	}
 	os << "], \"tasks\": " << ctr_.tasks << ", \"kernel_launches\": " << ctr_.kernels << ", \"copies\": " << ctr_.copies << ", \"bytes_copied\": " << ctr_.bytes_copied
 	   << "}";

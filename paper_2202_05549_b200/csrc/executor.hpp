@@ -51,6 +51,7 @@ struct executor_config {
 	int gpu_base = 0;             // first CUDA device ordinal this executor uses
 	int local_workers = -1;       // -1: all workers
 	uint64_t disk_capacity = 0;   // disk tier below the host tier (0: none)
+	uint64_t staging_threshold = 0; // throttle: bytes of chunks in use by in-flight tasks per device (0: off)
 	std::string spill_dir;        // spill file directory ("" = system temp directory)
 	uint64_t schedule_seed = 0;   // != 0: randomised stream choice + delays (reference ready_seed)
 };
@@ -95,6 +96,12 @@ class executor {
 	bool has_chunk(int64_t chunk) const { return bufs_.count(chunk) != 0; }
 	std::string report_json(); // waits for traced tasks' end events
 	const exec_counters& counters() const { return ctr_; }
+	// per worker, the fields of the reference's run_report memory counters (runtime.cpp:613-636)
+	struct worker_counters {
+		uint64_t evictions = 0, bytes_device_to_host = 0, bytes_host_to_device = 0, bytes_host_to_disk = 0, bytes_disk_to_host = 0;
+		uint64_t bytes_sent = 0, bytes_received = 0, staging_checks = 0, staging_violations = 0;
+	};
+	const worker_counters& worker_stats(int w) const { return wctr_.at(static_cast<size_t>(w)); }
 
 	// stream of the most recent execute on a chunk's device (bench timing hook)
 	cudaStream_t last_exec_stream() const { return last_exec_stream_; }
@@ -208,6 +215,23 @@ class executor {
 
 	executor_config cfg_;
 	std::vector<gpu_res> gpus_;
+	std::vector<worker_counters> wctr_;        // per worker
+	std::vector<uint64_t> dev_used_, dev_peak_; // per logical device (worker-major): chunk bytes by home
+	worker_counters& wc(int worker) { return wctr_[static_cast<size_t>(worker)]; }
+	void charge(const buffer& b, uint64_t bytes, bool add); // device bytes of a chunk (GPU pool + its home device)
+	// staging throttle + monitor (memory.cpp:290-295, 371-374): per logical device, the chunks
+	// used by issued tasks that have not completed, with their bytes; a task whose chunks would
+	// push the union past the threshold waits (on the host) for the oldest in-flight tasks
+	struct staged_task {
+		int64_t id;
+		size_t dev;
+		std::vector<std::pair<int64_t, uint64_t>> chunks;
+	};
+	std::deque<staged_task> staged_;
+	std::vector<std::unordered_map<int64_t, int>> pins_;
+	std::vector<uint64_t> pinned_bytes_;
+	void throttle(const task& t);
+	void unpin(const staged_task& s);
 	std::vector<ldev> ldevs_; // worker-major
 	std::unordered_map<int64_t, buffer> bufs_;
 	std::unordered_map<int64_t, done_ev> done_;

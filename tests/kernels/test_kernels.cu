@@ -54,6 +54,32 @@ int launch_partial_min(const mt_launch_ctx* c, void* stream) {
 	return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+// bf16 partial sums: cell c of the partial accumulates src[i] for i = c mod 8 of this superblock,
+// one f32 add rounded to bf16 (nearest-even) per element, in ascending i
+__device__ float bf(uint16_t b) { return __uint_as_float(static_cast<uint32_t>(b) << 16); }
+__device__ uint16_t to_bf(float f) {
+	uint32_t u = __float_as_uint(f);
+	u += 0x7fffu + ((u >> 16) & 1u);
+	return static_cast<uint16_t>(u >> 16);
+}
+
+__global__ void partial_sum_bf16_k(int64_t lo, int64_t hi, view1 src, view1 dst) {
+	const int64_t c = threadIdx.x;
+	auto* cell = reinterpret_cast<uint16_t*>(dst.base) + (c - dst.off0) * dst.st0;
+	uint16_t acc = *cell;
+	for(int64_t i = lo; i < hi; ++i)
+		if(i % 8 == c) acc = to_bf(__fadd_rn(bf(acc), bf(*(reinterpret_cast<uint16_t*>(src.base) + (i - src.off0) * src.st0))));
+	*cell = acc;
+}
+
+int launch_partial_sum_bf16(const mt_launch_ctx* c, void* stream) {
+	const int64_t n = c->scalars_int[0];
+	const int64_t lo = c->threads_lo[0], hi = c->threads_hi[0] < n ? c->threads_hi[0] : n;
+	if(lo >= hi) return 0;
+	partial_sum_bf16_k<<<1, 8, 0, static_cast<cudaStream_t>(stream)>>>(lo, hi, v(c->views[1]), v(c->views[2]));
+	return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 mt_param_spec P(const char* n, int kind, int dtype, int rank, int w) {
 	mt_param_spec p{};
 	std::strncpy(p.name, n, sizeof(p.name) - 1);
@@ -70,6 +96,8 @@ __attribute__((constructor)) void register_test_kernels() {
 	mt_kernel_register("row_reduce_i64", rr, 4, launch_row_reduce_i64);
 	const mt_param_spec pm[] = {P("n", MT_PARAM_SCALAR, MT_I64, 0, 0), P("src", MT_PARAM_ARRAY, MT_I64, 1, 0), P("dst", MT_PARAM_ARRAY, MT_I64, 1, 1)};
 	mt_kernel_register("partial_min", pm, 3, launch_partial_min);
+	const mt_param_spec ps[] = {P("n", MT_PARAM_SCALAR, MT_I64, 0, 0), P("src", MT_PARAM_ARRAY, MT_BF16, 1, 0), P("dst", MT_PARAM_ARRAY, MT_BF16, 1, 1)};
+	mt_kernel_register("partial_sum_bf16", ps, 3, launch_partial_sum_bf16);
 }
 
 } // namespace

@@ -144,3 +144,50 @@ def test_cli_seed_flag_randomises_and_matches(tmp_path, scenarios):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "oracle: PASS" in r.stdout or "PASS" in r.stdout
+
+
+def test_c5_staging_monitor_fires_without_violations(scenarios):
+    """acceptance.cpp:239-245: across the bundled scenarios run with the reference's default
+    staging threshold (64 MiB, scenario.hpp:72) the monitor fired and never saw a violation"""
+    import json
+    checks = violations = 0
+    for name in NAMES:
+        sc = scenarios[name]
+        with mb.context(workers=sc["system"]["workers"], devices=sc["system"]["devices"], num_gpus=1, staging_threshold=64 << 20) as ctx:
+            S.register_gather_kernels(ctx, sc)
+            S.run(ctx, sc)
+            rep = json.loads(ctx.report_json())
+        checks += sum(w["staging_checks"] for w in rep["workers"])
+        violations += sum(w["staging_violations"] for w in rep["workers"])
+    assert checks > 0 and violations == 0
+
+
+def test_staging_throttle_tight_and_fatal(scenarios, oracle_out):
+    """a threshold just above the largest task footprint throttles hard and stays exact; one below
+    it is the reference's fatal footprint error (memory.cpp:278-281)"""
+    import json
+    sc = scenarios["stencil"]
+    chunk = max_device_working_set(sc, 2, 2) // 2  # one array's chunk on a device (2 arrays per device)
+    with mb.context(workers=2, devices=2, num_gpus=1, staging_threshold=3 * chunk) as ctx:
+        got, coherent = S.run(ctx, sc)
+        rep = json.loads(ctx.report_json())
+    assert coherent and S.compare(got, oracle_out("stencil"), 1e-6) == []
+    assert sum(w["staging_checks"] for w in rep["workers"]) > 0
+    assert sum(w["staging_violations"] for w in rep["workers"]) == 0
+    with pytest.raises(mb.ExecutionError):
+        with mb.context(workers=2, devices=2, num_gpus=1, staging_threshold=chunk // 2) as ctx:
+            S.run(ctx, sc)
+
+
+def test_report_counters_per_worker_and_device(scenarios):
+    """run_report fields per worker (runtime.cpp:613-636): bytes_sent by the sending worker and one
+    peak_device_bytes entry per device of the worker"""
+    import json
+    sc = scenarios["stencil"]
+    with mb.context(workers=2, devices=2, num_gpus=1) as ctx:
+        S.run(ctx, sc)
+        rep = json.loads(ctx.report_json())
+    ws = rep["workers"]
+    assert [w["worker"] for w in ws] == [0, 1]
+    assert all(len(w["peak_device_bytes"]) == 2 and min(w["peak_device_bytes"]) > 0 for w in ws)
+    assert all(w["bytes_sent"] > 0 and w["bytes_received"] > 0 for w in ws)  # halo rows cross the worker boundary both ways

@@ -211,3 +211,36 @@ def test_heat2d_large_band_bit_exact(okern):
         okern.oracle_heat2d(C.c_int64(rows), C.c_int64(cols), C.c_double(0.1), cur.ctypes.data_as(f), nxt.ctypes.data_as(f))
         cur, nxt = nxt, cur
     assert np.array_equal(got.view(np.uint32), cur.view(np.uint32))
+
+
+def _bf16(x):
+    """f32 -> bf16 (nearest-even) as float32 values"""
+    u = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32)
+
+
+def test_bf16_reduce_tree(testkernels):
+    """bf16 reduce(+) through the reduce tree (a B200 extension; the reference has no bf16): the
+    per-superblock partials combine device -> worker -> root (planner.cpp:389-517) with every
+    combine rounded to nearest-even bf16, so the result is the host emulation bit for bit"""
+    n = 1024
+    src = _bf16(1.0 + (np.arange(n) % 97) / 97.0)
+    bits = (src.view(np.uint32) >> 16).astype(np.uint16)
+    with mb.context(workers=2, devices=2, num_gpus=1) as ctx:
+        devs = ctx.devices
+        x = ctx.create_array([n], "bf16", ctx.dist.row([n], n // 4, devs), 0)
+        y = ctx.create_array([8], "bf16", ctx.dist.replicated([8], devs), 0)
+        ctx.write(x, bits)
+        w = ctx.dist.block_work([n], [64], [n // 4], devs)
+        ctx.launch("partial_sum_bf16", [n], [64], w, [n, Arr(x), Arr(y)], "global i => read src[i], reduce(+) dst[:]")
+        got = (ctx.read(y).astype(np.uint32) << 16).view(np.float32)
+        assert ctx.replicas_coherent(y)
+    parts = []
+    for s in range(4):  # one superblock per device, in device order
+        acc = np.zeros(8, np.float32)
+        for i in range(s * n // 4, (s + 1) * n // 4):
+            acc[i % 8] = _bf16(acc[i % 8] + src[i])
+        parts.append(acc)
+    want = _bf16(_bf16(parts[0] + parts[1]) + _bf16(parts[2] + parts[3]))
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
