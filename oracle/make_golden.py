@@ -34,6 +34,7 @@ def main():
     import oracle
     from paper_2202_05549_b200 import Arr
     from paper_2202_05549_b200 import scenario as S
+    from oracle import scenario as R
     ref = oracle.reference()
     os.makedirs(OUT, exist_ok=True)
 
@@ -46,14 +47,14 @@ def main():
 
     outputs, plans = {}, {}
     for name, sc in scen.items():
-        res, coherent = S.reference_run(ref, sc, oracle_mode=True)
+        res, coherent = R.run(ref, sc, oracle_mode=True)
         outputs[name] = {"coherent": coherent, "arrays": {}}
         for an, arr in res.items():
             e = {"shape": list(arr.shape), "dtype": str(arr.dtype), "sha256": hashlib.sha256(arr.tobytes()).hexdigest()}
             if arr.size <= 4096:
                 e["values"] = arr.ravel().tolist()
             outputs[name]["arrays"][an] = e
-        plans[name] = {"system": S.reference_plan(ref, sc).dicts(), "oracle": S.reference_plan(ref, sc, oracle_mode=True).dicts()}
+        plans[name] = {"system": R.plan(ref, sc).dicts(), "oracle": R.plan(ref, sc, oracle_mode=True).dicts()}
     with open(os.path.join(OUT, "scenario_outputs.json"), "w") as fh:
         json.dump(outputs, fh, indent=1, sort_keys=True)
     with open(os.path.join(OUT, "plans.json"), "w") as fh:

@@ -16,6 +16,7 @@ import pytest
 
 from paper_2202_05549_b200 import cli
 from paper_2202_05549_b200 import scenario as S
+from oracle import scenario as R
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -67,7 +68,7 @@ def test_plan_counts_and_dot_match_reference(ref, scenarios, tmp_path, name):
     dot = str(tmp_path / f"{name}.dot")
     rc, out, err = run_cli("plan", path, "--dot", dot, "--compat-deps")
     assert rc == 0, err
-    tasks = S.reference_plan(ref, sc).dicts()
+    tasks = R.plan(ref, sc).dicts()
     workers = sc.get("system", {}).get("workers", 1)
     want = []
     for w in range(workers):

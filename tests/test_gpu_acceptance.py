@@ -23,6 +23,7 @@ import pytest
 
 import paper_2202_05549_b200 as mb
 from paper_2202_05549_b200 import scenario as S
+from oracle import scenario as R
 
 pytestmark = pytest.mark.gpu
 
@@ -36,7 +37,7 @@ def oracle_out(ref, scenarios):
 
     def get(name):
         if name not in cache:
-            cache[name] = S.reference_run(ref, scenarios[name], oracle_mode=True)[0]
+            cache[name] = R.run(ref, scenarios[name], oracle_mode=True)[0]
         return cache[name]
     return get
 

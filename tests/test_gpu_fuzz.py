@@ -10,6 +10,7 @@ import pytest
 
 import paper_2202_05549_b200 as mb
 from paper_2202_05549_b200 import scenario as S
+from oracle import scenario as R
 
 pytestmark = pytest.mark.gpu
 
@@ -34,7 +35,7 @@ def run_product(sc, suppress=False, streams=0):
 def test_correlator_like_scenario(ref, scenarios):
     sc = scenarios["correlator_like"]
     got, coherent = run_product(sc)
-    want, _ = S.reference_run(ref, sc, oracle_mode=True)
+    want, _ = R.run(ref, sc, oracle_mode=True)
     assert coherent
     assert S.compare(got, want) == []
 
@@ -46,7 +47,7 @@ def test_fuzz_campaign_matches_sequential_oracle(ref, block):
         seed = (0x2545F4914F6CDD1D * (block * 25 + i + 7)) % (1 << 63)
         sc = fuzz_scenario(ref, seed)
         try:
-            want, _ = S.reference_run(ref, sc, oracle_mode=True)
+            want, _ = R.run(ref, sc, oracle_mode=True)
         except mb.MantaError:
             continue  # the reference rejects the request sequence too (checked in test_planner_parity)
         got, coherent = run_product(sc)
@@ -64,7 +65,7 @@ def test_suppressed_conflict_edges_are_detected(ref):
     for i in range(160):
         sc = fuzz_scenario(ref, 1000 + i * 7919)
         try:
-            want, _ = S.reference_run(ref, sc, oracle_mode=True)
+            want, _ = R.run(ref, sc, oracle_mode=True)
         except mb.MantaError:
             continue
         tried += 1

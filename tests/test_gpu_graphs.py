@@ -109,6 +109,7 @@ def test_fuzz_scenarios_with_repeats_match_the_reference(ref):
     import ctypes as C2
 
     from paper_2202_05549_b200 import scenario as S
+    from oracle import scenario as R
     replays = 0
     checked = 0
     for i in range(60):
@@ -121,7 +122,7 @@ def test_fuzz_scenarios_with_repeats_match_the_reference(ref):
             launch["repeat"] = 3
         sc["system"]["device_capacity"] = 256 << 20  # no spill: graphs are eligible
         try:
-            want, _ = S.reference_run(ref, sc, oracle_mode=True)
+            want, _ = R.run(ref, sc, oracle_mode=True)
         except mb.MantaError:
             continue
         with mb.context(workers=sc["system"]["workers"], devices=sc["system"]["devices"], num_gpus=1) as ctx:

@@ -19,6 +19,7 @@ import pytest
 import paper_2202_05549_b200 as mb
 from paper_2202_05549_b200 import Arr
 from paper_2202_05549_b200 import scenario as S
+from oracle import scenario as R
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 HEAT = "global [i, j] => read in[i-1:i+1, j-1:j+1], write out[i,j]"
@@ -108,7 +109,7 @@ def test_bundled_scenario_matches_reference(name, mode, scenarios, ref):
     d = 1 if mode == "oracle" else sc["system"]["devices"]
     with mb.context(workers=w, devices=d, num_gpus=1) as ctx:
         got, coherent = S.run(ctx, sc, oracle_mode=(mode == "oracle"))
-    want, _ = S.reference_run(ref, sc, oracle_mode=True)
+    want, _ = R.run(ref, sc, oracle_mode=True)
     assert coherent
     tol = 1e-6
     assert S.compare(got, want, tol) == []
@@ -125,7 +126,7 @@ def test_reference_plan_runs_on_b200_executor(ref, scenarios):
     """Drop-in boundary: the reference driver's own task stream, executed by the B200
     executor (mt_exec_submit), reproduces the reference executor's chunk bytes."""
     sc = scenarios["stencil"]
-    plan = S.reference_plan(ref, sc)
+    plan = R.plan(ref, sc)
     ex = mb.Executor(mb.lib(), workers=2, devices=2, num_gpus=1)
     ex.submit(plan)
     ex.synchronize()
