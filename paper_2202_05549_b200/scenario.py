@@ -13,7 +13,7 @@ from typing import Callable
 import numpy as np
 
 from . import _capi as capi
-from .api import Arr, Context, ValidationError, _NP_DTYPE
+from .api import Arr, Context, ValidationError
 
 _sig_cache: dict = {}
 
