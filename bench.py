@@ -230,15 +230,15 @@ def cpu_reference_rate(rows, cols, iters, devices, bounds_check=True, warmup=CPU
     return rows * cols * iters / dt, dt
 
 
-def cpu_heat_baseline(cols, iters=CPU_ITERS, bounds_off=True) -> dict:
+def cpu_heat_baseline(cols, iters=CPU_ITERS, bounds_off=True, want_rows=CPU_ROWS) -> dict:
     """the heat2d CPU baseline under the shared protocol, plus its sensitivity to the sample
     height (half the rows)"""
     import oracle
     threads = oracle.reference().host_threads()
     devices = max(1, min(threads, 64))
-    rows = sample_rows(CPU_ROWS, devices)
+    rows = sample_rows(want_rows, devices)
     rate, dt = cpu_reference_rate(rows, cols, iters, devices)
-    half = sample_rows(CPU_ROWS // 2, devices)
+    half = sample_rows(want_rows // 2, devices)
     rate_half, _ = cpu_reference_rate(half, cols, iters, devices)
     out = {"value": rate, "unit": "cell-updates/s", "cores": devices, "kind": "reference",
            "sample": f"{rows}x{cols} band of the grid, {devices} chunks (stencil_dist halo [1,0]), 1 worker x {devices} device threads, "
@@ -602,7 +602,7 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": f"reference CPU executor not loadable: {e}"}))
         return
     devices = max(1, min(threads, 64))
-    rows = sample_rows(CPU_ROWS, devices)
+    rows = sample_rows(args.cpu_rows, devices)
     cols = args.cols
     # the shared protocol (CPU_ROWS band, warm-up launches in the same context), each step one
     # heat iteration over the band; the step count is capped so the arm ends within minutes
@@ -723,13 +723,14 @@ def run_c1(iters, ref_iters, hbm, cpu):
         a, b, work = setup_heat(ctx, rows, cols, 4)
 
         def run(n):
+            # the reference's repeat/swap loop in one native call (mt_launch_repeat); repeated
+            # launches replay their memoized plan (planner plan cache)
             nonlocal a, b
-            for i in range(n):
-                ctx.launch("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN)
-                if (i + 1) % C1_PER_FLUSH == 0:
-                    ctx.flush()
-                a, b = b, a
+            ctx.launch_repeat("heat2d", [rows, cols], [16, 16], work, [rows, cols, ALPHA, Arr(b), Arr(a)], ANN, n, swap=(a, b),
+                              flush_every=C1_PER_FLUSH)
             ctx.flush()
+            if n % 2:
+                a, b = b, a
 
         run(3 * C1_PER_FLUSH)
         ctx.synchronize()
@@ -739,13 +740,14 @@ def run_c1(iters, ref_iters, hbm, cpu):
         ms = ctx.elapsed_ms() / iters
         ctx.synchronize()
         st = ctx.exec_stats()
+        hits = ctx.plan_cache_hits()
     gbs = BYTES_PER_CELL * rows * cols / (ms / 1e3) / 1e9
-    out = {"workload": f"heat2d {rows}x{cols} f32, 4 chunks (stencil_dist halo [1,0]), {iters} iterations, one launch per iteration, "
-                       f"handed to the executor every {C1_PER_FLUSH} launches",
+    out = {"workload": f"heat2d {rows}x{cols} f32, 4 chunks (stencil_dist halo [1,0]), {iters} iterations, one launch per iteration "
+                       f"(mt_launch_repeat with the a/b swap), handed to the executor every {C1_PER_FLUSH} launches",
            "value": rows * cols / (ms / 1e3), "unit": "cell-updates/s", "ms_per_iter": ms,
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                         "note": "step time incl. planning, halo copies and graph launch; small grid: issue-bound"},
-           "graph_replays": st.get("graph_replays")}
+           "graph_replays": st.get("graph_replays"), "plan_cache_hits": hits}
     if cpu:
         try:
             rate, dt = cpu_reference_rate(rows, cols, ref_iters, 4, warmup=1)
@@ -937,7 +939,7 @@ def run_b200(args):
     cpu = None
     if rank == 0 and args.cpu_baseline:
         try:
-            cpu = cpu_heat_baseline(cols)
+            cpu = cpu_heat_baseline(cols, iters=args.cpu_iters, want_rows=args.cpu_rows)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "cell-updates/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
@@ -1045,6 +1047,8 @@ def main():
     p.add_argument("--e2e-pipeline", type=int, default=40, help="pipelined e2e steps (0: report the sequential e2e)")
     p.add_argument("--e2e-sets", type=int, default=3, help="array sets the pipelined e2e steps rotate over")
     p.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    p.add_argument("--cpu-rows", type=int, default=CPU_ROWS, help="rows of the heat CPU-baseline band (both arms)")
+    p.add_argument("--cpu-iters", type=int, default=CPU_ITERS, help="timed launches of the main arm's heat CPU baseline")
     p.add_argument("--matmul-n", type=int, default=32768, help="C3 contraction size (0 to skip)")
     p.add_argument("--matmul-steps", type=int, default=5)
     p.add_argument("--tf32-steps", type=int, default=3, help="steps of the C3 fp32 (TF32) contraction leg (0 to skip)")

@@ -191,6 +191,10 @@ typedef struct mt_config {
 	                                   drawn from a generator seeded with it, behind a random on-device delay,
 	                                   and graph replay is off: the GPU analogue of the reference's seeded
 	                                   ready-task choice (runtime.cpp:313-319, run_overrides::ready_seed) */
+	int32_t plan_cache_off;         /* 1: plan every launch from scratch; 0: a repeated identical launch whose
+	                                   chunks are in the earlier launch's conflict state (task ids moved)
+	                                   replays that plan (identical tasks, a fraction of the cost) */
+	int32_t pad_;
 } mt_config;
 
 /* One planned chunk access (a create counts as a write of the whole chunk). */
@@ -232,6 +236,14 @@ int mt_array_delete(mt_ctx* ctx, int64_t array_id);
 int mt_array_chunks(mt_ctx* ctx, int64_t array_id, mt_chunk_desc* out, int64_t cap, int64_t* n_out);
 int mt_launch(mt_ctx* ctx, const char* kernel, const mt_rect* grid, const int64_t* block, const mt_superblock* work, int64_t nwork,
     const mt_launch_arg* args, int32_t nargs, const char* annotation, int64_t* first_task, int64_t* past_last_task);
+/* The repeat loop of apply_scenario (scenario.cpp:407-441) in one call: `repeat` launches of the
+ * same request; after each one every array argument equal to swap_a becomes swap_b and vice
+ * versa (the scenario's name swap; pass -1 for no swap); the new tasks are handed to the executor
+ * after every `flush_every` launches (0: only at the end, negative: never). *first_task / *past_last_task cover
+ * all launches. */
+int mt_launch_repeat(mt_ctx* ctx, const char* kernel, const mt_rect* grid, const int64_t* block, const mt_superblock* work, int64_t nwork,
+    const mt_launch_arg* args, int32_t nargs, const char* annotation, int32_t repeat, int64_t swap_a, int64_t swap_b, int32_t flush_every,
+    int64_t* first_task, int64_t* past_last_task);
 /* Hands every task emitted since the previous call to the executor (take_pending+submit). */
 int mt_flush(mt_ctx* ctx);
 int mt_sync(mt_ctx* ctx);
@@ -261,6 +273,8 @@ int mt_array_check_replicas(mt_ctx* ctx, int64_t array_id, int32_t* coherent);
 int mt_plan_export(mt_ctx* ctx, int64_t first, int64_t last, mt_task* tasks, int64_t task_cap, int64_t* ntasks, int64_t* pool, int64_t pool_cap,
     int64_t* npool, mt_arg_binding* args, int64_t args_cap, int64_t* nargs);
 int64_t mt_plan_size(mt_ctx* ctx);
+/* launches planned by replaying an earlier identical launch's plan (mt_config.plan_cache_off) */
+uint64_t mt_plan_cache_hits(mt_ctx* ctx);
 /* access records of non-temporary chunks in emission order (needs cfg.record_accesses);
  * used to check that the dependency DAG orders every pair of conflicting accesses */
 int mt_plan_accesses(mt_ctx* ctx, mt_access* out, int64_t cap, int64_t* n_out);

@@ -646,6 +646,38 @@ int mr_flush(mt_ctx* ctx) {
 	});
 }
 
+// the repeat / swap loop of apply_scenario (scenario.cpp:407-441) over the reference driver
+int mr_launch_repeat(mt_ctx* ctx, const char* kernel, const mt_rect* grid, const int64_t* block, const mt_superblock* work, int64_t nwork,
+    const mt_launch_arg* args, int32_t nargs, const char* annotation, int32_t repeat, int64_t swap_a, int64_t swap_b, int32_t flush_every, int64_t* first,
+    int64_t* last) {
+	if(repeat < 1) {
+		g_last_error = "repeat must be at least 1";
+		return MT_EVALIDATION;
+	}
+	std::vector<mt_launch_arg> a(args, args + nargs);
+	int64_t lo = -1, hi = -1;
+	for(int32_t rep = 0; rep < repeat; ++rep) {
+		int64_t f = 0, l = 0;
+		if(const int rc = mr_launch(ctx, kernel, grid, block, work, nwork, a.data(), nargs, annotation, &f, &l)) return rc;
+		if(rep == 0) lo = f;
+		hi = l;
+		if(flush_every > 0 && (rep + 1) % flush_every == 0)
+			if(const int rc = mr_flush(ctx)) return rc;
+		for(auto& x : a) {
+			if(x.kind != MT_LARG_ARRAY) continue;
+			if(x.array == swap_a)
+				x.array = swap_b;
+			else if(x.array == swap_b)
+				x.array = swap_a;
+		}
+	}
+	if(flush_every == 0)
+		if(const int rc = mr_flush(ctx)) return rc;
+	*first = lo;
+	*last = hi;
+	return MT_OK;
+}
+
 int mr_sync(mt_ctx* ctx) {
 	return guarded([&] {
 		auto pending = ctx->drv->take_pending();

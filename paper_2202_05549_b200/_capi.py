@@ -92,7 +92,7 @@ class Config(C.Structure):
         ("device_capacity", C.c_uint64), ("host_capacity", C.c_uint64), ("staging_threshold", C.c_uint64),
         ("record_accesses", C.c_int32), ("lookahead_tasks", C.c_int32),
         ("worker_rank", C.c_int32), ("gpu_base", C.c_int32), ("collective_reduce", C.c_int32), ("drop_executed_tasks", C.c_int32), ("disk_capacity", C.c_uint64), ("spill_dir", C.c_char_p),
-        ("schedule_seed", C.c_uint64),
+        ("schedule_seed", C.c_uint64), ("plan_cache_off", C.c_int32), ("pad_", C.c_int32),
     ]
 
 
@@ -135,6 +135,8 @@ _SIGS = {
     "array_chunks": (C.c_int, [C.c_void_p, C.c_int64, P(ChunkDesc), C.c_int64, P(C.c_int64)]),
     "launch": (C.c_int, [C.c_void_p, C.c_char_p, P(Rect), P(C.c_int64), P(Superblock), C.c_int64, P(LaunchArg), C.c_int32, C.c_char_p,
                          P(C.c_int64), P(C.c_int64)]),
+    "launch_repeat": (C.c_int, [C.c_void_p, C.c_char_p, P(Rect), P(C.c_int64), P(Superblock), C.c_int64, P(LaunchArg), C.c_int32, C.c_char_p,
+                                C.c_int32, C.c_int64, C.c_int64, C.c_int32, P(C.c_int64), P(C.c_int64)]),
     "flush": (C.c_int, [C.c_void_p]),
     "sync": (C.c_int, [C.c_void_p]),
     "array_read": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_uint64]),
@@ -143,6 +145,7 @@ _SIGS = {
     "plan_export": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, P(Task), C.c_int64, P(C.c_int64), P(C.c_int64), C.c_int64, P(C.c_int64),
                               P(ArgBinding), C.c_int64, P(C.c_int64)]),
     "plan_size": (C.c_int64, [C.c_void_p]),
+    "plan_cache_hits": (C.c_uint64, [C.c_void_p]),
     "plan_accesses": (C.c_int, [C.c_void_p, P(Access), C.c_int64, P(C.c_int64)]),
     "chunk_meta": (C.c_int, [C.c_void_p, C.c_int64, P(ChunkDesc), P(C.c_int32), P(C.c_int32)]),
     "ctx_exec": (C.c_void_p, [C.c_void_p]),
@@ -185,7 +188,8 @@ _SIGS = {
 }
 # entry points the oracle shim may lack
 _OPTIONAL = {"exec_stats", "exec_last_stream", "kernel_info", "host_threads", "ctx_kernel_register", "fuzz_scenario_json", "scenario_plan", "scenario_dot",
-             "scenario_run", "plan_accesses", "ctx_gather_register", "ctx_peer_export", "ctx_peer_import", "ctx_nccl_unique_id", "ctx_nccl_init", "array_write_async", "array_read_async", "array_write_box_async", "array_read_box_async", "ctx_kernel_compile", "wrapper_source", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time", "exec_trace"}
+             "scenario_run", "plan_accesses", "ctx_gather_register", "ctx_peer_export", "ctx_peer_import", "ctx_nccl_unique_id", "ctx_nccl_init", "array_write_async", "array_read_async", "array_write_box_async", "array_read_box_async", "ctx_kernel_compile", "wrapper_source", "exec_mark", "exec_elapsed_ms", "exec_profile", "exec_kernel_time", "exec_trace",
+             "plan_cache_hits"}
 
 
 class MantaError(RuntimeError):

@@ -218,7 +218,7 @@ class Context:
     def __init__(self, lib: capi.Lib, workers=1, devices=1, execute=True, compat_deps=False, suppress_conflict_deps=False,
                  num_gpus=0, streams_per_device=0, device_capacity=0, host_capacity=0, staging_threshold=0, record_accesses=False,
                  lookahead_tasks=0, worker_rank=None, gpu_base=0, collective_reduce=False, retain_plan=True, disk_capacity=0,
-                 spill_dir=None, schedule_seed=0):
+                 spill_dir=None, schedule_seed=0, plan_cache=True):
         self.lib = lib
         self.dist = Distributions(lib)
         cfg = capi.Config()
@@ -239,6 +239,7 @@ class Context:
         self._spill_dir = spill_dir.encode() if spill_dir else None
         cfg.spill_dir = self._spill_dir
         cfg.schedule_seed = int(schedule_seed)
+        cfg.plan_cache_off = int(not plan_cache)
         if worker_rank is not None:  # one process per worker
             cfg.single_worker, cfg.worker_rank, cfg.gpu_base = 1, int(worker_rank), int(gpu_base)
         self.single_worker = worker_rank is not None
@@ -315,6 +316,19 @@ class Context:
         kb, g, b, w, nw, la, na, ab = hit
         first, last = C.c_int64(0), C.c_int64(0)
         self.lib.check(self.lib.launch(self.h, kb, C.byref(g), b, w, nw, la, na, ab, C.byref(first), C.byref(last)))
+        return first.value, last.value
+
+    def launch_repeat(self, kernel: str, grid, block, work: Sequence[Superblock], args: Iterable, annotation: str, repeat: int,
+                      swap=None, flush_every=0):
+        """`repeat` launches of one request in a single call (the repeat loop of apply_scenario,
+        scenario.cpp:407-441): after each launch the array arguments `swap` = (a, b) exchange
+        roles (the scenario's name swap); tasks go to the executor every `flush_every` launches
+        (0: at the end). Returns the task id range of all launches."""
+        kb, g, b, w, nw, la, na, ab = self._convert_launch(kernel, grid, block, work, list(args), annotation)
+        sa, sb = (-1, -1) if swap is None else (int(getattr(swap[0], "id", swap[0])), int(getattr(swap[1], "id", swap[1])))
+        first, last = C.c_int64(0), C.c_int64(0)
+        self.lib.check(self.lib.launch_repeat(self.h, kb, C.byref(g), b, w, nw, la, na, ab, int(repeat), sa, sb, int(flush_every), C.byref(first),
+                                              C.byref(last)))
         return first.value, last.value
 
     def _convert_launch(self, kernel, grid, block, work, args, annotation):
@@ -425,6 +439,9 @@ class Context:
     # -- plan --------------------------------------------------------------------------
     def plan_size(self) -> int:
         return int(self.lib.plan_size(self.h))
+
+    def plan_cache_hits(self) -> int:
+        return int(self.lib.plan_cache_hits(self.h)) if self.lib.has("plan_cache_hits") else 0
 
     def export_plan(self, first=0, last=None) -> PlanBuffer:
         if last is None:

@@ -334,6 +334,7 @@ int mt_ctx_create(const mt_config* cfg, mt_ctx** out) {
 		pc.compat_deps = cfg->compat_deps != 0;
 		pc.record_accesses = cfg->record_accesses != 0;
 		pc.collective_reduce = cfg->collective_reduce != 0;
+		pc.plan_cache = cfg->plan_cache_off == 0;
 		pc.retain_plan = cfg->drop_executed_tasks == 0;
 		ctx->plan = std::make_unique<planner>(pc);
 		if(cfg->execute) {
@@ -374,8 +375,15 @@ int mt_array_chunks(mt_ctx* ctx, int64_t id, mt_chunk_desc* out, int64_t cap, in
 
 int mt_launch(mt_ctx* ctx, const char* kernel, const mt_rect* grid, const int64_t* block, const mt_superblock* work, int64_t nwork,
     const mt_launch_arg* args, int32_t nargs, const char* ann_text, int64_t* first, int64_t* last) {
+	return mt_launch_repeat(ctx, kernel, grid, block, work, nwork, args, nargs, ann_text, 1, -1, -1, -1, first, last);
+}
+
+int mt_launch_repeat(mt_ctx* ctx, const char* kernel, const mt_rect* grid, const int64_t* block, const mt_superblock* work, int64_t nwork,
+    const mt_launch_arg* args, int32_t nargs, const char* ann_text, int32_t repeat, int64_t swap_a, int64_t swap_b, int32_t flush_every, int64_t* first,
+    int64_t* last) {
 	return guarded([&] {
-		nvtx3::scoped_range_in<mtb::nvtx_domain> range{kernel ? kernel : "mt_launch"}; // planning of one launch (NVTX, visible in nsys)
+		nvtx3::scoped_range_in<mtb::nvtx_domain> range{kernel ? kernel : "mt_launch"}; // planning of the launch(es) (NVTX, visible in nsys)
+		if(repeat < 1) throw validation_error("repeat must be at least 1");
 		const box g = to_box(*grid);
 		std::vector<superblock> w;
 		w.reserve(static_cast<size_t>(nwork));
@@ -389,9 +397,25 @@ int mt_launch(mt_ctx* ctx, const char* kernel, const mt_rect* grid, const int64_
 		}
 		auto it = ctx->ann_cache.find(ann_text);
 		if(it == ctx->ann_cache.end()) it = ctx->ann_cache.emplace(ann_text, parse_annotation(ann_text)).first;
-		const auto r = ctx->plan->launch(kernel, g, point::of(g.rank(), block), w, la, it->second);
-		*first = r.first;
-		*last = r.second;
+		const point blk = point::of(g.rank(), block);
+		int64_t lo = -1, hi = -1;
+		for(int32_t rep = 0; rep < repeat; ++rep) {
+			const auto r = ctx->plan->launch(kernel, g, blk, w, la, it->second);
+			if(rep == 0) lo = r.first;
+			hi = r.second;
+			if(flush_every > 0 && (rep + 1) % flush_every == 0) flush(ctx);
+			if(swap_a >= 0 || swap_b >= 0)
+				for(auto& a : la) {
+					if(a.kind != launch_arg::array_k) continue;
+					if(a.array == swap_a)
+						a.array = swap_b;
+					else if(a.array == swap_b)
+						a.array = swap_a;
+				}
+		}
+		if(flush_every == 0) flush(ctx);
+		*first = lo;
+		*last = hi;
 	});
 }
 
@@ -517,6 +541,8 @@ int mt_plan_export(mt_ctx* ctx, int64_t first, int64_t last, mt_task* tasks, int
 }
 
 int64_t mt_plan_size(mt_ctx* ctx) { return ctx->plan->next_id(); }
+
+uint64_t mt_plan_cache_hits(mt_ctx* ctx) { return ctx->plan->plan_cache_hits(); }
 
 int mt_plan_accesses(mt_ctx* ctx, mt_access* out, int64_t cap, int64_t* n_out) {
 	return guarded([&] {

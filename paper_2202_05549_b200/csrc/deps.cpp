@@ -258,4 +258,33 @@ void dep_tracker::write(int64_t chunk, int64_t task, const box& region_in, std::
 	settle(s, region);
 }
 
+dep_tracker::snapshot dep_tracker::save(int64_t chunk) const { return snapshot{get(chunk)}; }
+
+bool dep_tracker::matches(int64_t chunk, const snapshot& snap, int64_t delta) const {
+	const auto it = chunks_.find(chunk);
+	if(it == chunks_.end()) return false;
+	const state& a = it->second;
+	const state& b = snap.st;
+	if(a.filled != b.filled || a.axis != b.axis || a.cells.size() != b.cells.size() || a.region != b.region) return false;
+	for(auto x = a.cells.begin(), y = b.cells.begin(); x != a.cells.end(); ++x, ++y) {
+		const cell& c = x->second;
+		const cell& d = y->second;
+		if(x->first != y->first || c.region != d.region || c.readers.size() != d.readers.size()) return false;
+		if(c.writer != (d.writer < 0 ? d.writer : d.writer + delta)) return false;
+		for(size_t k = 0; k < c.readers.size(); ++k)
+			if(c.readers[k] != d.readers[k] + delta) return false;
+	}
+	return true;
+}
+
+void dep_tracker::restore(int64_t chunk, const snapshot& snap, int64_t delta) {
+	state& a = get(chunk);
+	a = snap.st;
+	a.probes = a.hits = 0;
+	for(auto& [k, c] : a.cells) {
+		if(c.writer >= 0) c.writer += delta;
+		for(auto& r : c.readers) r += delta;
+	}
+}
+
 } // namespace mtb

@@ -52,6 +52,13 @@ class dep_tracker {
 	size_t cell_count(int64_t chunk) const;
 	int index_axis(int64_t chunk) const;
 
+	// Launch-plan memo support (planner.cpp, plan cache): a chunk's complete conflict state, and
+	// the test / restore of "the same state with every task id moved by delta".
+	struct snapshot;
+	snapshot save(int64_t chunk) const;
+	bool matches(int64_t chunk, const snapshot& s, int64_t delta) const;
+	void restore(int64_t chunk, const snapshot& s, int64_t delta);
+
   private:
 	struct cell {
 		box region;
@@ -70,6 +77,13 @@ class dep_tracker {
 
 	bool compat_;
 	std::unordered_map<int64_t, state> chunks_;
+
+  public:
+	struct snapshot {
+		state st;
+	};
+
+  private:
 
 	state& get(int64_t chunk);
 	const state& get(int64_t chunk) const;

@@ -1,5 +1,7 @@
 #include "planner.hpp"
 
+#include <algorithm>
+#include <cstring>
 #include <numeric>
 
 namespace mtb {
@@ -78,6 +80,10 @@ int64_t planner::emit_create(int worker, device_id dev, int64_t chunk_id, fill_k
 
 // registry access for one task (array_registry.cpp:41-67 + planner.cpp:62-70)
 void planner::record(int64_t c, int64_t t, bool write, const box& region, bool check_filled, std::vector<int64_t>& out) {
+	if(recording_ && std::find(rec_chunks_.begin(), rec_chunks_.end(), c) == rec_chunks_.end()) {
+		rec_chunks_.push_back(c);
+		rec_before_.push_back(deps_.save(c));
+	}
 	if(check_filled && !deps_.filled(c))
 		throw plan_error("chunk " + std::to_string(c) + " is read before any fill or write; its contents would be undefined");
 	if(cfg_.suppress_conflict_deps) {
@@ -210,7 +216,113 @@ struct bound_param {
 
 } // namespace
 
+// ---- launch-plan memo ------------------------------------------------------------------------
+//
+// Planning is a deterministic function of the call (kernel, grid, block, work, arguments,
+// annotation), of the conflict state of the chunks the launch touches, of the per-pair message
+// tags and of the next task / chunk ids. An iterative loop repeats the same calls (a ping-pong
+// heat step is two alternating calls), and once the loop is in steady state every touched chunk
+// is in the state it had one period earlier with all task ids moved by the tasks emitted since.
+// A repeated call whose chunks pass that test (dep_tracker::matches) replays the recorded tasks
+// with ids, dependencies and tags moved, and sets the chunks to the recorded after-state moved
+// the same way: exactly the plan a fresh planning pass would emit, at a fraction of its cost.
+// Launches that create temporaries, reduce trees or collectives are not recorded.
+constexpr size_t kMemoMaxSuperblocks = 256;
+constexpr size_t kMemos = 8;
+
+bool planner::same_call(const launch_memo& m, const std::string& kernel, const box& grid, const point& block, const std::vector<superblock>& work,
+    const std::vector<launch_arg>& args, const annotation& ann) const {
+	if(m.ann != &ann || m.kernel != kernel || !(m.grid == grid) || !(m.block == block) || m.work.size() != work.size() || m.args.size() != args.size())
+		return false;
+	for(size_t i = 0; i < work.size(); ++i)
+		if(!(m.work[i].blocks == work[i].blocks) || !(m.work[i].device == work[i].device)) return false;
+	for(size_t i = 0; i < args.size(); ++i) {
+		const auto& a = m.args[i];
+		const auto& b = args[i];
+		if(a.kind != b.kind || a.i != b.i || a.array != b.array || std::memcmp(&a.f, &b.f, sizeof(double)) != 0) return false;
+	}
+	return true;
+}
+
+bool planner::replay(const launch_memo& m, std::pair<int64_t, int64_t>& out) {
+	const int64_t delta = next_task_ - m.first;
+	for(size_t i = 0; i < m.chunks.size(); ++i)
+		if(!deps_.matches(m.chunks[i], m.before[i], delta)) return false;
+	const int64_t first = next_task_;
+	for(const auto& rec : m.tasks) {
+		task t = rec;
+		for(auto& d : t.deps) d += delta;
+		if(t.kind == task_kind::send || t.kind == task_kind::recv) {
+			const std::pair<int, int> pair = t.kind == task_kind::send ? std::make_pair(t.worker, t.peer) : std::make_pair(t.peer, t.worker);
+			const auto b = m.tags_before.find(pair);
+			t.tag = t.tag - (b == m.tags_before.end() ? 0 : b->second) + tags_[pair];
+		}
+		emit(std::move(t));
+	}
+	for(const auto& [pair, used] : m.tags_used) tags_[pair] += used;
+	for(size_t i = 0; i < m.chunks.size(); ++i) deps_.restore(m.chunks[i], m.after[i], delta);
+	if(cfg_.record_accesses)
+		for(auto a : m.accesses) {
+			a.task += delta;
+			accesses_.push_back(a);
+		}
+	++memo_hits_;
+	out = {first, next_task_};
+	return true;
+}
+
 std::pair<int64_t, int64_t> planner::launch(const std::string& kernel, const box& grid, const point& block, const std::vector<superblock>& work,
+    const std::vector<launch_arg>& args, const annotation& ann) {
+	if(!cfg_.plan_cache) return plan_launch(kernel, grid, block, work, args, ann);
+	for(const auto& m : memos_) {
+		std::pair<int64_t, int64_t> r;
+		if(same_call(m, kernel, grid, block, work, args, ann) && replay(m, r)) return r;
+	}
+	const bool rec = work.size() <= kMemoMaxSuperblocks;
+	const int64_t first = next_task_, chunks0 = next_chunk_;
+	const uint64_t coll0 = collectives_;
+	const size_t acc0 = accesses_.size();
+	const auto tags0 = tags_;
+	recording_ = rec;
+	rec_chunks_.clear();
+	rec_before_.clear();
+	std::pair<int64_t, int64_t> r;
+	try {
+		r = plan_launch(kernel, grid, block, work, args, ann);
+	} catch(...) {
+		recording_ = false;
+		throw;
+	}
+	recording_ = false;
+	if(!rec || next_chunk_ != chunks0 || collectives_ != coll0 || rec_chunks_.empty()) return r;
+	launch_memo m;
+	m.kernel = kernel;
+	m.grid = grid;
+	m.block = block;
+	m.work = work;
+	m.args = args;
+	m.ann = &ann;
+	m.first = first;
+	for(int64_t id = first; id < next_task_; ++id) m.tasks.push_back(plan_[static_cast<size_t>(id - plan_base_)]);
+	m.tags_before = tags0;
+	for(const auto& [pair, n] : tags_) {
+		const auto b = tags0.find(pair);
+		const uint64_t used = n - (b == tags0.end() ? 0 : b->second);
+		if(used) m.tags_used[pair] = used;
+	}
+	m.chunks = rec_chunks_;
+	m.before = std::move(rec_before_);
+	for(const auto c : m.chunks) m.after.push_back(deps_.save(c));
+	if(cfg_.record_accesses) m.accesses.assign(accesses_.begin() + static_cast<std::ptrdiff_t>(acc0), accesses_.end());
+	rec_before_.clear();
+	// several memos per call are kept: a loop that interleaves other requests every few launches
+	// repeats its states with a longer period than the call sequence itself
+	memos_.push_front(std::move(m));
+	if(memos_.size() > kMemos) memos_.pop_back();
+	return r;
+}
+
+std::pair<int64_t, int64_t> planner::plan_launch(const std::string& kernel, const box& grid, const point& block, const std::vector<superblock>& work,
     const std::vector<launch_arg>& args, const annotation& ann) {
 	const int64_t first = next_task_;
 	const kernel_entry* kdef = find_kernel(kernel);

@@ -29,6 +29,9 @@ struct planner_config {
 	// cross-worker reduce trees as one allreduce task per worker (B200 extension; the
 	// default keeps the reference's send-to-root tree, planner.cpp:389-517)
 	bool collective_reduce = false;
+	// replay the plan of an identical earlier launch when the conflict state of every chunk it
+	// touches is that launch's state with task ids moved (iterative loops: plan once, replay)
+	bool plan_cache = true;
 };
 
 struct launch_arg {
@@ -100,6 +103,7 @@ class planner {
 		bool write;
 	};
 	const std::vector<access_rec>& accesses() const { return accesses_; }
+	uint64_t plan_cache_hits() const { return memo_hits_; }
 
   private:
 	planner_config cfg_;
@@ -119,6 +123,33 @@ class planner {
 	std::unordered_map<int64_t, std::vector<int64_t>> temp_users_;
 	std::vector<std::unique_ptr<kernel_entry>> local_kernels_;
 	std::vector<access_rec> accesses_;
+
+	std::pair<int64_t, int64_t> plan_launch(const std::string& kernel, const box& grid, const point& block, const std::vector<superblock>& work,
+	    const std::vector<launch_arg>& args, const annotation& ann);
+
+	// ---- launch-plan memo (plan cache) ----------------------------------------------------
+	struct launch_memo {
+		std::string kernel;
+		box grid;
+		point block;
+		std::vector<superblock> work;
+		std::vector<launch_arg> args;
+		const annotation* ann = nullptr;
+		int64_t first = 0;
+		std::vector<task> tasks;
+		std::map<std::pair<int, int>, uint64_t> tags_before, tags_used; // per (src, dst) worker pair
+		std::vector<int64_t> chunks;
+		std::vector<dep_tracker::snapshot> before, after;
+		std::vector<access_rec> accesses;
+	};
+	std::deque<launch_memo> memos_;
+	bool recording_ = false;
+	std::vector<int64_t> rec_chunks_;
+	std::vector<dep_tracker::snapshot> rec_before_;
+	uint64_t memo_hits_ = 0;
+	bool same_call(const launch_memo& m, const std::string& kernel, const box& grid, const point& block, const std::vector<superblock>& work,
+	    const std::vector<launch_arg>& args, const annotation& ann) const;
+	bool replay(const launch_memo& m, std::pair<int64_t, int64_t>& out);
 
 	int64_t emit(task&& t);
 	int64_t new_temp(const box& region, device_id home, dtype type);

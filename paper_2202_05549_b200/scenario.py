@@ -122,7 +122,10 @@ def apply(ctx: Context, sc: dict, oracle_mode=False, flush=True) -> dict:
         sig = kernel_signature(ctx, kernel)
         if l.get("repeat", 1) < 1:
             raise ValidationError("repeat must be at least 1")
-        for _ in range(l.get("repeat", 1)):
+        repeat = l.get("repeat", 1)
+        sw = l.get("swap")
+        native = repeat > 1 and ctx.lib.has("launch_repeat") and (not sw or (sw[0] in ids and sw[1] in ids))
+        for _ in range(1 if native else repeat):
             work = ctx.dist.block_work(l["grid"], l["block"], l["superblock"], devices)
             if len(l.get("args", [])) != len(sig):
                 raise ValidationError(f'kernel "{kernel}" takes {len(sig)} arguments')
@@ -141,11 +144,21 @@ def apply(ctx: Context, sc: dict, oracle_mode=False, flush=True) -> dict:
                     if spec not in ids:
                         raise ValidationError(f'unknown array "{spec}"')
                     args.append(Arr(ids[spec]))
+            if native:
+                # the whole repeat loop in one native call (mt_launch_repeat): same launches, swaps
+                # and hand-offs as the loop below
+                ctx.launch_repeat(kernel, l["grid"], l["block"], work, args, l["annotation"], repeat,
+                                  swap=(ids[sw[0]], ids[sw[1]]) if sw else None, flush_every=1 if flush else -1)
+                if sw and repeat % 2:
+                    ids[sw[0]], ids[sw[1]] = ids[sw[1]], ids[sw[0]]
+                continue
             ctx.launch(kernel, l["grid"], l["block"], work, args, l["annotation"])
             if flush:
                 ctx.flush()
-            if l.get("swap"):
-                a, b = l["swap"]
+            if sw:
+                a, b = sw
+                if a not in ids or b not in ids:
+                    raise ValidationError("swap names an unknown array")
                 ids[a], ids[b] = ids[b], ids[a]
     return ids
 

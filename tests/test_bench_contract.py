@@ -39,7 +39,7 @@ def test_bench_line_schema_on_gpu():
     """a short N=1 bench run prints one JSON line with every key the driver reads"""
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "10", "--warmup", "3", "--rows", "8192", "--cols", "8192",
                         "--matmul-n", "0", "--no-c4", "--no-c1", "--ooc-gib", "0", "--e2e-runs", "1", "--e2e-pipeline", "2", "--e2e-iters", "5",
-                        "--ref-rows", "256", "--ref-iters", "1"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+                        "--cpu-rows", "128", "--cpu-iters", "2"], capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
     assert len(lines) == 1

@@ -30,7 +30,7 @@ def test_reference_shim_exports_the_same_entry_points(ref):
     optional = {"mt_exec_stats", "mt_exec_last_stream", "mt_kernel_info", "mt_ctx_kernel_register", "mt_exec_mark", "mt_exec_elapsed_ms",
                 "mt_exec_profile", "mt_exec_kernel_time", "mt_exec_trace", "mt_plan_accesses", "mt_ctx_gather_register", "mt_ctx_peer_export",
                 "mt_ctx_peer_import", "mt_ctx_nccl_unique_id", "mt_ctx_nccl_init", "mt_array_write_async", "mt_array_read_async", "mt_array_write_box_async", "mt_array_read_box_async", "mt_ctx_kernel_compile", "mt_wrapper_source",
-                "mt_gemm_bf16_nt", "mt_gemm_tf32_nt", "mt_gemm_tf32_nn", "mt_tensor_core_launches"}  # GPU-only: the reference has no tensor-core contraction
+                "mt_gemm_bf16_nt", "mt_gemm_tf32_nt", "mt_gemm_tf32_nn", "mt_tensor_core_launches", "mt_plan_cache_hits"}  # GPU-only: the reference has no tensor-core contraction
     missing = [n for n in declared() if n not in optional and not hasattr(ref.dll, "mr_" + n[3:])]
     assert missing == []
 

@@ -1,0 +1,127 @@
+"""Launch-plan memo (planner.cpp, plan cache) and mt_launch_repeat.
+
+A repeated identical launch whose touched chunks are in the earlier launch's conflict state (task
+ids moved) replays the recorded plan. The replayed plan must be EXACTLY what planning from
+scratch emits: compared task by task (ids, kinds, deps, regions, tags, argument bindings) with
+the cache off, over ping-pong loops on several system shapes (copies, send/recv pairs with
+tags), interleaved host transfers and launches that must not be replayed (reduce trees with
+temporaries)."""
+import time
+
+import numpy as np
+import pytest
+
+import paper_2202_05549_b200 as mb
+from paper_2202_05549_b200 import Arr
+
+HEAT = "global [i, j] => read in[i-1:i+1, j-1:j+1], write out[i,j]"
+
+
+def _plan(cache, workers, devices, rows, cols, iters, strips=False, host=False, reduce_every=0, compat=False):
+    ctx = mb.context(workers=workers, devices=devices, execute=False, plan_cache=cache, record_accesses=True, compat_deps=compat)
+    devs = ctx.devices
+    nd = len(devs)
+    dist = lambda: ctx.dist.stencil([rows, cols], [rows // nd, cols], [1, 0], devs)  # noqa: E731
+    a = ctx.create_array([rows, cols], "f32", dist(), 0)
+    b = ctx.create_array([rows, cols], "f32", dist(), 0)
+    h = ctx.create_array([8], "i64", ctx.dist.replicated([8], devs), 0)
+    x = ctx.create_array([rows * cols], "i32", ctx.dist.row([rows * cols], rows * cols // nd, devs), 0)
+    if strips:
+        from paper_2202_05549_b200 import Superblock
+        rb = rows // nd // 2
+        work = []
+        for i, d in enumerate(devs):
+            b0 = i * rows // nd // 2
+            for lo, hi in ((b0, b0 + 1), (b0 + 1, b0 + rb - 1), (b0 + rb - 1, b0 + rb)):
+                work.append(Superblock((lo, 0), (hi, cols // 2), d))
+        blk = [2, 2]
+    else:
+        work = ctx.dist.block_work([rows, cols], [2, 2], [rows // nd, cols], devs)
+        blk = [2, 2]
+    buf = np.zeros((rows, cols), np.float32)
+    for it in range(iters):
+        ctx.launch("heat2d", [rows, cols], blk, work, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT)
+        a, b = b, a
+        if host and it % 5 == 2:
+            ctx.read_async(a, buf)
+        if reduce_every and it % reduce_every == 1:
+            w1 = ctx.dist.block_work([rows * cols], [16], [rows * cols // nd], devs)
+            ctx.launch("histogram", [rows * cols], [16], w1, [rows * cols, 8, Arr(x), Arr(h)], "global i => read x[i], reduce(+) hist[:]")
+    return ctx
+
+
+CASES = [dict(workers=1, devices=4, rows=64, cols=32, iters=12),
+         dict(workers=2, devices=2, rows=64, cols=32, iters=12),
+         dict(workers=4, devices=1, rows=64, cols=32, iters=12, strips=True),
+         dict(workers=2, devices=2, rows=64, cols=32, iters=14, host=True, reduce_every=4),
+         dict(workers=2, devices=1, rows=32, cols=16, iters=9, compat=True)]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[str(i) for i in range(len(CASES))])
+def test_replayed_plan_equals_fresh_plan(case):
+    on = _plan(True, **case)
+    off = _plan(False, **case)
+    strip = lambda plan: [{k: v for k, v in t.items() if k != "host"} for t in plan]  # noqa: E731 (host buffer addresses differ)
+    assert strip(on.plan()) == strip(off.plan())
+    assert on.accesses() == off.accesses()
+    assert off.plan_cache_hits() == 0
+    assert on.plan_cache_hits() > 0
+
+
+def test_launch_repeat_equals_python_loop():
+    rows, cols, iters = 64, 32, 11
+
+    def make():
+        ctx = mb.context(workers=2, devices=2, execute=False)
+        devs = ctx.devices
+        dist = lambda: ctx.dist.stencil([rows, cols], [rows // 4, cols], [1, 0], devs)  # noqa: E731
+        a = ctx.create_array([rows, cols], "f32", dist(), 0)
+        b = ctx.create_array([rows, cols], "f32", dist(), 0)
+        return ctx, a, b, ctx.dist.block_work([rows, cols], [2, 2], [rows // 4, cols], devs)
+
+    c1, a, b, w = make()
+    for _ in range(iters):
+        c1.launch("heat2d", [rows, cols], [2, 2], w, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT)
+        a, b = b, a
+    c2, a2, b2, w2 = make()
+    first, last = c2.launch_repeat("heat2d", [rows, cols], [2, 2], w2, [rows, cols, 0.1, Arr(b2), Arr(a2)], HEAT, iters, swap=(a2, b2),
+                                   flush_every=4)
+    assert (first, last) == (c1.plan()[-1]["id"] + 1 - (last - first), c1.plan()[-1]["id"] + 1)
+    assert c1.plan() == c2.plan()
+
+
+def test_reference_shim_launch_repeat_matches(ref):
+    """the same loop through the reference driver (oracle shim mr_launch_repeat)"""
+    import oracle
+    rows, cols = 32, 16
+    ctx = oracle.reference_context(workers=1, devices=2, execute=False)
+    devs = ctx.devices
+    a = ctx.create_array([rows, cols], "f32", ctx.dist.stencil([rows, cols], [rows // 2, cols], [1, 0], devs), 0)
+    b = ctx.create_array([rows, cols], "f32", ctx.dist.stencil([rows, cols], [rows // 2, cols], [1, 0], devs), 0)
+    w = ctx.dist.block_work([rows, cols], [2, 2], [rows // 2, cols], devs)
+    first, last = ctx.launch_repeat("heat2d", [rows, cols], [2, 2], w, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT, 5, swap=(a, b))
+    mine = mb.context(workers=1, devices=2, execute=False, compat_deps=True)
+    md = mine.devices
+    ma = mine.create_array([rows, cols], "f32", mine.dist.stencil([rows, cols], [rows // 2, cols], [1, 0], md), 0)
+    mb_ = mine.create_array([rows, cols], "f32", mine.dist.stencil([rows, cols], [rows // 2, cols], [1, 0], md), 0)
+    mw = mine.dist.block_work([rows, cols], [2, 2], [rows // 2, cols], md)
+    assert mine.launch_repeat("heat2d", [rows, cols], [2, 2], mw, [rows, cols, 0.1, Arr(mb_), Arr(ma)], HEAT, 5, swap=(ma, mb_)) == (first, last)
+    assert mine.plan() == ctx.plan()
+
+
+def test_plan_cache_cuts_small_launch_planning():
+    """C1 shape (4096^2, 4 chunks, one launch per iteration): replayed launches plan in a few us"""
+    def per_launch(cache):
+        rows = cols = 4096
+        with mb.context(workers=1, devices=4, execute=False, retain_plan=False, plan_cache=cache) as ctx:
+            devs = ctx.devices
+            dist = lambda: ctx.dist.stencil([rows, cols], [rows // 4, cols], [1, 0], devs)  # noqa: E731
+            a = ctx.create_array([rows, cols], "f32", dist(), 0)
+            b = ctx.create_array([rows, cols], "f32", dist(), 0)
+            w = ctx.dist.block_work([rows, cols], [16, 16], [rows // 4, cols], devs)
+            ctx.launch_repeat("heat2d", [rows, cols], [16, 16], w, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT, 10, swap=(a, b))
+            t0 = time.perf_counter()
+            ctx.launch_repeat("heat2d", [rows, cols], [16, 16], w, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT, 2000, swap=(a, b), flush_every=10)
+            return (time.perf_counter() - t0) / 2000 * 1e6
+    on, off = min(per_launch(True) for _ in range(3)), min(per_launch(False) for _ in range(3))
+    assert on < 0.6 * off, (on, off)
