@@ -10,7 +10,7 @@ from paper_2202_05549_b200 import Arr
 
 def heat(S, compat, launches=4):
     n = 65536
-    with mb.context(workers=1, devices=1, execute=False, compat_deps=compat) as ctx:
+    with mb.context(workers=1, devices=1, execute=False, compat_deps=compat, plan_cache=False) as ctx:
         devs = ctx.devices
         dist = lambda: ctx.dist.single([n, n], devs[0])  # noqa: E731
         a = ctx.create_array([n, n], "f32", dist(), 0)
@@ -29,7 +29,7 @@ def heat(S, compat, launches=4):
 def hist(S, compat, launches=4):
     n = 1 << 32
     bins = 256
-    with mb.context(workers=1, devices=1, execute=False, compat_deps=compat) as ctx:
+    with mb.context(workers=1, devices=1, execute=False, compat_deps=compat, plan_cache=False) as ctx:
         devs = ctx.devices
         x = ctx.create_array([n], "i32", ctx.dist.single([n], devs[0]), 0)
         h = ctx.create_array([bins], "i64", ctx.dist.single([bins], devs[0]), 0)

@@ -25,7 +25,7 @@ HEAT = "global [i, j] => read in[i-1:i+1, j-1:j+1], write out[i,j]"
 
 def _heat_ms(S, compat=False, launches=5):
     n = 65536
-    with mb.context(workers=1, devices=1, execute=False, compat_deps=compat) as ctx:
+    with mb.context(workers=1, devices=1, execute=False, compat_deps=compat, plan_cache=False) as ctx:
         devs = ctx.devices
         a = ctx.create_array([n, n], "f32", ctx.dist.single([n, n], devs[0]), 0)
         b = ctx.create_array([n, n], "f32", ctx.dist.single([n, n], devs[0]), 0)
@@ -41,7 +41,7 @@ def _heat_ms(S, compat=False, launches=5):
 
 def _hist_ms(S, launches=5):
     n, bins = 1 << 32, 256
-    with mb.context(workers=1, devices=1, execute=False) as ctx:
+    with mb.context(workers=1, devices=1, execute=False, plan_cache=False) as ctx:
         devs = ctx.devices
         x = ctx.create_array([n], "i32", ctx.dist.single([n], devs[0]), 0)
         h = ctx.create_array([bins], "i64", ctx.dist.single([bins], devs[0]), 0)
