@@ -712,7 +712,7 @@ def run_ooc(rows, cols, chunk_rows, capacity_gib, host_gib, iters, warmup, looka
 C1_PER_FLUSH = 10
 
 
-def run_c1(iters, ref_iters, hbm, cpu):
+def run_c1(iters, ref_iters, hbm, cpu, strip=0):
     """BASELINE configs[0] (the reference's CPU scenario): heat2d 4096^2 f32, row-block stencil
     distribution into 4 chunks, one distributed launch per iteration, on one GPU (4 logical
     devices), next to the reference CPU executor on the same grid and chunking."""
@@ -720,7 +720,7 @@ def run_c1(iters, ref_iters, hbm, cpu):
     from paper_2202_05549_b200 import Arr
     rows = cols = 4096
     with mb.context(workers=1, devices=4, num_gpus=1, retain_plan=False) as ctx:
-        a, b, work = setup_heat(ctx, rows, cols, 4)
+        a, b, work = setup_heat(ctx, rows, cols, 4, strip=strip)
 
         def run(n):
             # the reference's repeat/swap loop in one native call (mt_launch_repeat); repeated
@@ -743,7 +743,8 @@ def run_c1(iters, ref_iters, hbm, cpu):
         hits = ctx.plan_cache_hits()
     gbs = BYTES_PER_CELL * rows * cols / (ms / 1e3) / 1e9
     out = {"workload": f"heat2d {rows}x{cols} f32, 4 chunks (stencil_dist halo [1,0]), {iters} iterations, one launch per iteration "
-                       f"(mt_launch_repeat with the a/b swap), handed to the executor every {C1_PER_FLUSH} launches",
+                       f"(mt_launch_repeat with the a/b swap), handed to the executor every {C1_PER_FLUSH} launches"
+                       + (f"; 3 superblocks per chunk ({strip}-row halo-facing strips, interior)" if strip else ""),
            "value": rows * cols / (ms / 1e3), "unit": "cell-updates/s", "ms_per_iter": ms,
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                         "note": "step time incl. planning, halo copies and graph launch; small grid: issue-bound"},
@@ -976,7 +977,7 @@ def run_b200(args):
                 contraction["cpu_baseline"] = {"unavailable": str(e)}
     c1 = None
     if ws == 1 and args.c1:
-        c1 = run_c1(100, args.c1_ref_iters, peaks()[0], rank == 0 and args.cpu_baseline)
+        c1 = run_c1(100, args.c1_ref_iters, peaks()[0], rank == 0 and args.cpu_baseline, strip=args.c1_strip)
     c4 = None
     if args.c4:
         try:
@@ -1058,6 +1059,7 @@ def main():
     p.add_argument("--km-n", type=int, default=1_000_000_000)
     p.add_argument("--no-c1", dest="c1", action="store_false", help="skip the BASELINE configs[0] leg (4096^2, 4 chunks)")
     p.add_argument("--c1-ref-iters", type=int, default=5)
+    p.add_argument("--c1-strip", type=int, default=0, help="C1: rows of the halo-facing superblocks per chunk (0: one superblock per chunk)")
     p.add_argument("--ooc-gib", type=float, default=80.0, help="C5 out-of-core working set (2 arrays), 0 to skip")
     p.add_argument("--ooc-cap-gib", type=float, default=24.0, help="device capacity for the C5 leg (one array must not fit)")
     p.add_argument("--ooc-iters", type=int, default=12)

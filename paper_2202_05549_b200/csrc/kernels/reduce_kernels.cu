@@ -282,15 +282,40 @@ __global__ void __launch_bounds__(1024, 2) histogram_quad_kernel(const int32_t* 
 // The exact distance makes the argmin (first minimum, strict '<') identical to the int64
 // reference (kernels.cpp:283-292). Four points per thread share each broadcast centroid load.
 // Points outside the range take the int64 path.
-template <int kKmPts, int kMinBlocks>
+//
+// Centred FP32 tier (tried first). The argmin is translation invariant, so points and centroids
+// are moved by a per-dimension offset o (the midpoint of the centroid table's range) and the
+// criterion becomes: maximise v = x'.c' - |c'|^2 / 2 (x' = x - o, c' = c - o), the first maximum
+// being the first minimum of the squared distance. One FFMA chain per (point, centroid) starts at
+// -|c'|^2/2 and adds the 16 products: every partial sum is a half-integer of magnitude below
+// sum|x'_q| max|c'| + max|c'|^2/2, checked < 2^23 per point, so each FFMA is exact and the
+// comparison needs no conversion: 16 FFMA + FSETP + 2 SEL per pair (the uncentred tier needs a
+// second chain's FADD, an F2I and integer compare on top). BASELINE C4 data (values < 1000)
+// qualifies after centring (|x'|, |c'| ~ 500).
+template <int kKmPts, int kMinBlocks, int kCU = 1>
 __global__ void __launch_bounds__(256, kMinBlocks) kmeans_assign_fast_kernel(const int32_t* __restrict__ points, int64_t pld, int64_t n_local, int k, int d,
     const int32_t* __restrict__ cents, int64_t cld, int32_t* __restrict__ assign) {
-	extern __shared__ int4 cs4[]; // k rows of 16 values -2c (padded to 16 columns), k |c|^2, k rows of c as f32
+	// k rows of 16 values -2c (padded to 16 columns), k |c|^2, k rows of c as f32, k rows of c' as
+	// f32, k values -|c'|^2/2
+	extern __shared__ int4 cs4[];
 	int32_t* cs = reinterpret_cast<int32_t*>(cs4);
 	uint32_t* cn = reinterpret_cast<uint32_t*>(cs + k * 16);
 	float* cf = reinterpret_cast<float*>(cn + ((k + 3) / 4) * 4);
-	__shared__ int cmax; // max |c| over the table (f32 tier bound)
-	if(threadIdx.x == 0) cmax = 0;
+	float* cz = cf + k * 16;
+	float* hneg = cz + k * 16;
+	__shared__ int cmax;        // max |c| over the table (f32 tier bound)
+	__shared__ int omin[16], omax[16], off[16];
+	__shared__ int czmax;       // max |c'|
+	__shared__ unsigned long long hmax; // max |c'|^2
+	if(threadIdx.x == 0) {
+		cmax = 0;
+		czmax = 0;
+		hmax = 0;
+	}
+	if(threadIdx.x < 16) {
+		omin[threadIdx.x] = INT_MAX;
+		omax[threadIdx.x] = INT_MIN;
+	}
 	__syncthreads();
 	int big = 0, mymax = 0;
 	for(int e = threadIdx.x; e < k * 16; e += blockDim.x) {
@@ -301,10 +326,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) kmeans_assign_fast_kernel(con
 		cs[e] = b ? 0 : -2 * v;
 		cf[e] = b ? 0.f : static_cast<float>(v);
 		mymax = max(mymax, b ? 8192 : abs(v));
+		atomicMin(&omin[q], v);
+		atomicMax(&omax[q], v);
 	}
 	atomicMax(&cmax, mymax);
 	const int cent_big = __syncthreads_or(big);
 	const uint64_t mc = static_cast<uint64_t>(cmax);
+	if(threadIdx.x < 16) off[threadIdx.x] = cent_big ? 0 : (omin[threadIdx.x] + omax[threadIdx.x]) >> 1;
 	for(int c = threadIdx.x; c < k; c += blockDim.x) {
 		uint32_t s = 0;
 		for(int q = 0; q < 16; ++q) {
@@ -314,8 +342,86 @@ __global__ void __launch_bounds__(256, kMinBlocks) kmeans_assign_fast_kernel(con
 		cn[c] = s;
 	}
 	__syncthreads();
+	int myz = 0;
+	for(int e = threadIdx.x; e < k * 16; e += blockDim.x) {
+		const int q = e % 16;
+		const int z = q < d && !cent_big ? static_cast<int>(cf[e]) - off[q] : 0;
+		cz[e] = static_cast<float>(z);
+		myz = max(myz, abs(z));
+	}
+	atomicMax(&czmax, myz);
+	__syncthreads();
+	for(int c = threadIdx.x; c < k; c += blockDim.x) {
+		unsigned long long s = 0;
+		for(int q = 0; q < 16; ++q) {
+			const long long z = static_cast<long long>(cz[c * 16 + q]);
+			s += static_cast<unsigned long long>(z * z);
+		}
+		hneg[c] = -0.5f * static_cast<float>(s); // exact whenever the tier's bound holds (s < 2^24)
+		atomicMax(&hmax, s);
+	}
+	__syncthreads();
+	const uint64_t zc = static_cast<uint64_t>(czmax);
+	const uint64_t hm = hmax;
 	const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * kKmPts;
 	for(int64_t base = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kKmPts; base < n_local; base += stride) {
+		int bi[kKmPts];
+		// centred tier first: its bound, sum|x'_q| max|c'| + max|c'|^2/2 < 2^23 for every point of
+		// the thread (half-integers below 2^23 are exact floats); the point registers of the other
+		// tiers are loaded only when it fails, so the two register sets are never live together
+		bool zok = !cent_big && hm < (uint64_t{1} << 24);
+		float pz[kKmPts][16];
+#pragma unroll
+		for(int j = 0; j < kKmPts; ++j) {
+			const int64_t i = base + j;
+			uint32_t sz = 0;
+#pragma unroll
+			for(int q = 0; q < 16; ++q) {
+				const int32_t v = (i < n_local && q < d) ? points[i * pld + q] : 0;
+				const bool in = v < 8192 && v > -8192;
+				const int32_t z = in ? v - (q < d ? off[q] : 0) : 0;
+				zok &= in;
+				pz[j][q] = static_cast<float>(z);
+				sz += static_cast<uint32_t>(abs(z));
+			}
+			zok &= static_cast<uint64_t>(sz) * zc * 2 + hm < (uint64_t{1} << 24);
+		}
+		if(zok) {
+			float bv[kKmPts];
+#pragma unroll
+			for(int j = 0; j < kKmPts; ++j) {
+				bv[j] = -INFINITY;
+				bi[j] = 0;
+			}
+			const float4* cz4 = reinterpret_cast<const float4*>(cz);
+#pragma unroll kCU
+			for(int c = 0; c < k; ++c) {
+				float cv[16];
+#pragma unroll
+				for(int v4 = 0; v4 < 4; ++v4) {
+					const float4 t = cz4[c * 4 + v4];
+					cv[4 * v4] = t.x;
+					cv[4 * v4 + 1] = t.y;
+					cv[4 * v4 + 2] = t.z;
+					cv[4 * v4 + 3] = t.w;
+				}
+				const float h = hneg[c];
+#pragma unroll
+				for(int j = 0; j < kKmPts; ++j) {
+					float v = h;
+#pragma unroll
+					for(int q = 0; q < 16; ++q) v = fmaf(pz[j][q], cv[q], v);
+					if(v > bv[j]) {
+						bv[j] = v;
+						bi[j] = c;
+					}
+				}
+			}
+#pragma unroll
+			for(int j = 0; j < kKmPts; ++j)
+				if(base + j < n_local) assign[base + j] = bi[j];
+			continue;
+		}
 		uint32_t p[kKmPts][16];
 		uint32_t xx[kKmPts];
 		bool ok = !cent_big;
@@ -338,7 +444,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) kmeans_assign_fast_kernel(con
 			f32ok &= static_cast<uint64_t>(sx) * mc <= (uint64_t{1} << 24);
 		}
 		uint32_t best[kKmPts];
-		int bi[kKmPts];
 #pragma unroll
 		for(int j = 0; j < kKmPts; ++j) {
 			best[j] = 0xFFFFFFFFu;
@@ -567,7 +672,7 @@ int launch_kmeans_assign_i32(const mt_launch_ctx* c, void* stream) {
 	const mt_view& va = c->views[3];
 	const mt_view& vp = c->views[4];
 	const mt_view& vc = c->views[5];
-	const size_t fast_smem = static_cast<size_t>(k) * 16 * 4 * 2 + static_cast<size_t>((k + 3) / 4) * 4 * 4;
+	const size_t fast_smem = static_cast<size_t>(k) * 16 * 4 * 3 + static_cast<size_t>((k + 3) / 4) * 4 * 4 + static_cast<size_t>(k) * 4;
 	const bool fast = d >= 1 && d <= 16 && fast_smem <= 200 * 1024 && vp.stride[1] == 1 && vc.stride[1] == 1 && va.stride[0] == 1 && vc.offset[0] == 0
 	                  && vc.offset[1] == 0 && vp.offset[1] == 0 && vc.extent[0] >= k;
 	if(fast) {
@@ -579,9 +684,22 @@ int launch_kmeans_assign_i32(const mt_launch_ctx* c, void* stream) {
 			kern<<<blocks, 256, fast_smem, s>>>(pts, vp.stride[0], r.total, static_cast<int>(k), static_cast<int>(d), static_cast<const int32_t*>(vc.base),
 			    vc.stride[0], asg);
 		};
-		// 4 points per thread, two 256-thread CTAs per SM (with the FP32 tier: 4x2 47.4 ms, 8x1
-		// 48.2, 6x1 50.4, 2x3 56.7 for 2e8 points; the IMAD-only kernel took 55.1)
-		run(kmeans_assign_fast_kernel<4, 2>, 4, 2);
+		// uncentred FP32 tier (round 1): 4x2 47.4 ms, 8x1 48.2, 6x1 50.4, 2x3 56.7 for 2e8 points;
+		// the IMAD-only kernel took 55.1
+		static const int variant = [] {
+			const char* e = std::getenv("MTB_KM_VARIANT");
+			return e ? std::atoi(e) : 0;
+		}();
+		// measured on 2e8 points (centred tier): 8 points x 1 CTA per SM with the centroid loop
+		// unrolled twice 36.5 ms; 4 x 2 CTAs 39.2 (unrolled) / 41-42 (not); 8 x 1 not unrolled 42.8;
+		// 6 x 1 40.7. MTB_KM_VARIANT selects the others for A/B runs
+		switch(variant) {
+		case 1: run(kmeans_assign_fast_kernel<8, 1>, 8, 1); break;
+		case 2: run(kmeans_assign_fast_kernel<4, 2, 2>, 4, 2); break;
+		case 4: run(kmeans_assign_fast_kernel<6, 1>, 6, 1); break;
+		case 5: run(kmeans_assign_fast_kernel<4, 2>, 4, 2); break;
+		default: run(kmeans_assign_fast_kernel<8, 1, 2>, 8, 1); break;
+		}
 		return cudaGetLastError() == cudaSuccess ? 0 : 1;
 	}
 	const size_t smem = static_cast<size_t>(k * d) * sizeof(int32_t);

@@ -168,15 +168,15 @@ def test_staging_throttle_tight_and_fatal(scenarios, oracle_out):
     it is the reference's fatal footprint error (memory.cpp:278-281)"""
     import json
     sc = scenarios["stencil"]
-    chunk = max_device_working_set(sc, 2, 2) // 2  # one array's chunk on a device (2 arrays per device)
-    with mb.context(workers=2, devices=2, num_gpus=1, staging_threshold=3 * chunk) as ctx:
+    chunk = (64000 + 2) * 4  # one stencil chunk (64000 elements + halo, f32); a task uses two
+    with mb.context(workers=2, devices=2, num_gpus=1, staging_threshold=5 * chunk // 2) as ctx:
         got, coherent = S.run(ctx, sc)
         rep = json.loads(ctx.report_json())
     assert coherent and S.compare(got, oracle_out("stencil"), 1e-6) == []
     assert sum(w["staging_checks"] for w in rep["workers"]) > 0
     assert sum(w["staging_violations"] for w in rep["workers"]) == 0
     with pytest.raises(mb.ExecutionError):
-        with mb.context(workers=2, devices=2, num_gpus=1, staging_threshold=chunk // 2) as ctx:
+        with mb.context(workers=2, devices=2, num_gpus=1, staging_threshold=chunk) as ctx:
             S.run(ctx, sc)
 
 
