@@ -50,6 +50,9 @@ constexpr int STAGES2 = 6;
 constexpr uint32_t B2_STAGE_BYTES = (BN / 2) * BK * 2; // 16 KB
 constexpr uint32_t STAGE2_BYTES = A_STAGE_BYTES + B2_STAGE_BYTES;
 constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + 256;
+constexpr int kTileRing = 4; // dynamic scheduler: tile ids in flight per CTA
+static_assert((2 * STAGES2 + 4 + 2 * kTileRing) * 8 + 4 * kTileRing + 4 <= 256, "barrier area");
+static_assert((2 * STAGES + 4 + 2 * kTileRing) * 8 + 4 * kTileRing + 4 <= 256, "barrier area");
 
 struct gemm_args {
 	float* c;
@@ -62,6 +65,8 @@ struct gemm_args {
 	uint64_t hint_a, hint_b; // L2 cache policies of the operand loads
 	int no_store;            // diagnostics (MTB_GEMM_NOSTORE): skip the C stores
 	int n_major;             // diagnostics (MTB_GEMM_NMAJOR): rasterise N-first
+	unsigned* sched;         // dynamic tile counter (zeroed per launch); null: static round robin
+	unsigned long long* trace; // diagnostics (MTB_GEMM_TRACE): per tile {cluster, start ns, end ns} of the MMA issue
 };
 
 // ---- PTX wrappers -------------------------------------------------------------------------
@@ -135,6 +140,27 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
 	    "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
 	    "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
 	    "r"(rank)
+	    : "memory");
+}
+
+// acquire at cluster scope: the data guarded by the barrier was written by the peer CTA
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+	asm volatile(
+	    "{\n\t.reg .pred P1;\n\t"
+	    "WAIT_%=:\n\t"
+	    "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+	    "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+	    "r"(parity)
+	    : "memory");
+}
+
+// store `v` at `dst`'s offset in CTA `rank`'s shared memory
+__device__ __forceinline__ void st_cluster_u32(uint32_t* dst, uint32_t rank, uint32_t v) {
+	asm volatile(
+	    "{\n\t.reg .b32 ra;\n\t"
+	    "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+	    "st.shared::cluster.u32 [ra], %2;\n\t}" ::"r"(smem_u32(dst)),
+	    "r"(rank), "r"(v)
 	    : "memory");
 }
 
@@ -243,11 +269,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	uint64_t* empty = bars + STAGES;
 	uint64_t* tmem_full = bars + 2 * STAGES;
 	uint64_t* tmem_empty = bars + 2 * STAGES + 2;
-	uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+	uint64_t* tile_full = bars + 2 * STAGES + 4; // dynamic scheduler ring (see the CTA-pair kernel)
+	uint64_t* tile_empty = tile_full + kTileRing;
+	uint32_t* tile_ring = reinterpret_cast<uint32_t*>(tile_empty + kTileRing);
+	uint32_t* tmem_slot = tile_ring + kTileRing;
 
 	const int warp = threadIdx.x / 32;
 	const int lane = threadIdx.x % 32;
 	const int num_tiles = p.m_blocks * p.n_blocks;
+	const bool dyn = p.sched != nullptr;
+	const auto next_tile = [&](int i, int t_static) -> int {
+		if(!dyn) return t_static;
+		const int slot = i % kTileRing;
+		mbar_wait(&tile_full[slot], static_cast<uint32_t>((i / kTileRing) & 1));
+		const int t = static_cast<int>(tile_ring[slot]);
+		mbar_arrive(&tile_empty[slot]);
+		return t;
+	};
 
 	if(warp == 0 && lane == 0) {
 		for(int s = 0; s < STAGES; ++s) {
@@ -257,6 +295,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 		for(int a = 0; a < 2; ++a) {
 			mbar_init(&tmem_full[a], 1);
 			mbar_init(&tmem_empty[a], 4);
+		}
+		for(int r = 0; r < kTileRing; ++r) {
+			mbar_init(&tile_full[r], 1);
+			mbar_init(&tile_empty[r], 5); // MMA + 4 epilogue warps
 		}
 		asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 		asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
@@ -276,7 +318,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			// ---- TMA producer ----
 			int stage = 0;
 			uint32_t phase = 0;
-			for(int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+			for(int i = 0, ts = blockIdx.x;; ++i, ts += gridDim.x) {
+				int t = ts;
+				if(dyn) {
+					const int slot = i % kTileRing;
+					mbar_wait(&tile_empty[slot], static_cast<uint32_t>(((i / kTileRing) & 1) ^ 1));
+					t = static_cast<int>(atomicAdd(p.sched, 1u));
+					tile_ring[slot] = static_cast<uint32_t>(t);
+					mbar_arrive(&tile_full[slot]); // release (cta): the ring entry is visible to the waiters
+				}
+				if(t >= num_tiles) break;
 				int mb, nb;
 				tile_coords(t, p, mb, nb, p.m_blocks);
 				const int32_t arow = static_cast<int32_t>(p.a_row0 + static_cast<int64_t>(mb) * BM);
@@ -299,8 +350,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			constexpr uint32_t idesc = TF32 ? instr_desc_tf32() : instr_desc();
 			int stage = 0;
 			uint32_t phase = 0;
-			int local = 0;
-			for(int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+			for(int local = 0, ts = blockIdx.x;; ++local, ts += gridDim.x) {
+				const int t = next_tile(local, ts);
+				if(t >= num_tiles) break;
 				const int acc = local & 1;
 				mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
 				tc_fence_after();
@@ -329,8 +381,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	} else {
 		// ---- epilogue: warps 2..5, TMEM lanes 32*(warp%4) .. +31 ----
 		const int quarter = warp & 3;
-		int local = 0;
-		for(int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+		for(int local = 0, ts = blockIdx.x;; ++local, ts += gridDim.x) {
+			int t = ts;
+			if(dyn) {
+				if(lane == 0) t = next_tile(local, ts);
+				t = __shfl_sync(0xffffffffu, t, 0);
+			}
+			if(t >= num_tiles) break;
 			int mb, nb;
 			tile_coords(t, p, mb, nb, p.m_blocks);
 			const int acc = local & 1;
@@ -392,7 +449,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	uint64_t* empty = bars + STAGES2;
 	uint64_t* tmem_full = bars + 2 * STAGES2;
 	uint64_t* tmem_empty = bars + 2 * STAGES2 + 2;
-	uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
+	uint64_t* tile_full = bars + 2 * STAGES2 + 4;  // dynamic scheduler ring (kTileRing slots)
+	uint64_t* tile_empty = tile_full + kTileRing;
+	uint32_t* tile_ring = reinterpret_cast<uint32_t*>(tile_empty + kTileRing);
+	uint32_t* tmem_slot = tile_ring + kTileRing;
 
 	const int warp = threadIdx.x / 32;
 	const int lane = threadIdx.x % 32;
@@ -403,6 +463,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	const int first_unit = static_cast<int>(blockIdx.x) / 2;
 	const int unit_stride = static_cast<int>(gridDim.x) / 2;
 	constexpr uint16_t kPair = 0x3;
+	// Tile sequence of this cluster. Static: first_unit, += unit_stride. Dynamic (p.sched): the
+	// leader's producer thread takes the next tile from a global counter and publishes it in both
+	// CTAs' rings; every other role reads it from its own ring. Tiles then start in id order as
+	// clusters free up, so the tiles in flight stay a window of consecutive ids: panels shared by
+	// neighbouring tiles are read at nearly the same K and stay in L2. With a static round robin
+	// the clusters drift apart over a long kernel (221 tiles each at 32768^3) and the shared
+	// panels are re-read from DRAM (ncu: 274 GB of DRAM reads against 73 GB lockstep).
+	const bool dyn = p.sched != nullptr;
+	// consumer side: the i-th tile of this role (sentinel >= num_units ends the loop)
+	const auto next_tile = [&](int i, int t_static, bool release) -> int {
+		if(!dyn) return t_static;
+		const int slot = i % kTileRing;
+		mbar_wait_cluster(&tile_full[slot], static_cast<uint32_t>((i / kTileRing) & 1));
+		const int t = static_cast<int>(tile_ring[slot]);
+		if(release) mbar_arrive_remote(&tile_empty[slot], 0);
+		return t;
+	};
 
 	if(warp == 0 && lane == 0) {
 		for(int s = 0; s < STAGES2; ++s) {
@@ -412,6 +489,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 		for(int a = 0; a < 2; ++a) {
 			mbar_init(&tmem_full[a], 1);
 			mbar_init(&tmem_empty[a], 8);
+		}
+		for(int r = 0; r < kTileRing; ++r) {
+			mbar_init(&tile_full[r], 1);
+			mbar_init(&tile_empty[r], 10); // leader: MMA + 4 epilogue warps; peer: producer + 4 epilogue warps
 		}
 		asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 		asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
@@ -432,7 +513,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			// ---- TMA producer (both CTAs) ----
 			int stage = 0;
 			uint32_t phase = 0;
-			for(int t = first_unit; t < num_units; t += unit_stride) {
+			for(int i = 0, ts = first_unit;; ++i, ts += unit_stride) {
+				int t = ts;
+				if(dyn && leader) {
+					// take the next tile and publish it to both CTAs' rings
+					const int slot = i % kTileRing;
+					mbar_wait(&tile_empty[slot], static_cast<uint32_t>(((i / kTileRing) & 1) ^ 1));
+					t = static_cast<int>(atomicAdd(p.sched, 1u));
+					for(uint32_t r = 0; r < 2; ++r) {
+						st_cluster_u32(&tile_ring[slot], r, static_cast<uint32_t>(t));
+						mbar_arrive_remote(&tile_full[slot], r);
+					}
+				} else if(dyn) {
+					t = next_tile(i, ts, true);
+				}
+				if(t >= num_units) break;
 				int mu, nb;
 				tile_coords(t, p, mu, nb, m_pairs);
 				const int32_t arow = static_cast<int32_t>(p.a_row0 + static_cast<int64_t>(mu) * 2 * BM + rank * BM);
@@ -455,12 +550,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			constexpr uint32_t idesc = TF32 ? instr_desc_tf32(2 * BM) : instr_desc(2 * BM);
 			int stage = 0;
 			uint32_t phase = 0;
-			int local = 0;
-			for(int t = first_unit; t < num_units; t += unit_stride, ++local) {
+			for(int local = 0, ts = first_unit;; ++local, ts += unit_stride) {
+				const int t = next_tile(local, ts, true);
+				if(t >= num_units) break;
 				const int acc = local & 1;
 				mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
 				tc_fence_after();
 				const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+				uint64_t t_start = 0;
+				if(p.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 				for(int kb = 0; kb < p.k_blocks; ++kb) {
 					mbar_wait(&full[stage], phase);
 					tc_fence_after();
@@ -480,13 +578,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 					}
 				}
 				tc_commit2_mc(&tmem_full[acc], kPair);
+				if(p.trace) {
+					uint64_t t_end;
+					asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+					p.trace[3 * t] = blockIdx.x / 2;
+					p.trace[3 * t + 1] = t_start;
+					p.trace[3 * t + 2] = t_end;
+				}
 			}
 		}
 	} else {
 		// ---- epilogue (both CTAs): warps 2..5, own TMEM lanes = own 128 rows ----
 		const int quarter = warp & 3;
-		int local = 0;
-		for(int t = first_unit; t < num_units; t += unit_stride, ++local) {
+		for(int local = 0, ts = first_unit;; ++local, ts += unit_stride) {
+			int t = ts;
+			if(dyn) {
+				if(lane == 0) t = next_tile(local, ts, true);
+				t = __shfl_sync(0xffffffffu, t, 0);
+			}
+			if(t >= num_units) break;
 			int mu, nb;
 			tile_coords(t, p, mu, nb, m_pairs);
 			const int acc = local & 1;
@@ -601,12 +711,33 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	// 16384^3 (677 vs 747), so f32 operands keep single CTAs once K exceeds 8192
 	const bool big = tf32 ? k > 8192 : static_cast<double>(m) * static_cast<double>(n) > 16384.0 * 16384.0 && k > 16384;
 	p.no_store = std::getenv("MTB_GEMM_NOSTORE") != nullptr;
+	if(const char* e = std::getenv("MTB_GEMM_TRACE")) p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(e, nullptr, 0));
 	p.n_major = std::getenv("MTB_GEMM_NMAJOR") != nullptr;
 	const bool force_pair = std::getenv("MTB_GEMM_FORCE_PAIR") != nullptr;
 	const bool pair = p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && (!big || force_pair) && std::getenv("MTB_GEMM_NO_PAIR") == nullptr;
 	CUtensorMap ma, mb;
 	if(!make_map(&ma, a, a_rows, k, lda, BM, tf32) || !make_map(&mb, bt, b_rows, k, ldb, pair ? BN / 2 : BN, tf32)) return 7;
 	g_tc_launches.fetch_add(1, std::memory_order_relaxed);
+	// dynamic tile scheduling (MTB_GEMM_DYNAMIC=1; default: static round robin): a counter per
+	// launch (round robin over a per-device pool, so concurrent launches on other streams never
+	// share one), zeroed on the stream before the launch. Measured (profiles/round2/
+	// gemm_scheduling.md): it removes the CTA-pair kernel's drift (tiles sharing a B panel start
+	// within 38 us instead of 985 us at 32768^3) but not its L2 misses on the A panels, and it is
+	// not faster than the static schedule on either kernel, so it stays opt-in
+	if(std::getenv("MTB_GEMM_DYNAMIC")) {
+		constexpr unsigned kCounters = 1024;
+		static unsigned* counters[64] = {};
+		static unsigned next_counter[64] = {};
+		int dev = 0;
+		cudaGetDevice(&dev);
+		const char* ds = std::getenv("MTB_GEMM_DYN_SINGLE");
+		const bool want = !std::getenv("MTB_GEMM_STATIC") && (pair || !ds || std::atoi(ds) != 0);
+		if(want && dev < 64) {
+			if(!counters[dev] && cudaMalloc(&counters[dev], kCounters * sizeof(unsigned)) != cudaSuccess) counters[dev] = nullptr;
+			unsigned* c = counters[dev] ? counters[dev] + (next_counter[dev]++ % kCounters) : nullptr;
+			if(c && cudaMemsetAsync(c, 0, sizeof(unsigned), s) == cudaSuccess) p.sched = c;
+		}
+	}
 	if(!pair) {
 		const int grid = std::min(p.m_blocks * p.n_blocks, sms);
 		if(tf32) {
@@ -644,6 +775,7 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	}
 	const int units = ((p.m_blocks + 1) / 2) * p.n_blocks;
 	cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(units, max_clusters)));
+
 	if(cudaLaunchKernelEx(&cfg, pair_kernel, ma, mb, p) != cudaSuccess) return 1;
 	return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
