@@ -620,6 +620,67 @@ def run_reference_arm(args):
     }))
 
 
+# FP64-pipe instructions per pair interaction of nbody_tiled_k<3> (DADD 9 + DMUL 10 + DFMA 10 +
+# MUFU 2 per pair: the unrolled loop issues 124 for 4 pairs; cuobjdump -sass of libmanta_b200.so)
+NBODY_DP_PER_PAIR = 31
+
+
+def run_nbody(n, steps, cpu):
+    """nbody_like (the reference kernel, kernels.cpp:369-401: all pairs, f64, bit-exact) on one
+    GPU through the planner: pair interactions per second, roofline = FP64-pipe instructions
+    (NBODY_DP_PER_PAIR per pair) against 148 SMs x 64 FP64 lanes x the SM clock; the reference
+    CPU executor on an n=8192 sample beside it"""
+    import numpy as np
+
+    import paper_2202_05549_b200 as mb
+    from paper_2202_05549_b200 import Arr
+    d = 3
+    with mb.context(workers=1, devices=1, num_gpus=1) as ctx:
+        dv = ctx.devices
+        pos = ctx.create_array([n, d], "f64", ctx.dist.single([n, d], dv[0]), 0)
+        force = ctx.create_array([n, d], "f64", ctx.dist.single([n, d], dv[0]), 0)
+        ctx.write(pos, np.random.default_rng(1).standard_normal((n, d)))
+        w = ctx.dist.block_work([n], [256], [n], dv)
+
+        def step():
+            ctx.launch("nbody_like", [n], [256], w, [n, d, Arr(force), Arr(pos)], "global i => write force[i,:], read pos[:,:]")
+            ctx.flush()
+
+        ms, kms = _timed(ctx, "nbody_like", step, steps)
+    pairs = float(n) * (n - 1)
+    dp_peak = 148 * 64 * 1.965e9
+    out = {"workload": f"nbody_like n={n} d={d} f64 all pairs", "value": pairs / (ms / 1e3), "unit": "pair interactions/s", "ms_per_step": ms,
+           "roofline": {"bound": "fp64 pipe", "achieved": pairs * NBODY_DP_PER_PAIR / (kms / 1e3), "peak": dp_peak, "unit": "FP64 instructions/s",
+                        "frac": pairs * NBODY_DP_PER_PAIR / (kms / 1e3) / dp_peak,
+                        "peak_kind": "derived: 148 SM x 64 FP64 lanes x 1.965 GHz (B200 FP64 37 TFLOP/s = 2 x that)",
+                        "note": f"{NBODY_DP_PER_PAIR} FP64-pipe instructions per pair (IEEE-rounded sqrt and divide for bit-exactness)"}}
+    if cpu:
+        try:
+            import oracle
+            threads = oracle.reference().host_threads()
+            dvn = max(1, min(threads, 64))
+            m = 8192
+            rctx = oracle.reference_context(workers=1, devices=dvn, execute=True)
+            devs = rctx.devices
+            per = ((m + dvn - 1) // dvn + 15) // 16 * 16
+            p2 = rctx.create_array([m, d], "f64", rctx.dist.replicated([m, d], devs), 0)
+            f2 = rctx.create_array([m, d], "f64", rctx.dist.row([m, d], per, devs), 0)
+            rctx.launch("ramp2d", [m, d], [16, 1], rctx.dist.block_work([m, d], [16, 1], [m, d], devs[:1]), [m, d, 1000, -0.5, 1e-3, Arr(p2)],
+                        "global [i, j] => write out[i,j]")
+            rctx.synchronize()
+            t0 = time.perf_counter()
+            rctx.launch("nbody_like", [m], [16], rctx.dist.block_work([m], [16], [per], devs), [m, d, Arr(f2), Arr(p2)],
+                        "global i => write force[i,:], read pos[:,:]")
+            rctx.synchronize()
+            dt = time.perf_counter() - t0
+            rctx.close()
+            out["cpu_baseline"] = {"value": float(m) * (m - 1) / dt, "unit": "pair interactions/s", "cores": dvn, "kind": "reference",
+                                   "sample": f"n={m}, d={d}, 1 worker x {dvn} device threads ({dt:.1f} s)"}
+        except Exception as e:  # noqa: BLE001
+            out["cpu_baseline"] = {"unavailable": str(e)}
+    return out
+
+
 def link_bandwidth(gib=4):
     """pinned host <-> HBM copy bandwidth (GB/s): H2D, D2H and each way with both at once"""
     import torch
@@ -975,6 +1036,9 @@ def run_b200(args):
                 contraction["cpu_baseline"] = cpu_matmul_baseline()
             except Exception as e:  # noqa: BLE001
                 contraction["cpu_baseline"] = {"unavailable": str(e)}
+    nbody = None
+    if ws == 1 and args.nbody_n > 0:
+        nbody = run_nbody(args.nbody_n, 3, rank == 0 and args.cpu_baseline)
     c1 = None
     if ws == 1 and args.c1:
         c1 = run_c1(100, args.c1_ref_iters, peaks()[0], rank == 0 and args.cpu_baseline, strip=args.c1_strip)
@@ -1009,6 +1073,7 @@ def run_b200(args):
             "contraction": contraction,
             "reductions": c4,
             "small_grid": c1,
+            "nbody": nbody,
         }
     if ws > 1:
         import torch.distributed as dist
@@ -1058,6 +1123,7 @@ def main():
     p.add_argument("--strip", type=int, default=128, help="N>1: rows of the halo-facing superblocks per GPU")
     p.add_argument("--km-n", type=int, default=1_000_000_000)
     p.add_argument("--no-c1", dest="c1", action="store_false", help="skip the BASELINE configs[0] leg (4096^2, 4 chunks)")
+    p.add_argument("--nbody-n", type=int, default=65536, help="n-body leg (f64 all pairs, d=3); 0 to skip")
     p.add_argument("--c1-ref-iters", type=int, default=5)
     p.add_argument("--c1-strip", type=int, default=0, help="C1: rows of the halo-facing superblocks per chunk (0: one superblock per chunk)")
     p.add_argument("--ooc-gib", type=float, default=80.0, help="C5 out-of-core working set (2 arrays), 0 to skip")

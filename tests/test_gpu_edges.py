@@ -190,3 +190,44 @@ def test_heat2d_random_layouts(okern):
             got = ctx.read(a)
         want = oracle_heat(okern, x, iters, alpha)
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (case, rows, cols, er, ec, halo, block)
+
+
+def _heat_full(parts, steps):
+    rows = cols = 65536
+    with mb.context(workers=1, devices=parts, num_gpus=1, retain_plan=False) as ctx:
+        devs = ctx.devices
+        dist = lambda: ctx.dist.stencil([rows, cols], [rows // parts, cols], [1, 0], devs)  # noqa: E731
+        a = ctx.create_array([rows, cols], "f32", dist(), 0)
+        b = ctx.create_array([rows, cols], "f32", dist(), 0)
+        work = ctx.dist.block_work([rows, cols], [16, 16], [rows // parts, cols], devs)
+        ctx.launch("ramp2d_f32", [rows, cols], [16, 16], work, [rows, cols, 1000, 0.0, 1.0, Arr(a)], "global [i, j] => write out[i,j]")
+        ctx.launch_repeat("heat2d", [rows, cols], [16, 16], work, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT, steps, swap=(a, b))
+        out = b if steps % 2 else a
+        got = ctx.read(out)
+        assert ctx.replicas_coherent(out)
+    return got
+
+
+def test_heat2d_full_size_multi_step(okern):
+    """BASELINE C2 at full size, several steps: the 4-device run equals the 1-device run bit for
+    bit over all 65536^2 cells (distributed == serial, test_runtime.cpp:67-72), and bands at the
+    chunk boundaries, the domain edges and the middle equal the C oracle, which evolves each band
+    from the ramp with `steps` extra rows on either side (the dependency cone of the stencil)"""
+    rows = cols = 65536
+    steps = 5
+    got = _heat_full(4, steps)
+    serial = _heat_full(1, steps)
+    assert np.array_equal(got.view(np.uint32), serial.view(np.uint32))
+    del serial
+    bands = [(0, 8)] + [(k * rows // 4 - 4, k * rows // 4 + 4) for k in range(1, 4)] + [(rows - 8, rows), (40000, 40008)]
+    for r0, r1 in bands:
+        lo, hi = max(0, r0 - steps), min(rows, r1 + steps)
+        cur = np.ascontiguousarray(ramp_rows(lo, hi, cols))
+        for _ in range(steps):
+            nlo = lo if lo == 0 else lo + 1
+            nhi = hi if hi == rows else hi - 1
+            nxt = np.empty((nhi - nlo, cols), np.float32)
+            okern.oracle_heat2d_rows(C.c_int64(rows), C.c_int64(cols), C.c_double(0.1), cur.ctypes.data_as(F32), C.c_int64(lo), C.c_int64(hi - lo),
+                                     nxt.ctypes.data_as(F32), C.c_int64(nlo), C.c_int64(nhi))
+            cur, lo, hi = nxt, nlo, nhi
+        assert np.array_equal(got[r0:r1].view(np.uint32), cur[r0 - lo:r1 - lo].view(np.uint32)), (r0, r1)
