@@ -548,7 +548,7 @@ def cpu_c4(oracle):
     threads = oracle.reference().host_threads()
     dv = max(1, min(threads, 64))
     res = {}
-    n, bins = 100_000_000, 256
+    n, bins = 1_000_000_000, 256
     ctx = oracle.reference_context(workers=1, devices=dv, execute=True)
     devs = ctx.devices
     per = (n + dv - 1) // dv
@@ -564,7 +564,7 @@ def cpu_c4(oracle):
     dt = time.perf_counter() - t0
     ctx.close()
     res["histogram"] = {"value": n / dt, "unit": "elements/s", "cores": dv, "kind": "reference", "sample": f"n={n}, {bins} bins, {dt:.1f} s"}
-    n, k, d = 400_000, 256, 16
+    n, k, d = 1_000_000, 256, 16  # 1e6 points
     ctx = oracle.reference_context(workers=1, devices=dv, execute=True)
     devs = ctx.devices
     per = ((n + dv - 1) // dv + 255) // 256 * 256
