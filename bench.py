@@ -765,7 +765,10 @@ def run_ooc(rows, cols, chunk_rows, capacity_gib, host_gib, iters, warmup, looka
             "survey_bound_gib_each_way": survey_bound / 2**30,
             "time_over_survey_bound": per_iter / (survey_bound / (bw["duplex_each_way"] * 1e9)) if survey_bound else None,
             "link_gbs": bw, "bound_s_per_iter": bound, "time_over_bound": per_iter / bound if bound else None,
-            "lookahead_tasks": la, "warmup_s": t_setup, "evictions": s1["evictions"] - s0["evictions"]}
+            "lookahead_tasks": la, "warmup_s": t_setup, "evictions": s1["evictions"] - s0["evictions"],
+            "scale_note": "BASELINE configs[4] asks for a 400 GB array; this box has one B200 (180 GB HBM) and ~196 GB of host RAM, "
+                          "so the pinned host tier cannot hold the ~250 GB that must live off-device: the leg runs a working set larger "
+                          "than the capped device capacity instead (profiles/round1/ooc_192gib_over_hbm.json: 192 GiB on the full HBM)"}
 
 
 # launches per mt_flush in the C1 leg: a 10-launch submission is replayed as one CUDA graph whose

@@ -848,7 +848,37 @@ bool tf32_truncate() {
 
 int64_t pad4(int64_t k) { return (k + 3) / 4 * 4; }
 
+// 16-byte form: every row start 16-byte aligned, cols a multiple of 4; each thread moves four
+// float4 per row (independent loads in flight), CTAs stride over rows
+__global__ void round_rows_tf32_v4_k(const float4* __restrict__ src, int64_t ld4_src, float4* __restrict__ dst, int64_t ld4_dst, int64_t rows, int64_t cols4) {
+	for(int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+		const float4* sr = src + r * ld4_src;
+		float4* dr = dst + r * ld4_dst;
+		for(int64_t c0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * 4 + threadIdx.x; c0 < cols4; c0 += static_cast<int64_t>(gridDim.x) * blockDim.x * 4) {
+			float4 v[4];
+#pragma unroll
+			for(int u = 0; u < 4; ++u)
+				if(c0 + u * blockDim.x < cols4) v[u] = __ldcs(sr + c0 + u * blockDim.x);
+#pragma unroll
+			for(int u = 0; u < 4; ++u)
+				if(c0 + u * blockDim.x < cols4) {
+					const float4 t = v[u];
+					dr[c0 + u * blockDim.x] = make_float4(tf32_rne(t.x), tf32_rne(t.y), tf32_rne(t.z), tf32_rne(t.w));
+				}
+		}
+	}
+}
+
 void round_rows(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t rows, int64_t cols, cudaStream_t s) {
+	const bool v4 = cols % 4 == 0 && ld_src % 4 == 0 && ld_dst % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0;
+	if(v4) {
+		const int64_t cols4 = cols / 4;
+		const unsigned gx = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((cols4 + 1023) / 1024, 64)));
+		const unsigned gy = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(rows, 148 * 16 / gx + 1)));
+		round_rows_tf32_v4_k<<<dim3(gx, gy), 256, 0, s>>>(reinterpret_cast<const float4*>(src), ld_src / 4, reinterpret_cast<float4*>(dst), ld_dst / 4, rows,
+		    cols4);
+		return;
+	}
 	const unsigned gx = static_cast<unsigned>(std::min<int64_t>((cols + 255) / 256, 64));
 	const unsigned gy = static_cast<unsigned>(std::min<int64_t>(rows, 65535));
 	round_rows_tf32_k<<<dim3(gx, gy), 256, 0, s>>>(src, ld_src, dst, ld_dst, rows, cols);
