@@ -194,7 +194,7 @@ def host_cpu() -> dict:
 # per host thread, CPU_WARMUP untimed launches, then timed launches in the same context. The
 # reference pipelines consecutive launches across chunks, so its rate climbs over
 # the first few launches; timing after the warm-up gives the steady-state rate either arm sees.
-CPU_ROWS, CPU_WARMUP, CPU_ITERS = 512, 3, 20
+CPU_ROWS, CPU_WARMUP, CPU_ITERS = 512, 10, 60
 
 
 def cpu_reference_rate(rows, cols, iters, devices, bounds_check=True, warmup=CPU_WARMUP) -> tuple[float, float]:
@@ -230,28 +230,30 @@ def cpu_reference_rate(rows, cols, iters, devices, bounds_check=True, warmup=CPU
     return rows * cols * iters / dt, dt
 
 
-def cpu_heat_baseline(cols, iters=CPU_ITERS, bounds_off=True, want_rows=CPU_ROWS) -> dict:
-    """the heat2d CPU baseline under the shared protocol, plus its sensitivity to the sample
-    height (half the rows)"""
-    import oracle
-    threads = oracle.reference().host_threads()
-    devices = max(1, min(threads, 64))
-    rows = sample_rows(want_rows, devices)
-    rate, dt = cpu_reference_rate(rows, cols, iters, devices)
-    half = sample_rows(want_rows // 2, devices)
-    rate_half, _ = cpu_reference_rate(half, cols, iters, devices)
-    out = {"value": rate, "unit": "cell-updates/s", "cores": devices, "kind": "reference",
-           "sample": f"{rows}x{cols} band of the grid, {devices} chunks (stencil_dist halo [1,0]), 1 worker x {devices} device threads, "
-                     f"{CPU_WARMUP} warm-up + {iters} timed launches ({dt:.1f} s)",
-           "bounds_check": "on (the reference default, memory.hpp:54)", "host": host_cpu(),
-           "sensitivity": {"rows": half, "value": rate_half, "ratio": rate_half / rate}}
-    if bounds_off:
-        try:
-            rate_off, dt_off = cpu_reference_rate(rows, cols, iters, devices, bounds_check=False)
-            out["bounds_check_off"] = {"value": rate_off, "seconds": dt_off}
-        except Exception as e:  # noqa: BLE001
-            out["bounds_check_off"] = {"unavailable": str(e)}
-    return out
+def cpu_heat_baseline(cols, rows_total, want_rows=CPU_ROWS, steps=CPU_ITERS, warmup=CPU_WARMUP) -> dict:
+    """the heat2d CPU baseline: the `--impl reference` arm itself, run as a fresh subprocess with
+    the driver-style flags (so both numbers come from one protocol in the same kind of process:
+    no GPU context, clock sampler or pinned host tier beside it), plus its sensitivity to the
+    sample height (half the rows)"""
+    import subprocess
+
+    def arm(rows):
+        env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT")}
+        cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--rows", str(rows_total), "--cols", str(cols),
+               "--cpu-rows", str(rows), "--steps", str(steps), "--warmup", str(warmup)]
+        r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        if r.returncode != 0 or not lines:
+            raise RuntimeError(f"reference arm failed (rc {r.returncode}): {r.stderr[-300:]}")
+        return json.loads(lines[-1])
+
+    full = arm(want_rows)
+    half = arm(want_rows // 2)
+    cb = full["cpu_baseline"]
+    return {"value": full["value"], "unit": "cell-updates/s", "cores": cb["cores"], "kind": "reference",
+            "sample": cb["sample"] + f" ({full['ms_per_step'] * steps / 1e3:.1f} s); the `--impl reference` protocol, run as a subprocess",
+            "bounds_check": "on (the reference default, memory.hpp:54)", "host": cb.get("host"),
+            "sensitivity": {"rows": half["config"]["rows"], "value": half["value"], "ratio": half["value"] / full["value"]}}
 
 
 def cpu_matmul_baseline(sizes=(1024, 2048)) -> dict:
@@ -549,7 +551,11 @@ def cpu_c4(oracle):
     dv = max(1, min(threads, 64))
     res = {}
     n, bins = 1_000_000_000, 256
-    ctx = oracle.reference_context(workers=1, devices=dv, execute=True)
+    # a 1e9-element sample puts 250 MB chunks on each of 16 devices: above the reference's
+    # default staging threshold (64 MiB, memory.hpp:50) and device capacity (256 MiB), so both
+    # are raised (the workload is in-core on the CPU; the limits only model a device)
+    big = {"staging_threshold": 1 << 40, "device_capacity": 1 << 40}
+    ctx = oracle.reference_context(workers=1, devices=dv, execute=True, **big)
     devs = ctx.devices
     per = (n + dv - 1) // dv
     per = (per + 255) // 256 * 256
@@ -565,7 +571,7 @@ def cpu_c4(oracle):
     ctx.close()
     res["histogram"] = {"value": n / dt, "unit": "elements/s", "cores": dv, "kind": "reference", "sample": f"n={n}, {bins} bins, {dt:.1f} s"}
     n, k, d = 1_000_000, 256, 16  # 1e6 points
-    ctx = oracle.reference_context(workers=1, devices=dv, execute=True)
+    ctx = oracle.reference_context(workers=1, devices=dv, execute=True, **big)
     devs = ctx.devices
     per = ((n + dv - 1) // dv + 255) // 256 * 256
     pts = ctx.create_array([n, d], "i32", ctx.dist.row([n, d], per, devs), 0)
@@ -607,9 +613,10 @@ def run_reference_arm(args):
     # the shared protocol (CPU_ROWS band, warm-up launches in the same context), each step one
     # heat iteration over the band; the step count is capped so the arm ends within minutes
     steps = max(1, min(args.steps, 60))
-    rate, dt = cpu_reference_rate(rows, cols, steps, devices, warmup=max(CPU_WARMUP, min(args.warmup, 10)))
+    # the CPU warm-up is the protocol's own (first-touch of the band), not the GPU's W
+    rate, dt = cpu_reference_rate(rows, cols, steps, devices, warmup=CPU_WARMUP)
     sample = (f"{rows}x{cols} band of the {args.rows}x{args.cols} grid, {devices} chunks (stencil_dist halo [1,0]), 1 worker x {devices} "
-              f"device threads, {max(CPU_WARMUP, min(args.warmup, 10))} warm-up + {steps} timed launches")
+              f"device threads, {CPU_WARMUP} warm-up + {steps} timed launches")
     print(json.dumps({
         "metric": METRIC, "impl": "reference", "value": rate, "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3 / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -1002,9 +1009,9 @@ def run_b200(args):
             pass
 
     cpu = None
-    if rank == 0 and args.cpu_baseline:
+    if rank == 0 and ws == 1 and args.cpu_baseline:  # N=1 only (the reference arm covers N>1)
         try:
-            cpu = cpu_heat_baseline(cols, iters=args.cpu_iters, want_rows=args.cpu_rows)
+            cpu = cpu_heat_baseline(cols, rows, want_rows=args.cpu_rows, steps=args.cpu_iters)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "cell-updates/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 

@@ -994,7 +994,9 @@ void executor::accesses_of(const task& t, std::vector<access_t>& out) const {
 			const box whole = full(a.chunk);
 			const bool known = a.access != 0 && whole.rank() == a.region.rank();
 			const box r = known ? intersect(a.region, whole) : whole;
-			const bool dense = t.kern && t.kern->dense_writes;
+			// a trailing partial block's threads outside the grid write nothing (the kernels
+			// guard on their extents), so such a superblock's region is not fully overwritten
+			const bool dense = t.kern && t.kern->dense_writes && t.sb_inside_grid;
 			const bool overwrite = known && (a.access & 2) && !(a.access & 1) && dense;
 			out.push_back({a.chunk, r, !overwrite, overwrite, false});
 		}

@@ -46,6 +46,9 @@ struct task {
 	const struct kernel_entry* kern = nullptr; // global or context-local registry entry
 	device_id device;
 	box sb_blocks, sb_threads;
+	// every thread of sb_threads lies inside the launch grid (no partial trailing block): only
+	// then may a dense_writes kernel's write region count as overwritten (executor spill tier)
+	bool sb_inside_grid = false;
 	point block_size;
 	std::vector<arg_bind> args;
 	// copy

@@ -547,6 +547,7 @@ std::pair<int64_t, int64_t> planner::plan_launch(const std::string& kernel, cons
 		e.device = dev;
 		e.sb_blocks = work[s].blocks;
 		e.sb_threads = sb_threads[s];
+		e.sb_inside_grid = encloses(grid, sb_threads[s]);
 		e.block_size = block;
 		e.args = std::move(binds);
 		const int64_t exec_id = emit(std::move(e));
