@@ -161,7 +161,37 @@ __device__ __forceinline__ void tma_box(float* dst, const CUtensorMap* map, uint
 	    : "memory");
 }
 
-template <int ROWS, int STAGES, int SEG>
+__device__ __forceinline__ void tma_box_hint(float* dst, const CUtensorMap* map, uint64_t* bar, int32_t x, int32_t y, uint64_t pol) {
+	asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+	                 smem_addr(dst)),
+	    "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(x), "r"(y), "l"(pol)
+	    : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+	uint64_t p;
+	asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+	return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+	uint64_t p;
+	asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+	return p;
+}
+
+__device__ __forceinline__ void st_hint(float4* dst, float4 v, uint64_t pol) {
+	asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+
+// L2 residency of a step (template L2 of heat2d_tma_kernel):
+//   0  streaming: outputs stored evict-first (st.global.cs), loads default — grids >> L2
+//   1  L2-resident grids: loads evict-first (the input is dead after this step), outputs
+//      evict-last so the next step's reads of them hit L2
+//   2  loads evict-first, outputs default
+//   3  both default
+
+template <int ROWS, int STAGES, int SEG, int L2 = 0>
 __global__ void __launch_bounds__(kTThreads) heat2d_tma_kernel(const __grid_constant__ CUtensorMap main_map, const __grid_constant__ CUtensorMap halo_map,
     heat_tma_args p) {
 	constexpr uint32_t kHalo = ROWS * 4 <= kTHaloSlot ? kTHaloSlot : ROWS * 4;
@@ -193,9 +223,16 @@ __global__ void __launch_bounds__(kTThreads) heat2d_tma_kernel(const __grid_cons
 		const int32_t y = static_cast<int32_t>(first + static_cast<int64_t>(t) * ROWS - p.in_r0);
 		float* base = st[s];
 		tbar_expect(&full[s], kTStageBytes);
-		tma_box(base, &main_map, &full[s], xm, y);
-		tma_box(base + ROWS * kTCols, &halo_map, &full[s], xm - 4, y);
-		tma_box(base + ROWS * kTCols + (kHalo + 31) / 32 * 32, &halo_map, &full[s], xm + kTCols, y);
+		if constexpr(L2 == 1 || L2 == 2) {
+			const uint64_t pol = policy_evict_first();
+			tma_box_hint(base, &main_map, &full[s], xm, y, pol);
+			tma_box_hint(base + ROWS * kTCols, &halo_map, &full[s], xm - 4, y, pol);
+			tma_box_hint(base + ROWS * kTCols + (kHalo + 31) / 32 * 32, &halo_map, &full[s], xm + kTCols, y, pol);
+		} else {
+			tma_box(base, &main_map, &full[s], xm, y);
+			tma_box(base + ROWS * kTCols, &halo_map, &full[s], xm - 4, y);
+			tma_box(base + ROWS * kTCols + (kHalo + 31) / 32 * 32, &halo_map, &full[s], xm + kTCols, y);
+		}
 	};
 	if(tid == 0)
 		for(int t = 0; t < STAGES && t < tiles; ++t) issue(t);
@@ -225,7 +262,13 @@ __global__ void __launch_bounds__(kTThreads) heat2d_tma_kernel(const __grid_cons
 				o.y = heat_point(cur.y, up.y, v.y, cur.x, cur.z, p.a);
 				o.z = heat_point(cur.z, up.z, v.z, cur.y, cur.w, p.a);
 				o.w = heat_point(cur.w, up.w, v.w, cur.z, cur_r, p.a);
-				__stcs(reinterpret_cast<float4*>(p.out + (k - 1 - p.out_r0) * p.out_ld + (j - p.out_c0)), o);
+				float4* dst = reinterpret_cast<float4*>(p.out + (k - 1 - p.out_r0) * p.out_ld + (j - p.out_c0));
+				if constexpr(L2 == 0)
+					__stcs(dst, o);
+				else if constexpr(L2 == 1)
+					st_hint(dst, o, policy_evict_last());
+				else
+					*dst = o;
 			}
 			up = cur;
 			cur = v;
@@ -268,6 +311,16 @@ bool heat_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int
 	return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
 	           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
 	       == CUDA_SUCCESS;
+}
+
+template <int SEG>
+void launch_tma(int l2, dim3 grid, cudaStream_t s, const CUtensorMap& mm, const CUtensorMap& hm, const heat_tma_args& t) {
+	switch(l2) {
+	case 1: heat2d_tma_kernel<kTRows, kTStages, SEG, 1><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
+	case 2: heat2d_tma_kernel<kTRows, kTStages, SEG, 2><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
+	case 3: heat2d_tma_kernel<kTRows, kTStages, SEG, 3><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
+	default: heat2d_tma_kernel<kTRows, kTStages, SEG, 0><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
+	}
 }
 
 // any shape / alignment: one thread per cell
@@ -346,10 +399,19 @@ int launch_heat2d(const mt_launch_ctx* c, void* stream) {
 			const int64_t segs = (p.r1 - p.r0 + seg - 1) / seg;
 			if(segs <= 65535) {
 				const dim3 grid(static_cast<unsigned>(strips), static_cast<unsigned>(segs));
+				// L2 residency mode (see heat2d_tma_kernel; MTB_HEAT_L2 forces one). A grid whose
+				// whole f32 array fits in half the 126 MB L2 (BASELINE C1: 4096^2 = 64 MiB) keeps
+				// its outputs in L2 for the next step and reads its (dead) inputs evict-first;
+				// larger grids stream. Measured (scripts/diag/heat_l2_modes.sh, B200): C1 4 chunks
+				// 26.2 -> 23.6 us per step (mode 0 -> 2); 16384^2 x 4 chunks 347 us in mode 0,
+				// 391 us in mode 2
+				static const int l2_env = std::getenv("MTB_HEAT_L2") ? std::atoi(std::getenv("MTB_HEAT_L2")) : -1;
+				const bool resident = p.rows * p.cols * 4 <= (int64_t{64} << 20);
+				const int l2 = l2_env >= 0 ? l2_env : (resident ? 2 : 0);
 				if(small)
-					heat2d_tma_kernel<kTRows, kTStages, kTSegSmall><<<grid, kTThreads, 0, s>>>(mm, hm, t);
+					launch_tma<kTSegSmall>(l2, grid, s, mm, hm, t);
 				else
-					heat2d_tma_kernel<kTRows, kTStages, kTSegRows><<<grid, kTThreads, 0, s>>>(mm, hm, t);
+					launch_tma<kTSegRows>(l2, grid, s, mm, hm, t);
 				vec_hi = v_hi;
 			}
 		}

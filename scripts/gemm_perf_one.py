@@ -13,14 +13,15 @@ import paper_2202_05549_b200 as mb  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+pad = int(os.environ.get("GEMM_PAD", "0"))  # extra elements per operand row (row pitch n + pad)
 fn = mb.lib().dll.mt_gemm_bf16_nt
 fn.restype = C.c_int
 fn.argtypes = [C.c_void_p] * 3 + [C.c_int64] * 6 + [C.c_void_p]
-a = torch.rand(n, n, device="cuda").to(torch.bfloat16)
-b = torch.rand(n, n, device="cuda").to(torch.bfloat16)
+a = torch.rand(n, n + pad, device="cuda").to(torch.bfloat16)
+b = torch.rand(n, n + pad, device="cuda").to(torch.bfloat16)
 c = torch.empty(n, n, device="cuda", dtype=torch.float32)
 s = torch.cuda.current_stream().cuda_stream
-call = lambda: fn(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, n, n, n, n, n, s)  # noqa: E731
+call = lambda: fn(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, n, n, n + pad, n + pad, n, s)  # noqa: E731
 for _ in range(2):
     assert call() == 0
 torch.cuda.synchronize()
