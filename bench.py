@@ -493,6 +493,25 @@ def _timed(ctx, kernel, fn, steps):
     return ms / steps, (m1 - m0) / max(1, k1 - k0)
 
 
+def ffma_probe(achieved):
+    """the measured register-operand FFMA ceiling of this box (scripts/microbench/fma_dot.cu:
+    16-term dot products, the assign kernel's inner-loop shape, best of 4 / 8 chains per thread)
+    and the assign kernel's fraction of it"""
+    import ctypes
+    path = os.path.join(ROOT, "scripts", "microbench", "libfma_probe.so")
+    try:
+        lib = ctypes.CDLL(path)
+        lib.mt_probe_ffma_dot.restype = ctypes.c_double
+        lib.mt_probe_ffma_dot.argtypes = [ctypes.c_int]
+        tmacs = lib.mt_probe_ffma_dot(20)
+        if tmacs <= 0:
+            raise RuntimeError("probe failed")
+    except Exception as e:  # noqa: BLE001
+        return {"measured_ffma_ceiling": {"unavailable": str(e)}}
+    return {"measured_ffma_ceiling": {"value": tmacs * 1e12, "unit": "FFMA/s", "source": "scripts/microbench/fma_dot.cu (live, this run)"},
+            "frac_of_measured_ffma": achieved / (tmacs * 1e12)}
+
+
 def run_c4(ctx, hist_n, km_n, steps, hbm, cpu):
     """BASELINE config C4 on one GPU through the planner: histogram (reduce(+) into i64 bins)
     and int32 k-means (d=16, k=256). Step times from device events (all streams joined)."""
@@ -554,10 +573,11 @@ def run_c4(ctx, hist_n, km_n, steps, hbm, cpu):
     out["kmeans"] = {"workload": f"int32 k-means n={n} d={d} k={k}", "value": n / ((a_ms + u_ms) / 1e3), "unit": "points/s (assign + update)",
                      "assign": {"ms": a_kms, "roofline": {"bound": "fp32 fma pipe", "achieved": triples / (a_kms / 1e3), "peak": fma_peak,
                                                            "unit": "(point, centroid, dim) terms/s", "frac": triples / (a_kms / 1e3) / fma_peak,
-                                                           "peak_kind": "derived: 148 SM x 128 FFMA/clk x 1.965 GHz (nominal; register-operand FFMA "
-                                                                        "dot products measure ~90/clk/SM); one exact FFMA per term, the "
-                                                                        "u32 / int64 tiers take over beyond 2^24",
-                                                           "frac_of_imad_bound": triples / (a_kms / 1e3) / (148 * 64 * 1.965e9)}},
+                                                           "peak_kind": "derived: 148 SM x 128 FFMA/clk x 1.965 GHz (nominal; a three-register FFMA "
+                                                                        "issues every 2nd cycle per SMSP, see measured_ffma_ceiling); one exact "
+                                                                        "FFMA per term, the u32 / int64 tiers take over beyond 2^24",
+                                                           "frac_of_imad_bound": triples / (a_kms / 1e3) / (148 * 64 * 1.965e9),
+                                                           **ffma_probe(triples / (a_kms / 1e3))}},
                      "update": {"ms": u_ms, "kernel_ms": u_kms, "roofline": {"bound": "hbm", "achieved": ubytes / (u_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                                                            "frac": ubytes / (u_ms / 1e3) / 1e9 / hbm,
                                                            "note": "68 B/point read-only stream over the step time (consecutive updates overlap)"}},

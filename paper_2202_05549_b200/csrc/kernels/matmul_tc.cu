@@ -51,6 +51,16 @@ constexpr uint32_t B2_STAGE_BYTES = (BN / 2) * BK * 2; // 16 KB
 constexpr uint32_t STAGE2_BYTES = A_STAGE_BYTES + B2_STAGE_BYTES;
 constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + 256;
 constexpr int kTileRing = 4; // dynamic scheduler: tile ids in flight per CTA
+// Wide CTA pair (NSUB = 2): a 256x512 tile per pair, two M256 N256 MMAs per K step into the two
+// halves of the 512 TMEM columns (one accumulator, no double buffering); per CTA a stage holds
+// 128 A rows and 2 x 128 Bt rows = 48 KB, so 4 stages. Per flop it moves half the operand bytes
+// of the single-CTA kernel from L2 (the tile shape cuBLAS picks at 32768^3,
+// nvjet_tst_256x256_64x4_2x1_2cta).
+__host__ __device__ constexpr int pair_stages(int nsub) { return nsub == 1 ? STAGES2 : 4; }
+__host__ __device__ constexpr size_t pair_smem_bytes(int nsub) {
+	return 1024 + static_cast<size_t>(pair_stages(nsub)) * (A_STAGE_BYTES + nsub * B2_STAGE_BYTES) + 256;
+}
+static_assert(pair_smem_bytes(2) <= 227 * 1024, "wide pair stages");
 static_assert((2 * STAGES2 + 4 + 2 * kTileRing) * 8 + 4 * kTileRing + 4 <= 256, "barrier area");
 static_assert((2 * STAGES + 4 + 2 * kTileRing) * 8 + 4 * kTileRing + 4 <= 256, "barrier area");
 
@@ -234,18 +244,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // tile t -> (M unit, N block), rasterised in groups of GROUP_M M units (units = M blocks, or
 // M block pairs for the CTA-pair kernel)
-__device__ __forceinline__ void tile_coords(int t, const gemm_args& p, int& mb, int& nb, int m_units) {
+__device__ __forceinline__ void tile_coords(int t, const gemm_args& p, int& mb, int& nb, int m_units, int n_units) {
 	if(p.n_major) { // diagnostics: groups of group_m N blocks, M fastest across the group
 		const int group = p.group_m * m_units;
 		const int g = t / group;
 		const int first_n = g * p.group_m;
-		const int cols = min(p.group_m, p.n_blocks - first_n);
+		const int cols = min(p.group_m, n_units - first_n);
 		const int r = t % group;
 		nb = first_n + r % cols;
 		mb = r / cols;
 		return;
 	}
-	const int group = p.group_m * p.n_blocks;
+	const int group = p.group_m * n_units;
 	const int g = t / group;
 	const int first_m = g * p.group_m;
 	const int rows = min(p.group_m, m_units - first_m);
@@ -329,7 +339,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 				}
 				if(t >= num_tiles) break;
 				int mb, nb;
-				tile_coords(t, p, mb, nb, p.m_blocks);
+				tile_coords(t, p, mb, nb, p.m_blocks, p.n_blocks);
 				const int32_t arow = static_cast<int32_t>(p.a_row0 + static_cast<int64_t>(mb) * BM);
 				const int32_t brow = static_cast<int32_t>(p.b_row0 + static_cast<int64_t>(nb) * BN);
 				for(int kb = 0; kb < p.k_blocks; ++kb) {
@@ -389,7 +399,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			}
 			if(t >= num_tiles) break;
 			int mb, nb;
-			tile_coords(t, p, mb, nb, p.m_blocks);
+			tile_coords(t, p, mb, nb, p.m_blocks, p.n_blocks);
 			const int acc = local & 1;
 			mbar_wait(&tmem_full[acc], (local >> 1) & 1);
 			tc_fence_after();
@@ -436,20 +446,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // the leader for both); the leader's MMA commit frees the stage in both CTAs and signals both
 // CTAs' `tmem_full`; both CTAs' epilogue warps release the accumulator on the leader's
 // `tmem_empty` (count 8).
-template <bool TF32>
+template <bool TF32, int NSUB>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_nt_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, gemm_args p) {
 	constexpr int BKE = TF32 ? BK / 2 : BK; // K elements per stage
+	constexpr int kStages = pair_stages(NSUB);
+	constexpr uint32_t kBStage = NSUB * B2_STAGE_BYTES;   // this CTA's Bt rows of every N sub-tile
+	constexpr uint32_t kStageBytes = A_STAGE_BYTES + kBStage;
+	constexpr int kAcc = NSUB == 1 ? 2 : 1;               // accumulators in the 512 TMEM columns
+	constexpr int kAccCols = BN * NSUB;                   // columns of one accumulator (= tile N)
 	extern __shared__ uint8_t smem_raw[];
 	uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
 	uint8_t* a_smem = smem;
-	uint8_t* b_smem = smem + STAGES2 * A_STAGE_BYTES;
-	uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+	uint8_t* b_smem = smem + kStages * A_STAGE_BYTES;
+	uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
 	uint64_t* full = bars;
-	uint64_t* empty = bars + STAGES2;
-	uint64_t* tmem_full = bars + 2 * STAGES2;
-	uint64_t* tmem_empty = bars + 2 * STAGES2 + 2;
-	uint64_t* tile_full = bars + 2 * STAGES2 + 4;  // dynamic scheduler ring (kTileRing slots)
+	uint64_t* empty = bars + kStages;
+	uint64_t* tmem_full = bars + 2 * kStages;
+	uint64_t* tmem_empty = bars + 2 * kStages + 2;
+	uint64_t* tile_full = bars + 2 * kStages + 4;  // dynamic scheduler ring (kTileRing slots)
 	uint64_t* tile_empty = tile_full + kTileRing;
 	uint32_t* tile_ring = reinterpret_cast<uint32_t*>(tile_empty + kTileRing);
 	uint32_t* tmem_slot = tile_ring + kTileRing;
@@ -459,7 +474,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	const uint32_t rank = cluster_rank();
 	const bool leader = rank == 0;
 	const int m_pairs = (p.m_blocks + 1) / 2;
-	const int num_units = m_pairs * p.n_blocks;
+	const int n_units = (p.n_blocks + NSUB - 1) / NSUB;
+	const int num_units = m_pairs * n_units;
 	const int first_unit = static_cast<int>(blockIdx.x) / 2;
 	const int unit_stride = static_cast<int>(gridDim.x) / 2;
 	constexpr uint16_t kPair = 0x3;
@@ -482,7 +498,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	};
 
 	if(warp == 0 && lane == 0) {
-		for(int s = 0; s < STAGES2; ++s) {
+		for(int s = 0; s < kStages; ++s) {
 			mbar_init(&full[s], 1);
 			mbar_init(&empty[s], 1);
 		}
@@ -529,15 +545,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 				}
 				if(t >= num_units) break;
 				int mu, nb;
-				tile_coords(t, p, mu, nb, m_pairs);
+				tile_coords(t, p, mu, nb, m_pairs, n_units);
 				const int32_t arow = static_cast<int32_t>(p.a_row0 + static_cast<int64_t>(mu) * 2 * BM + rank * BM);
-				const int32_t brow = static_cast<int32_t>(p.b_row0 + static_cast<int64_t>(nb) * BN + rank * (BN / 2));
+				// sub-tile s of the tile's N: Bt rows [s*BN, (s+1)*BN), this CTA holds half of each
+				const int32_t brow = static_cast<int32_t>(p.b_row0 + static_cast<int64_t>(nb) * kAccCols + rank * (BN / 2));
 				for(int kb = 0; kb < p.k_blocks; ++kb) {
 					mbar_wait(&empty[stage], phase ^ 1);
-					if(leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE2_BYTES);
+					if(leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
 					tma_load_2d_2sm(a_smem + stage * A_STAGE_BYTES, &tmap_a, &full[stage], kb * BKE, arow, p.hint_a);
-					tma_load_2d_2sm(b_smem + stage * B2_STAGE_BYTES, &tmap_b, &full[stage], kb * BKE, brow, p.hint_b);
-					if(++stage == STAGES2) {
+#pragma unroll
+					for(int sub = 0; sub < NSUB; ++sub)
+						tma_load_2d_2sm(b_smem + stage * kBStage + sub * B2_STAGE_BYTES, &tmap_b, &full[stage], kb * BKE, brow + sub * BN, p.hint_b);
+					if(++stage == kStages) {
 						stage = 0;
 						phase ^= 1;
 					}
@@ -553,26 +572,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			for(int local = 0, ts = first_unit;; ++local, ts += unit_stride) {
 				const int t = next_tile(local, ts, true);
 				if(t >= num_units) break;
-				const int acc = local & 1;
-				mbar_wait(&tmem_empty[acc], ((local >> 1) & 1) ^ 1);
+				const int acc = local % kAcc;
+				mbar_wait(&tmem_empty[acc], ((local / kAcc) & 1) ^ 1);
 				tc_fence_after();
-				const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+				const uint32_t d = tmem_base + static_cast<uint32_t>(acc * kAccCols);
 				uint64_t t_start = 0;
 				if(p.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 				for(int kb = 0; kb < p.k_blocks; ++kb) {
 					mbar_wait(&full[stage], phase);
 					tc_fence_after();
 					const uint32_t a0 = smem_u32(a_smem + stage * A_STAGE_BYTES);
-					const uint32_t b0 = smem_u32(b_smem + stage * B2_STAGE_BYTES);
+					const uint32_t b0 = smem_u32(b_smem + stage * kBStage);
 #pragma unroll
 					for(int k = 0; k < BK / UMMA_K; ++k) {
-						if constexpr(TF32)
-							tc_mma2_tf32(d, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0 ? 1u : 0u);
-						else
-							tc_mma2(d, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+#pragma unroll
+						for(int sub = 0; sub < NSUB; ++sub) {
+							const uint32_t dd = d + static_cast<uint32_t>(sub * BN);
+							const uint64_t bd = smem_desc(b0 + sub * B2_STAGE_BYTES + k * UMMA_K * 2);
+							if constexpr(TF32)
+								tc_mma2_tf32(dd, smem_desc(a0 + k * UMMA_K * 2), bd, idesc, (kb | k) != 0 ? 1u : 0u);
+							else
+								tc_mma2(dd, smem_desc(a0 + k * UMMA_K * 2), bd, idesc, (kb | k) != 0 ? 1u : 0u);
+						}
 					}
 					tc_commit2_mc(&empty[stage], kPair);
-					if(++stage == STAGES2) {
+					if(++stage == kStages) {
 						stage = 0;
 						phase ^= 1;
 					}
@@ -598,19 +622,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			}
 			if(t >= num_units) break;
 			int mu, nb;
-			tile_coords(t, p, mu, nb, m_pairs);
-			const int acc = local & 1;
-			mbar_wait(&tmem_full[acc], (local >> 1) & 1);
+			tile_coords(t, p, mu, nb, m_pairs, n_units);
+			const int acc = local % kAcc;
+			mbar_wait(&tmem_full[acc], (local / kAcc) & 1);
 			tc_fence_after();
 			const int64_t row = static_cast<int64_t>(mu) * 2 * BM + rank * BM + quarter * 32 + lane;
 			const bool row_ok = row < p.m && !p.no_store;
 			float* crow = p.c + row * p.ldc;
-			const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
+			const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kAccCols);
 #pragma unroll 1
-			for(int c = 0; c < BN; c += 32) {
+			for(int c = 0; c < kAccCols; c += 32) {
 				uint32_t r[32];
 				tmem_ld32(taddr + static_cast<uint32_t>(c), r);
-				const int64_t col0 = static_cast<int64_t>(nb) * BN + c;
+				const int64_t col0 = static_cast<int64_t>(nb) * kAccCols + c;
 				if(!row_ok) continue;
 				if(col0 + 32 <= p.n && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0)) {
 #pragma unroll
@@ -697,34 +721,44 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	const int64_t bke = tf32 ? BK / 2 : BK;
 	p.k_blocks = static_cast<int>((k + bke - 1) / bke);
 	const int sms = num_sms();
-	p.group_m = GROUP_M;
-	if(const char* e = std::getenv("MTB_GEMM_GROUP")) p.group_m = std::max(1, std::atoi(e));
 	// L2 policies (the CUTLASS encodings): normal 0x1000000000000000, evict-first 0x12F0..., evict-last 0x14F0...
 	p.hint_a = p.hint_b = 0x1000000000000000ull;
 	if(const char* e = std::getenv("MTB_GEMM_HINT_A")) p.hint_a = std::strtoull(e, nullptr, 16);
 	if(const char* e = std::getenv("MTB_GEMM_HINT_B")) p.hint_b = std::strtoull(e, nullptr, 16);
-	// CTA pairs once there are enough 256x256 tiles to fill the machine. Measured (ncu, B200):
-	// pairs are 5-12% faster from 4096^3 to 16384^2 x 32768, but at M = N = K = 32768 they read
-	// ~4x the DRAM bytes of the single-CTA kernel (L2 reuse across the wave is lost; the cause is
-	// not understood yet), so problems with both M*N > 16384^2 and K > 16384 stay on single CTAs.
-	// TF32 (twice the operand bytes per K): pairs win at 8192^3 (830 vs 767 TFLOP/s) and lose from
-	// 16384^3 (677 vs 747), so f32 operands keep single CTAs once K exceeds 8192
-	const bool big = tf32 ? k > 8192 : static_cast<double>(m) * static_cast<double>(n) > 16384.0 * 16384.0 && k > 16384;
+	// Kernel choice (measured on B200 under sustained load, interleaved launches,
+	// scripts/diag/gemm_interleaved_ab.py; profiles/round2/gemm_scheduling.md):
+	//  * CTA pairs (256x256 tiles, static raster in groups of 16 M units) once there are enough
+	//    tiles to fill the machine: best up to 16384^3 (bf16 1532 vs 1214 TFLOP/s single-CTA;
+	//    TF32 735 vs 652);
+	//  * wide CTA pairs (256x512 tiles) with the dynamic tile counter in groups of 4 M units when
+	//    M*N > 16384^2 and K > 16384: 32768^3 bf16 1355 vs 1282 median (single-CTA), TF32 736 vs
+	//    630. The 256x256 pair kernel reads 2-4x the DRAM bytes there (132-301 GB against 69 GB)
+	//    whatever its schedule; the wide tile halves the L2->SM operand bytes per flop and its
+	//    dynamic schedule keeps DRAM reads at the single-CTA kernel's 69 GB.
+	//  * single CTAs (128x256) otherwise.
+	const bool big = static_cast<double>(m) * static_cast<double>(n) > 16384.0 * 16384.0 && k > 16384;
 	p.no_store = std::getenv("MTB_GEMM_NOSTORE") != nullptr;
 	if(const char* e = std::getenv("MTB_GEMM_TRACE")) p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(e, nullptr, 0));
 	p.n_major = std::getenv("MTB_GEMM_NMAJOR") != nullptr;
 	const bool force_pair = std::getenv("MTB_GEMM_FORCE_PAIR") != nullptr;
-	const bool pair = p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && (!big || force_pair) && std::getenv("MTB_GEMM_NO_PAIR") == nullptr;
+	const bool no_pair = std::getenv("MTB_GEMM_NO_PAIR") != nullptr;
+	// MTB_GEMM_WIDE=1 forces the wide pair kernel, =0 disables it
+	const char* we = std::getenv("MTB_GEMM_WIDE");
+	const bool wide_ok = p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * ((p.n_blocks + 1) / 2) * 2 >= sms && !no_pair;
+	const bool wide = wide_ok && (we ? std::atoi(we) != 0 : big && !force_pair);
+	const bool pair = wide || (p.m_blocks >= 2 && ((p.m_blocks + 1) / 2) * p.n_blocks * 2 >= sms && (!big || force_pair) && !no_pair);
+	p.group_m = wide ? 4 : GROUP_M;
+	if(const char* e = std::getenv("MTB_GEMM_GROUP")) p.group_m = std::max(1, std::atoi(e));
 	CUtensorMap ma, mb;
 	if(!make_map(&ma, a, a_rows, k, lda, BM, tf32) || !make_map(&mb, bt, b_rows, k, ldb, pair ? BN / 2 : BN, tf32)) return 7;
 	g_tc_launches.fetch_add(1, std::memory_order_relaxed);
-	// dynamic tile scheduling (MTB_GEMM_DYNAMIC=1; default: static round robin): a counter per
-	// launch (round robin over a per-device pool, so concurrent launches on other streams never
-	// share one), zeroed on the stream before the launch. Measured (profiles/round2/
-	// gemm_scheduling.md): it removes the CTA-pair kernel's drift (tiles sharing a B panel start
-	// within 38 us instead of 985 us at 32768^3) but not its L2 misses on the A panels, and it is
-	// not faster than the static schedule on either kernel, so it stays opt-in
-	if(std::getenv("MTB_GEMM_DYNAMIC")) {
+	// dynamic tile scheduling (default for the wide kernel, MTB_GEMM_DYNAMIC=1 for the others,
+	// MTB_GEMM_STATIC=1 turns it off): a counter per launch (round robin over a per-device pool,
+	// so concurrent launches on other streams never share one), zeroed on the stream before the
+	// launch. It keeps the tiles in flight a window of consecutive ids (tiles sharing a B panel
+	// start within 38 us instead of 985 us at 32768^3 with the static round robin), which the wide
+	// kernel needs to keep its shared panels in L2; on the other kernels it is not faster.
+	if(std::getenv("MTB_GEMM_DYNAMIC") || wide) {
 		constexpr unsigned kCounters = 1024;
 		static unsigned* counters[64] = {};
 		static unsigned next_counter[64] = {};
@@ -749,8 +783,10 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 		}
 		return cudaGetLastError() == cudaSuccess ? 0 : 1;
 	}
-	const auto pair_kernel = tf32 ? gemm_bf16_nt_2sm_kernel<true> : gemm_bf16_nt_2sm_kernel<false>;
-	kern::ensure_smem(pair_kernel, static_cast<int>(SMEM2_BYTES));
+	const auto pair_kernel = wide ? (tf32 ? gemm_bf16_nt_2sm_kernel<true, 2> : gemm_bf16_nt_2sm_kernel<false, 2>)
+	                              : (tf32 ? gemm_bf16_nt_2sm_kernel<true, 1> : gemm_bf16_nt_2sm_kernel<false, 1>);
+	const size_t smem2 = pair_smem_bytes(wide ? 2 : 1);
+	kern::ensure_smem(pair_kernel, static_cast<int>(smem2));
 	cudaLaunchConfig_t cfg{};
 	cudaLaunchAttribute attr[1];
 	attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -758,12 +794,12 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	attr[0].val.clusterDim.y = 1;
 	attr[0].val.clusterDim.z = 1;
 	cfg.blockDim = dim3(NUM_THREADS);
-	cfg.dynamicSmemBytes = SMEM2_BYTES;
+	cfg.dynamicSmemBytes = smem2;
 	cfg.stream = s;
 	cfg.attrs = attr;
 	cfg.numAttrs = 1;
-	static int max_clusters_by_kind[2] = {0, 0};
-	int& max_clusters = max_clusters_by_kind[tf32 ? 1 : 0];
+	static int max_clusters_by_kind[4] = {0, 0, 0, 0};
+	int& max_clusters = max_clusters_by_kind[(tf32 ? 1 : 0) + (wide ? 2 : 0)];
 	if(max_clusters == 0) {
 		cfg.gridDim = dim3(static_cast<unsigned>(sms & ~1));
 		int n_cl = 0;
@@ -773,7 +809,7 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 		if(const char* e = std::getenv("MTB_GEMM_CLUSTERS")) max_clusters = std::max(1, std::atoi(e));
 		if(std::getenv("MTB_GEMM_VERBOSE")) std::fprintf(stderr, "[gemm] max active clusters %d (occupancy query %d)\n", max_clusters, n_cl);
 	}
-	const int units = ((p.m_blocks + 1) / 2) * p.n_blocks;
+	const int units = ((p.m_blocks + 1) / 2) * (wide ? (p.n_blocks + 1) / 2 : p.n_blocks);
 	cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(units, max_clusters)));
 
 	if(cudaLaunchKernelEx(&cfg, pair_kernel, ma, mb, p) != cudaSuccess) return 1;

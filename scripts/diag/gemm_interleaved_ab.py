@@ -2,7 +2,7 @@
 rounds, each running every variant for `per` back-to-back launches (device events per launch),
 so power-cap clock drift hits all variants alike. Prints per-variant median and best TFLOP/s.
   usage: python scripts/diag/gemm_interleaved_ab.py [n] [rounds] [per] variant...
-  variant: single-static | single-dyn-G | pair-static-G | pair-dyn-G"""
+  variant: single-static | single-dyn-G | pair-static-G | pair-dyn-G | wide-static-G | wide-dyn-G"""
 import ctypes as C
 import os
 import statistics
@@ -17,12 +17,13 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 per = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 variants = sys.argv[4:] or ["single-static", "pair-dyn-4"]
-KEYS = ("MTB_GEMM_FORCE_PAIR", "MTB_GEMM_NO_PAIR", "MTB_GEMM_DYNAMIC", "MTB_GEMM_GROUP")
+KEYS = ("MTB_GEMM_FORCE_PAIR", "MTB_GEMM_NO_PAIR", "MTB_GEMM_DYNAMIC", "MTB_GEMM_GROUP", "MTB_GEMM_WIDE")
 
 
 def env_of(v):
     kind, sched, *g = v.split("-")
-    e = {"MTB_GEMM_FORCE_PAIR" if kind == "pair" else "MTB_GEMM_NO_PAIR": "1"}
+    e = {"wide": {"MTB_GEMM_WIDE": "1"}, "pair": {"MTB_GEMM_FORCE_PAIR": "1", "MTB_GEMM_WIDE": "0"},
+         "single": {"MTB_GEMM_NO_PAIR": "1"}}[kind]
     if sched == "dyn":
         e["MTB_GEMM_DYNAMIC"] = "1"
     if g:
@@ -30,11 +31,14 @@ def env_of(v):
     return e
 
 
-fn = mb.lib().dll.mt_gemm_bf16_nt
+tf32 = os.environ.get("GEMM_TF32") == "1"  # f32 operands through mt_gemm_tf32_nt (rounding pass included)
+fn = mb.lib().dll.mt_gemm_tf32_nt if tf32 else mb.lib().dll.mt_gemm_bf16_nt
 fn.restype = C.c_int
 fn.argtypes = [C.c_void_p] * 3 + [C.c_int64] * 6 + [C.c_void_p]
-a = torch.rand(n, n, device="cuda").to(torch.bfloat16)
-b = torch.rand(n, n, device="cuda").to(torch.bfloat16)
+a = torch.rand(n, n, device="cuda")
+b = torch.rand(n, n, device="cuda")
+if not tf32:
+    a, b = a.to(torch.bfloat16), b.to(torch.bfloat16)
 c = torch.empty(n, n, device="cuda", dtype=torch.float32)
 s = torch.cuda.current_stream().cuda_stream
 rates = {v: [] for v in variants}

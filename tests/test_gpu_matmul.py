@@ -200,3 +200,46 @@ def test_matmul_nt_tf32_through_the_planner():
         got = ctx.read(Cm).astype(np.float64)
     want = a.astype(np.float64) @ bt.astype(np.float64).T
     assert (np.abs(got - want) / np.maximum(np.abs(want), 1e-30)).max() <= TF32_REL
+
+
+@pytest.mark.parametrize("kind", ["bf16", "tf32"])
+@pytest.mark.parametrize("m,n,k", [(4096, 4096, 1024), (4224, 4352, 512), (3000, 5000, 776), (2304, 9472, 256)])
+def test_wide_pair_kernel_matches_single_cta(kind, m, n, k, monkeypatch):
+    """the wide CTA-pair kernel (256x512 tiles, two M256 N256 MMAs per K step into the 512 TMEM
+    columns; the default for M*N > 16384^2 with K > 16384, forced here with MTB_GEMM_WIDE=1 at
+    test sizes, dynamic tile counter included) gives bit-identical C to the single-CTA kernel
+    (same K order per element) on ragged M / N / K and odd 512-column unit counts, within 1e-3
+    of fp64"""
+    import torch
+    rng = np.random.default_rng(m * 7 + n + k)
+    a = rng.random((m, k), dtype=np.float32)
+    bt = rng.random((n, k), dtype=np.float32)
+    if kind == "bf16":
+        a, bt = from_bf16_bits(to_bf16_bits(a)), from_bf16_bits(to_bf16_bits(bt))
+        da = torch.from_numpy(to_bf16_bits(a).view(np.int16)).cuda()
+        db = torch.from_numpy(to_bf16_bits(bt).view(np.int16)).cuda()
+        fn = _gemm_fn()
+    else:
+        da, db = torch.from_numpy(a).cuda(), torch.from_numpy(bt).cuda()
+        fn = _tf32_fn()
+
+    def run(env):
+        for key in ("MTB_GEMM_WIDE", "MTB_GEMM_NO_PAIR", "MTB_GEMM_FORCE_PAIR"):
+            monkeypatch.delenv(key, raising=False)
+        for key, v in env.items():
+            monkeypatch.setenv(key, v)
+        dc = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+        assert fn(da.data_ptr(), db.data_ptr(), dc.data_ptr(), m, n, k, k, k, n, torch.cuda.current_stream().cuda_stream) == 0
+        torch.cuda.synchronize()
+        return dc
+
+    mb.lib().dll.mt_tensor_core_launches.restype = C.c_uint64
+    before = mb.lib().dll.mt_tensor_core_launches()
+    wide = run({"MTB_GEMM_WIDE": "1"})
+    single = run({"MTB_GEMM_NO_PAIR": "1"})
+    assert mb.lib().dll.mt_tensor_core_launches() >= before + 2
+    assert torch.isfinite(wide).all()
+    assert torch.equal(wide, single)
+    got = wide.cpu().numpy().astype(np.float64)
+    want = a.astype(np.float64) @ bt.astype(np.float64).T
+    assert (np.abs(got - want) / np.abs(want)).max() <= 1e-3
