@@ -830,15 +830,15 @@ def run_ooc(rows, cols, chunk_rows, capacity_gib, host_gib, iters, warmup, looka
 C1_PER_FLUSH = 10
 
 
-def run_c1(iters, ref_iters, hbm, cpu, strip=0):
+def run_c1(iters, ref_iters, hbm, cpu, strip=0, chunks=4):
     """BASELINE configs[0] (the reference's CPU scenario): heat2d 4096^2 f32, row-block stencil
     distribution into 4 chunks, one distributed launch per iteration, on one GPU (4 logical
     devices), next to the reference CPU executor on the same grid and chunking."""
     import paper_2202_05549_b200 as mb
     from paper_2202_05549_b200 import Arr
     rows = cols = 4096
-    with mb.context(workers=1, devices=4, num_gpus=1, retain_plan=False) as ctx:
-        a, b, work = setup_heat(ctx, rows, cols, 4, strip=strip)
+    with mb.context(workers=1, devices=chunks, num_gpus=1, retain_plan=False) as ctx:
+        a, b, work = setup_heat(ctx, rows, cols, chunks, strip=strip)
 
         def run(n):
             # the reference's repeat/swap loop in one native call (mt_launch_repeat); repeated
@@ -866,7 +866,8 @@ def run_c1(iters, ref_iters, hbm, cpu, strip=0):
            "value": rows * cols / (ms / 1e3), "unit": "cell-updates/s", "ms_per_iter": ms,
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                         "note": "step time incl. planning, halo copies and graph launch; the 64 MiB grid is kept L2-resident between steps (outputs stored with the default policy, dead inputs read evict-first), so the HBM figure is a reference line, not a ceiling"},
-           "graph_replays": st.get("graph_replays"), "plan_cache_hits": hits}
+           "graph_replays": st.get("graph_replays"), "plan_cache_hits": hits, "fused_halo_copies": st.get("fused_copies"),
+           "halo_copies": st.get("copies")}
     if cpu:
         try:
             rate, dt = cpu_reference_rate(rows, cols, ref_iters, 4, warmup=1)
@@ -1075,7 +1076,7 @@ def run_b200(args):
         # the timed region is a few 50 ms launches: a kernel timed alone, so the burst figure
         contraction["roofline"] = {"bound": "tensor", "achieved": kach, "peak": tburst, "unit": "TFLOP/s", "frac": kach / tburst,
                                    "peak_kind": "measured burst (cuBLAS bf16 8192^3, best of 10)", "frac_of_sustained": kach / tpeak,
-                                   "kernel": "gemm_bf16_nt_kernel (tcgen05.mma cta_group::1 M128 N256, TMA, TMEM)"}
+                                   "kernel": "gemm_bf16_nt_2sm_kernel<bf16, wide> (CTA pairs, 256x512 tiles: two tcgen05.mma cta_group::2 M256 N256 per K step, TMA, TMEM, dynamic tile counter)"}
         try:
             cb = cublas_same_size(args.matmul_n, args.matmul_steps)
             contraction["cublas_same_size"] = cb
@@ -1091,7 +1092,7 @@ def run_b200(args):
                 p32, p32_kind = tburst / 2, f"half the measured bf16 burst (cuBLAS TF32 measurement failed: {e})"
             t32["roofline"] = {"bound": "tensor", "achieved": k32, "peak": p32, "unit": "TFLOP/s", "frac": k32 / p32, "peak_kind": p32_kind,
                                "frac_of_half_bf16_burst": k32 / (tburst / 2),
-                               "kernel": "tf32_rne rounding pass + gemm_bf16_nt_kernel<TF32> (tcgen05.mma kind::tf32 M128 N256, TMA, TMEM); "
+                               "kernel": "tf32_rne rounding pass + gemm_bf16_nt_2sm_kernel<TF32, wide> (tcgen05.mma cta_group::2 kind::tf32 M256 N256 x2, TMA, TMEM); "
                                          "kernel_ms includes the rounding pass"}
             contraction["tf32"] = t32
         if rank == 0 and args.cpu_baseline:

@@ -312,7 +312,9 @@ int mt_exec_report_json(mt_exec* ex, char* buf, int64_t cap, int64_t* len);
 /* counters: tasks, device launches, copies, bytes copied, bytes sent, bytes received, peak
  * device bytes, evictions, spill bytes D2H, spill bytes H2D, dead drops (evictions without
  * write-back), dead skips (restores without H2D), host reclaims, host_write bytes, host_read
- * bytes, CUDA-graph captures, CUDA-graph replays (first n of them) */
+ * bytes, CUDA-graph captures, CUDA-graph replays, disk bytes out / in, inter-process messages,
+ * their stream operations, copy tasks fused into their producing kernel (halo mirrors) and their
+ * bytes (first n of them) */
 int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n);
 /* cudaStream_t of the most recent execute task (for event timing on the launching stream) */
 void* mt_exec_last_stream(mt_exec* ex);
@@ -357,7 +359,23 @@ typedef struct mt_launch_ctx {
 	const double* scalars_float; /* per param index */
 	const mt_view* views;        /* per param index (base NULL when unbound) */
 	const void* user;            /* the `user` pointer given at registration */
+	/* Fused halo copies (B200 extension; launchers that ignore them leave mirror_applied at 0 and
+	 * the executor issues the copies itself). Each mirror asks the kernel to store the cells it
+	 * writes into param `param` inside the global box [lo, hi) a second time, into `dst` (another
+	 * chunk: the halo of a neighbouring chunk on this GPU or, over NVLink, on a peer GPU). The
+	 * launcher sets mirror_applied[i] = 1 for each mirror it wrote completely. */
+	int32_t nmirrors;
+	const struct mt_mirror* mirrors;
+	int32_t* mirror_applied;
 } mt_launch_ctx;
+
+typedef struct mt_mirror {
+	int32_t param;
+	int32_t pad_;
+	int64_t lo[MT_MAX_RANK];
+	int64_t hi[MT_MAX_RANK];
+	mt_view dst;
+} mt_mirror;
 
 /* Launcher: enqueue the superblock's work on `stream` (a cudaStream_t) and return 0. */
 typedef int (*mt_launcher_fn)(const mt_launch_ctx* ctx, void* stream);

@@ -110,7 +110,12 @@ class LaunchCtx(C.Structure):
                 ("block_count", C.c_int64 * MAX_RANK), ("block_size", C.c_int64 * MAX_RANK),
                 ("threads_lo", C.c_int64 * MAX_RANK), ("threads_hi", C.c_int64 * MAX_RANK),
                 ("scalars_int", C.POINTER(C.c_int64)), ("scalars_float", C.POINTER(C.c_double)),
-                ("views", C.POINTER(View))]
+                ("views", C.POINTER(View)), ("user", C.c_void_p), ("nmirrors", C.c_int32),
+                ("mirrors", C.c_void_p), ("mirror_applied", C.POINTER(C.c_int32))]
+
+
+class Mirror(C.Structure):
+    _fields_ = [("param", C.c_int32), ("pad_", C.c_int32), ("lo", C.c_int64 * MAX_RANK), ("hi", C.c_int64 * MAX_RANK), ("dst", View)]
 
 
 class ParamSpec(C.Structure):

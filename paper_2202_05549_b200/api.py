@@ -478,7 +478,8 @@ class Context:
             return {}
         keys = ["tasks", "kernels", "copies", "bytes_copied", "bytes_sent", "bytes_received", "peak_device_bytes", "evictions",
                 "spill_bytes_d2h", "spill_bytes_h2d", "dead_drops", "dead_skips", "host_reclaims",
-                "host_write_bytes", "host_read_bytes", "graph_captures", "graph_replays", "bytes_host_to_disk", "bytes_disk_to_host", "messages", "message_ops"]
+                "host_write_bytes", "host_read_bytes", "graph_captures", "graph_replays", "bytes_host_to_disk", "bytes_disk_to_host", "messages", "message_ops",
+                "fused_copies", "bytes_fused"]
         out = (C.c_uint64 * len(keys))()
         self.lib.check(self.lib.exec_stats(ex, out, len(keys)))
         return dict(zip(keys, [int(v) for v in out]))

@@ -627,7 +627,7 @@ int mt_exec_stats(mt_exec* ex, uint64_t* out, int32_t n) {
 		const auto& c = ex->ex->counters();
 		const uint64_t v[] = {c.tasks, c.kernels, c.copies, c.bytes_copied, c.bytes_sent, c.bytes_received, c.peak_device_bytes, c.evictions,
 		    c.bytes_device_to_host, c.bytes_host_to_device, c.dead_drops, c.dead_skips, c.host_reclaims, c.bytes_host_in, c.bytes_host_out,
-		    c.graph_captures, c.graph_replays, c.bytes_host_to_disk, c.bytes_disk_to_host, c.messages, c.message_ops};
+		    c.graph_captures, c.graph_replays, c.bytes_host_to_disk, c.bytes_disk_to_host, c.messages, c.message_ops, c.fused_copies, c.bytes_fused};
 		for(int32_t i = 0; i < n && i < static_cast<int32_t>(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
 	});
 }

@@ -329,12 +329,15 @@ executor::executor(const executor_config& cfg) : cfg_(cfg), rng_state_(cfg.sched
 	}
 	spill_ = cfg.host_capacity > 0;
 	free_events_.resize(static_cast<size_t>(ng));
+	peer_ok_.assign(static_cast<size_t>(ng * ng), 0);
 	for(int a = 0; a < ng; ++a) {
+		peer_ok_[static_cast<size_t>(a * ng + a)] = 1;
 		for(int b = 0; b < ng; ++b) {
 			if(a == b) continue;
 			int can = 0;
 			cudaDeviceCanAccessPeer(&can, ord(a), ord(b));
 			if(!can) continue;
+			peer_ok_[static_cast<size_t>(a * ng + b)] = 1; // kernels on a may store into b's pool
 			cudaSetDevice(ord(a));
 			const cudaError_t pe = cudaDeviceEnablePeerAccess(ord(b), 0);
 			if(pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) check_cuda(pe, "cudaDeviceEnablePeerAccess");
@@ -605,10 +608,44 @@ void executor::end_submit() {
 	issue_batch();
 }
 
+void executor::plan_mirrors(const std::vector<task>& b) {
+	mirror_plan_.clear();
+	if(!fusion_on_ || spill_ || trace_ || cfg_.staging_threshold || cfg_.schedule_seed) return;
+	std::unordered_map<int64_t, const task*> execs;
+	for(const auto& t : b)
+		if(t.kind == task_kind::execute && t.kern && t.kern->mirror_param >= 0) execs[t.id] = &t;
+	if(execs.empty()) return;
+	const int ng = static_cast<int>(gpus_.size());
+	for(const auto& c : b) {
+		if(c.kind != task_kind::copy) continue;
+		const task* e = nullptr;
+		for(const auto d : c.deps) {
+			const auto it = execs.find(d);
+			if(it == execs.end()) continue;
+			const auto& arg = it->second->args[static_cast<size_t>(it->second->kern->mirror_param)];
+			if(arg.kind == arg_kind::chunk && arg.chunk == c.src && (arg.access & 2)) e = it->second;
+		}
+		if(!e) continue;
+		bool older = true; // E may wait for C's other dependencies without reordering anything
+		for(const auto d : c.deps)
+			if(d != e->id && d >= e->id) older = false;
+		const auto s = bufs_.find(c.src), d = bufs_.find(c.dst);
+		if(!older || s == bufs_.end() || d == bufs_.end() || !s->second.ptr || !d->second.ptr || s->second.type != d->second.type) continue;
+		if(d->second.gpu < 0 || d->second.gpu >= ng || !peer_ok_[static_cast<size_t>(s->second.gpu * ng + d->second.gpu)]) continue;
+		auto& v = mirror_plan_[e->id];
+		if(v.size() < 4) v.push_back(&c);
+	}
+}
+
 void executor::issue_batch() {
 	if(gbatch_.empty()) return;
 	std::vector<task> b;
 	b.swap(gbatch_);
+	plan_mirrors(b);
+	struct clear_plan {
+		executor* x;
+		~clear_plan() { x->mirror_plan_.clear(); }
+	} clear{this};
 	int gpu = -1;
 	if(graph_eligible(b, &gpu)) {
 		const std::string sig = signature(b);
@@ -768,6 +805,8 @@ bool executor::capture(const std::vector<task>& b, int gpu, graph_entry& out) {
 	out.kernels = static_cast<int64_t>(ctr_.kernels - before.kernels);
 	out.copies = static_cast<int64_t>(ctr_.copies - before.copies);
 	out.bytes_copied = ctr_.bytes_copied - before.bytes_copied;
+	out.fused_copies = static_cast<int64_t>(ctr_.fused_copies - before.fused_copies);
+	out.bytes_fused = ctr_.bytes_fused - before.bytes_fused;
 	ctr_ = before;
 	if(ok) ++ctr_.graph_captures;
 	return ok;
@@ -800,6 +839,8 @@ void executor::replay(const graph_entry& g, const std::vector<task>& b) {
 	ctr_.kernels += static_cast<uint64_t>(g.kernels);
 	ctr_.copies += static_cast<uint64_t>(g.copies);
 	ctr_.bytes_copied += g.bytes_copied;
+	ctr_.fused_copies += static_cast<uint64_t>(g.fused_copies);
+	ctr_.bytes_fused += g.bytes_fused;
 	++ctr_.graph_replays;
 	if(done_.size() > 16384) retire_completed();
 }
@@ -909,6 +950,13 @@ void executor::unpin(const staged_task& st) {
 }
 
 void executor::issue(const task& t) {
+	if(t.kind == task_kind::copy) {
+		const auto it = mirrored_.find(t.id);
+		if(it != mirrored_.end()) { // stored by its producing kernel, completion already recorded
+			mirrored_.erase(it);
+			return;
+		}
+	}
 	nvtx3::scoped_range_in<nvtx_domain> range{task_kind_name(t.kind)};
 	if(cfg_.staging_threshold && !remote_worker(t.resource.worker)) throttle(t);
 	if(spill_) stage(t);
@@ -1444,6 +1492,17 @@ void executor::run_execute(const task& t) {
 	ldev& L = dev(t.device);
 	cudaStream_t s = pick_compute(t, L);
 	wait_deps(t, s);
+	// fused halo copies planned for this task: the kernel runs after their other dependencies too
+	const auto mp = mirror_plan_.find(t.id);
+	const std::vector<const task*>* fused = mp == mirror_plan_.end() ? nullptr : &mp->second;
+	if(fused)
+		for(const task* c : *fused)
+			for(const auto d : c->deps) {
+				if(d == t.id || (capturing_ && d < capture_first_)) continue;
+				const auto it = done_.find(d);
+				if(it == done_.end() || it->second.stream == s) continue;
+				check_cuda(cudaStreamWaitEvent(s, it->second.ev, 0), "cudaStreamWaitEvent");
+			}
 	const size_t np = t.args.size();
 	std::vector<int64_t> si(np, 0);
 	std::vector<double> sf(np, 0.0);
@@ -1482,6 +1541,35 @@ void executor::run_execute(const task& t) {
 	c.scalars_float = sf.data();
 	c.views = views.data();
 	c.user = k.user;
+	std::vector<mt_mirror> mirrors;
+	std::vector<int32_t> applied;
+	if(fused) {
+		for(const task* cp : *fused) {
+			const buffer& d = buf(cp->dst);
+			mt_mirror m{};
+			m.param = k.mirror_param;
+			const int r = cp->dst_region.rank();
+			for(int q = 0; q < r; ++q) {
+				m.lo[q] = cp->dst_region.lo[q];
+				m.hi[q] = cp->dst_region.hi[q];
+			}
+			m.dst.base = d.ptr;
+			m.dst.dtype = static_cast<int32_t>(d.type);
+			m.dst.rank = d.region.rank();
+			int64_t st[kMaxRank];
+			strides_of(d.region, st);
+			for(int q = 0; q < m.dst.rank; ++q) {
+				m.dst.offset[q] = d.region.lo[q];
+				m.dst.stride[q] = st[q];
+				m.dst.extent[q] = d.region.extent(q);
+			}
+			mirrors.push_back(m);
+		}
+		applied.assign(mirrors.size(), 0);
+		c.nmirrors = static_cast<int32_t>(mirrors.size());
+		c.mirrors = mirrors.data();
+		c.mirror_applied = applied.data();
+	}
 	cudaEvent_t kt0 = nullptr, kt1 = nullptr;
 	if(profile_) {
 		check_cuda(cudaEventCreate(&kt0), "cudaEventCreate");
@@ -1498,6 +1586,14 @@ void executor::run_execute(const task& t) {
 	++ctr_.kernels;
 	last_exec_stream_ = s;
 	finish(t, s);
+	for(size_t i = 0; i < applied.size(); ++i) {
+		if(!applied[i]) continue; // issued as an ordinary copy when its turn comes
+		const task& cp = *(*fused)[i];
+		finish(cp, s);
+		mirrored_[cp.id] = 1;
+		++ctr_.fused_copies;
+		ctr_.bytes_fused += static_cast<uint64_t>(cp.dst_region.volume()) * dtype_size(buf(cp.dst).type);
+	}
 }
 
 void executor::run_copy(const task& t) {

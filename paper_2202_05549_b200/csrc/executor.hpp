@@ -75,6 +75,7 @@ struct exec_counters {
 	uint64_t bytes_host_to_disk = 0, bytes_disk_to_host = 0; // disk tier
 	uint64_t messages = 0;    // inter-process send + recv tasks
 	uint64_t message_ops = 0; // stream operations (kernels, copies, allocations) they enqueued
+	uint64_t fused_copies = 0, bytes_fused = 0; // copy tasks stored by their producing kernel
 };
 
 class executor {
@@ -268,8 +269,8 @@ class executor {
 	struct graph_entry {
 		cudaGraphExec_t exec = nullptr;
 		int gpu = 0;
-		int64_t tasks = 0, kernels = 0, copies = 0;
-		uint64_t bytes_copied = 0;
+		int64_t tasks = 0, kernels = 0, copies = 0, fused_copies = 0;
+		uint64_t bytes_copied = 0, bytes_fused = 0;
 	};
 	bool graphs_on_ = std::getenv("MTB_NO_GRAPHS") == nullptr;
 	bool capturing_ = false;
@@ -284,6 +285,21 @@ class executor {
 	void replay(const graph_entry& g, const std::vector<task>& b);
 	void release_done_event(cudaEvent_t ev, int gpu);
 	void issue_batch();
+
+	// ---- halo copies fused into the producing kernel ---------------------------------------
+	// In a submission, a copy task C whose source region the preceding execute task E writes
+	// (C depends on E, E's kernel declares a mirror param, every other dependency of C is older
+	// than E, and C's destination chunk lives on E's GPU or a peer-accessible one) is handed to
+	// E's launcher as a mirror: the kernel stores those output cells a second time, straight into
+	// the destination chunk. E then also waits for C's other dependencies, and C completes with E.
+	// A launcher that cannot apply a mirror leaves it, and C is issued as an ordinary copy.
+	// Off under spill, tracing, staging throttle or schedule perturbation; MTB_NO_HALO_FUSION=1
+	// disables it.
+	bool fusion_on_ = std::getenv("MTB_NO_HALO_FUSION") == nullptr || std::atoi(std::getenv("MTB_NO_HALO_FUSION")) == 0;
+	std::unordered_map<int64_t, std::vector<const task*>> mirror_plan_; // E id -> copies
+	std::unordered_map<int64_t, int> mirrored_;                         // fused copy ids
+	std::vector<char> peer_ok_;                                          // [a * ngpus + b]
+	void plan_mirrors(const std::vector<task>& b);
 
 	// ---- disk tier (memory.cpp:85-159): host copies of evicted chunks move to a spill file when
 	// the pinned-host tier is full, and come back through a pinned block on restore

@@ -125,12 +125,24 @@ constexpr int kTSegSmall = 16;
 // shared memory at 128-byte aligned addresses)
 constexpr uint32_t kTHaloSlot = 32; // floats (one 128-byte slot fits a 4-column box of up to 8 rows)
 
+// A mirror: output rows [r0, r1) x cols [c0, c1) are also stored at base[(i - row0) * ld + (j -
+// col0)] — the halo rows of a neighbouring chunk (this GPU, or a peer GPU over NVLink), so the
+// halo exchange that follows the step is fused into it (mt_launch_ctx mirrors).
+constexpr int kMaxMirrors = 2;
+struct heat_mirror {
+	int64_t r0, r1, c0, c1;
+	float* base;
+	int64_t row0, col0, ld;
+};
+
 struct heat_tma_args {
 	float* out;
 	int64_t out_r0, out_c0, out_ld;
 	int64_t in_r0, in_c0; // chunk view origin (tensor-map coordinate 0)
 	int64_t r0, r1, c0, c1;
 	float a;
+	int nm; // mirrors in use
+	heat_mirror m[kMaxMirrors];
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -269,6 +281,12 @@ __global__ void __launch_bounds__(kTThreads) heat2d_tma_kernel(const __grid_cons
 					st_hint(dst, o, policy_evict_last());
 				else
 					*dst = o;
+#pragma unroll
+				for(int q = 0; q < kMaxMirrors; ++q) {
+					const heat_mirror& m = p.m[q];
+					if(q < p.nm && k - 1 >= m.r0 && k - 1 < m.r1 && j >= m.c0 && j < m.c1)
+						*reinterpret_cast<float4*>(m.base + (k - 1 - m.row0) * m.ld + (j - m.col0)) = o;
+				}
 			}
 			up = cur;
 			cur = v;
@@ -381,6 +399,21 @@ int launch_heat2d(const mt_launch_ctx* c, void* stream) {
 		if(v_hi > col_lo && heat_map(&mm, p.in, vi.extent[0], vi.extent[1], vi.stride[0], kTCols, kTRows)
 		    && heat_map(&hm, p.in, vi.extent[0], vi.extent[1], vi.stride[0], 4, kTRows)) {
 			heat_tma_args t{};
+			int32_t mirror_idx[kMaxMirrors] = {};
+			// fused halo copies: a mirror is applied when its box lies in the rows and the
+			// vectorised columns this kernel writes, float4-aligned in both chunks
+			for(int32_t i = 0; i < c->nmirrors && c->mirrors && c->mirror_applied; ++i) {
+				const mt_mirror& mr = c->mirrors[i];
+				const mt_view& d = mr.dst;
+				const int64_t mr0 = mr.lo[0], mr1 = mr.hi[0], mc0 = mr.lo[1], mc1 = mr.hi[1];
+				const bool fits = mr.param == 3 && t.nm < kMaxMirrors && d.base && d.rank == 2 && d.stride[1] == 1 && mr0 >= p.r0 && mr1 <= p.r1 && mr0 < mr1
+				                  && mc0 >= col_lo && mc1 <= v_hi && mc0 < mc1 && (mc0 - col_lo) % 4 == 0 && (mc1 - col_lo) % 4 == 0 && d.stride[0] % 4 == 0
+				                  && (mc0 - d.offset[1]) % 4 == 0 && reinterpret_cast<uintptr_t>(d.base) % 16 == 0 && mr0 >= d.offset[0]
+				                  && mr1 <= d.offset[0] + d.extent[0] && mc0 >= d.offset[1] && mc1 <= d.offset[1] + d.extent[1];
+				if(!fits) continue;
+				mirror_idx[t.nm] = i;
+				t.m[t.nm++] = heat_mirror{mr0, mr1, mc0, mc1, static_cast<float*>(d.base), d.offset[0], d.offset[1], d.stride[0]};
+			}
 			t.out = p.out;
 			t.out_r0 = p.out_r0;
 			t.out_c0 = p.out_c0;
@@ -413,6 +446,7 @@ int launch_heat2d(const mt_launch_ctx* c, void* stream) {
 				else
 					launch_tma<kTSegRows>(l2, grid, s, mm, hm, t);
 				vec_hi = v_hi;
+				for(int q = 0; q < t.nm; ++q) c->mirror_applied[mirror_idx[q]] = 1; // written by this launch
 			}
 		}
 	}

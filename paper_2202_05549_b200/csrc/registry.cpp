@@ -46,6 +46,13 @@ void kernel_table::set_dense_writes(const std::string& id) {
 	entries_[static_cast<size_t>(it->second)]->dense_writes = true;
 }
 
+void kernel_table::set_mirror_param(const std::string& id, int param) {
+	std::lock_guard<std::mutex> lock(mu_);
+	const auto it = by_name_.find(id);
+	if(it == by_name_.end()) throw validation_error("unknown kernel \"" + id + "\"");
+	entries_[static_cast<size_t>(it->second)]->mirror_param = param;
+}
+
 int kernel_table::size() const {
 	std::lock_guard<std::mutex> lock(mu_);
 	return static_cast<int>(entries_.size());

@@ -29,6 +29,9 @@ struct kernel_entry {
 	// every cell of a declared `write` region (inside the array domain) is written by the
 	// kernel; lets the spill tier skip restoring data that is about to be overwritten
 	bool dense_writes = false;
+	// param index whose writes the launcher can store a second time into a neighbouring chunk
+	// (mt_launch_ctx mirrors: halo copies fused into the producing kernel); -1: none
+	int mirror_param = -1;
 };
 
 class kernel_table {
@@ -40,6 +43,7 @@ class kernel_table {
 	const kernel_entry& at(int index) const;
 	int size() const;
 	void set_dense_writes(const std::string& id); // see kernel_entry::dense_writes
+	void set_mirror_param(const std::string& id, int param); // see kernel_entry::mirror_param
 
   private:
 	kernel_table();
