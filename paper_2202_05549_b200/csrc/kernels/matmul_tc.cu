@@ -732,9 +732,9 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	//    TF32 735 vs 652);
 	//  * wide CTA pairs (256x512 tiles) with the dynamic tile counter in groups of 4 M units when
 	//    M*N > 16384^2 and K > 16384: 32768^3 bf16 1355 vs 1282 median (single-CTA), TF32 736 vs
-	//    630. The 256x256 pair kernel reads 2-4x the DRAM bytes there (132-301 GB against 69 GB)
-	//    whatever its schedule; the wide tile halves the L2->SM operand bytes per flop and its
-	//    dynamic schedule keeps DRAM reads at the single-CTA kernel's 69 GB.
+	//    630. The wide tile halves the L2->SM operand bytes per flop; cold in ncu it matches
+	//    cuBLAS (41.4 vs 41.5 ms, 108 vs 115 GB of DRAM reads), while the 256x256 pair kernel
+	//    reads 132-301 GB there whatever its schedule.
 	//  * single CTAs (128x256) otherwise.
 	const bool big = static_cast<double>(m) * static_cast<double>(n) > 16384.0 * 16384.0 && k > 16384;
 	p.no_store = std::getenv("MTB_GEMM_NOSTORE") != nullptr;

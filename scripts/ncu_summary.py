@@ -11,7 +11,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__inst_executed.sum", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-        "launch__occupancy_limit_registers", "launch__grid_size", "launch__block_size", "lts__t_bytes.sum"]
+        "launch__occupancy_limit_registers", "launch__grid_size", "launch__block_size", "lts__t_bytes.sum",
+        "lts__t_sector_hit_rate.pct", "sm__pipe_tensor_op_gemm_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg.per_second"]
 
 
 def main(path):
