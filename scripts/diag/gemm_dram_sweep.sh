@@ -10,12 +10,12 @@ variants=${@:-"single-static pair-dyn-4 pair-dyn-8 pair-dyn-16"}
 envs_of() {
   case $1 in
     single-static) echo "MTB_GEMM_NO_PAIR=1" ;;
-    *) echo "unknown variant $1" >&2; exit 1 ;;
     single-dyn-*) echo "MTB_GEMM_NO_PAIR=1 MTB_GEMM_DYNAMIC=1 MTB_GEMM_GROUP=${1##*-}" ;;
     pair-static-*) echo "MTB_GEMM_FORCE_PAIR=1 MTB_GEMM_WIDE=0 MTB_GEMM_GROUP=${1##*-}" ;;
     pair-dyn-*) echo "MTB_GEMM_FORCE_PAIR=1 MTB_GEMM_WIDE=0 MTB_GEMM_DYNAMIC=1 MTB_GEMM_GROUP=${1##*-}" ;;
     wide-dyn-*) echo "MTB_GEMM_WIDE=1 MTB_GEMM_DYNAMIC=1 MTB_GEMM_GROUP=${1##*-}" ;;
     wide-static-*) echo "MTB_GEMM_WIDE=1 MTB_GEMM_STATIC=1 MTB_GEMM_GROUP=${1##*-}" ;;
+    *) echo "unknown variant $1" >&2; exit 1 ;;
   esac
 }
 for v in $variants; do
