@@ -626,6 +626,10 @@ void executor::plan_mirrors(const std::vector<task>& b) {
 			if(arg.kind == arg_kind::chunk && arg.chunk == c.src && (arg.access & 2)) e = it->second;
 		}
 		if(!e) continue;
+		bool aliased = false; // the kernel must not store into a chunk it also reads or writes
+		for(const auto& arg : e->args)
+			if(arg.kind == arg_kind::chunk && arg.chunk == c.dst) aliased = true;
+		if(aliased) continue;
 		bool older = true; // E may wait for C's other dependencies without reordering anything
 		for(const auto d : c.deps)
 			if(d != e->id && d >= e->id) older = false;
