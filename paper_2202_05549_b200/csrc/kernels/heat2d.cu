@@ -203,7 +203,7 @@ __device__ __forceinline__ void st_hint(float4* dst, float4 v, uint64_t pol) {
 //   2  loads evict-first, outputs default
 //   3  both default
 
-template <int ROWS, int STAGES, int SEG, int L2 = 0>
+template <int ROWS, int STAGES, int SEG, int L2 = 0, bool MIRROR = false>
 __global__ void __launch_bounds__(kTThreads) heat2d_tma_kernel(const __grid_constant__ CUtensorMap main_map, const __grid_constant__ CUtensorMap halo_map,
     heat_tma_args p) {
 	constexpr uint32_t kHalo = ROWS * 4 <= kTHaloSlot ? kTHaloSlot : ROWS * 4;
@@ -281,11 +281,13 @@ __global__ void __launch_bounds__(kTThreads) heat2d_tma_kernel(const __grid_cons
 					st_hint(dst, o, policy_evict_last());
 				else
 					*dst = o;
+				if constexpr(MIRROR) {
 #pragma unroll
-				for(int q = 0; q < kMaxMirrors; ++q) {
-					const heat_mirror& m = p.m[q];
-					if(q < p.nm && k - 1 >= m.r0 && k - 1 < m.r1 && j >= m.c0 && j < m.c1)
-						*reinterpret_cast<float4*>(m.base + (k - 1 - m.row0) * m.ld + (j - m.col0)) = o;
+					for(int q = 0; q < kMaxMirrors; ++q) {
+						const heat_mirror& m = p.m[q];
+						if(q < p.nm && k - 1 >= m.r0 && k - 1 < m.r1 && j >= m.c0 && j < m.c1)
+							*reinterpret_cast<float4*>(m.base + (k - 1 - m.row0) * m.ld + (j - m.col0)) = o;
+					}
 				}
 			}
 			up = cur;
@@ -331,14 +333,24 @@ bool heat_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int
 	       == CUDA_SUCCESS;
 }
 
+// the mirror stores are compiled only into the instances that take mirrors (MIRROR), so the
+// plain streaming path keeps its instruction count
+template <int SEG, bool MIRROR>
+void launch_tma_m(int l2, dim3 grid, cudaStream_t s, const CUtensorMap& mm, const CUtensorMap& hm, const heat_tma_args& t) {
+	switch(l2) {
+	case 1: heat2d_tma_kernel<kTRows, kTStages, SEG, 1, MIRROR><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
+	case 2: heat2d_tma_kernel<kTRows, kTStages, SEG, 2, MIRROR><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
+	case 3: heat2d_tma_kernel<kTRows, kTStages, SEG, 3, MIRROR><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
+	default: heat2d_tma_kernel<kTRows, kTStages, SEG, 0, MIRROR><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
+	}
+}
+
 template <int SEG>
 void launch_tma(int l2, dim3 grid, cudaStream_t s, const CUtensorMap& mm, const CUtensorMap& hm, const heat_tma_args& t) {
-	switch(l2) {
-	case 1: heat2d_tma_kernel<kTRows, kTStages, SEG, 1><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
-	case 2: heat2d_tma_kernel<kTRows, kTStages, SEG, 2><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
-	case 3: heat2d_tma_kernel<kTRows, kTStages, SEG, 3><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
-	default: heat2d_tma_kernel<kTRows, kTStages, SEG, 0><<<grid, kTThreads, 0, s>>>(mm, hm, t); break;
-	}
+	if(t.nm > 0)
+		launch_tma_m<SEG, true>(l2, grid, s, mm, hm, t);
+	else
+		launch_tma_m<SEG, false>(l2, grid, s, mm, hm, t);
 }
 
 // any shape / alignment: one thread per cell
