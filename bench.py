@@ -237,10 +237,10 @@ def cpu_heat_baseline(cols, rows_total, want_rows=CPU_ROWS, steps=CPU_ITERS, war
     sample height (half the rows)"""
     import subprocess
 
-    def arm(rows):
+    def arm(rows, bounds="on"):
         env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT")}
         cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--rows", str(rows_total), "--cols", str(cols),
-               "--cpu-rows", str(rows), "--steps", str(steps), "--warmup", str(warmup)]
+               "--cpu-rows", str(rows), "--steps", str(steps), "--warmup", str(warmup), "--cpu-bounds-check", bounds]
         r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
         lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
         if r.returncode != 0 or not lines:
@@ -250,10 +250,16 @@ def cpu_heat_baseline(cols, rows_total, want_rows=CPU_ROWS, steps=CPU_ITERS, war
     full = arm(want_rows)
     half = arm(want_rows // 2)
     cb = full["cpu_baseline"]
-    return {"value": full["value"], "unit": "cell-updates/s", "cores": cb["cores"], "kind": "reference",
-            "sample": cb["sample"] + f" ({full['ms_per_step'] * steps / 1e3:.1f} s); the `--impl reference` protocol, run as a subprocess",
-            "bounds_check": "on (the reference default, memory.hpp:54)", "host": cb.get("host"),
-            "sensitivity": {"rows": half["config"]["rows"], "value": half["value"], "ratio": half["value"] / full["value"]}}
+    out = {"value": full["value"], "unit": "cell-updates/s", "cores": cb["cores"], "kind": "reference",
+           "sample": cb["sample"] + f" ({full['ms_per_step'] * steps / 1e3:.1f} s); the `--impl reference` protocol, run as a subprocess",
+           "bounds_check": "on (the reference default, memory.hpp:54)", "host": cb.get("host"),
+           "sensitivity": {"rows": half["config"]["rows"], "value": half["value"], "ratio": half["value"] / full["value"]}}
+    try:  # the reference with its array_view bounds checks off as well
+        off = arm(want_rows, "off")
+        out["bounds_check_off"] = {"value": off["value"], "ratio": off["value"] / full["value"]}
+    except Exception as e:  # noqa: BLE001
+        out["bounds_check_off"] = {"unavailable": str(e)}
+    return out
 
 
 def cpu_matmul_baseline(sizes=(1024, 2048)) -> dict:
@@ -661,9 +667,10 @@ def run_reference_arm(args):
     # heat iteration over the band; the step count is capped so the arm ends within minutes
     steps = max(1, min(args.steps, 60))
     # the CPU warm-up is the protocol's own (first-touch of the band), not the GPU's W
-    rate, dt = cpu_reference_rate(rows, cols, steps, devices, warmup=CPU_WARMUP)
+    rate, dt = cpu_reference_rate(rows, cols, steps, devices, warmup=CPU_WARMUP, bounds_check=args.cpu_bounds_check == "on")
     sample = (f"{rows}x{cols} band of the {args.rows}x{args.cols} grid, {devices} chunks (stencil_dist halo [1,0]), 1 worker x {devices} "
-              f"device threads, {CPU_WARMUP} warm-up + {steps} timed launches")
+              f"device threads, {CPU_WARMUP} warm-up + {steps} timed launches"
+              + ("" if args.cpu_bounds_check == "on" else ", array_view bounds checks off"))
     print(json.dumps({
         "metric": METRIC, "impl": "reference", "value": rate, "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3 / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -1179,6 +1186,8 @@ def main():
     p.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     p.add_argument("--cpu-rows", type=int, default=CPU_ROWS, help="rows of the heat CPU-baseline band (both arms)")
     p.add_argument("--cpu-iters", type=int, default=CPU_ITERS, help="timed launches of the main arm's heat CPU baseline")
+    p.add_argument("--cpu-bounds-check", choices=["on", "off"], default="on",
+                   help="--impl reference: the reference's array_view bounds checks (memory.hpp:54; default on, as shipped)")
     p.add_argument("--matmul-n", type=int, default=32768, help="C3 contraction size (0 to skip)")
     p.add_argument("--matmul-steps", type=int, default=5)
     p.add_argument("--tf32-steps", type=int, default=3, help="steps of the C3 fp32 (TF32) contraction leg (0 to skip)")
