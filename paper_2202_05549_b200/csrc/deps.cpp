@@ -49,17 +49,62 @@ dep_tracker::key dep_tracker::key_of(const state& s, const box& b) {
 	return k;
 }
 
+void dep_tracker::reader_list::insert(int64_t task) {
+	int64_t* const p = std::lower_bound(begin(), end(), task);
+	if(p != end() && *p == task) return;
+	const size_t at = static_cast<size_t>(p - begin());
+	if(!heap_on_ && n_ < kInline) {
+		std::copy_backward(inline_ + at, inline_ + n_, inline_ + n_ + 1);
+		inline_[at] = task;
+		++n_;
+		return;
+	}
+	if(!heap_on_) {
+		heap_.assign(inline_, inline_ + n_);
+		heap_on_ = true;
+	}
+	heap_.insert(heap_.begin() + static_cast<std::ptrdiff_t>(at), task);
+	++n_;
+}
+
+bool dep_tracker::reader_list::operator==(const reader_list& o) const { return n_ == o.n_ && std::equal(begin(), end(), o.begin()); }
+
+void dep_tracker::count_extent(state& s, int64_t e, int64_t by) {
+	auto& v = s.extents;
+	auto it = std::lower_bound(v.begin(), v.end(), e, [](const std::pair<int64_t, int64_t>& x, int64_t y) { return x.first < y; });
+	if(it != v.end() && it->first == e) {
+		if((it->second += by) == 0) v.erase(it);
+	} else {
+		v.insert(it, {e, by});
+	}
+}
+
+std::vector<std::map<dep_tracker::key, dep_tracker::cell>::node_type>& dep_tracker::spare_nodes() {
+	static thread_local std::vector<std::map<key, cell>::node_type> spare;
+	return spare;
+}
+
 void dep_tracker::insert(state& s, cell&& c) {
-	++s.extents[c.region.hi[s.axis] - c.region.lo[s.axis]];
+	count_extent(s, c.region.hi[s.axis] - c.region.lo[s.axis], 1);
 	const key k = key_of(s, c.region);
+	auto& spare = spare_nodes();
+	if(!spare.empty()) {
+		auto nh = std::move(spare.back());
+		spare.pop_back();
+		nh.key() = k;
+		nh.mapped() = std::move(c);
+		s.cells.insert(std::move(nh));
+		return;
+	}
 	s.cells.emplace(k, std::move(c));
 }
 
 dep_tracker::cell dep_tracker::take(state& s, std::map<key, cell>::iterator it) {
-	cell c = std::move(it->second);
-	s.cells.erase(it);
-	const auto e = s.extents.find(c.region.hi[s.axis] - c.region.lo[s.axis]);
-	if(--e->second == 0) s.extents.erase(e);
+	auto nh = s.cells.extract(it);
+	cell c = std::move(nh.mapped());
+	auto& spare = spare_nodes();
+	if(spare.size() < 4096) spare.push_back(std::move(nh));
+	count_extent(s, c.region.hi[s.axis] - c.region.lo[s.axis], -1);
 	return c;
 }
 
@@ -67,7 +112,7 @@ dep_tracker::cell dep_tracker::take(state& s, std::map<key, cell>::iterator it) 
 // (q.lo - max_extent, q.hi): the scan starts there and stops at q.hi.
 void dep_tracker::extract(state& s, const box& q, std::vector<cell>& out) {
 	const int ax = s.axis;
-	const int64_t reach = s.extents.empty() ? 0 : s.extents.rbegin()->first;
+	const int64_t reach = dep_tracker::reach(s);
 	key from{std::numeric_limits<int64_t>::min(), std::numeric_limits<int64_t>::min(), std::numeric_limits<int64_t>::min()};
 	from[0] = q.lo[ax] - reach + 1;
 	auto it = s.cells.lower_bound(from);
@@ -115,20 +160,44 @@ void dep_tracker::split(cell&& c, const box& cut, std::vector<cell>& inside, std
 	box rest = c.region;
 	for(int k = 0; k < rest.rank(); ++k) {
 		if(rest.lo[k] < cut.lo[k]) {
-			cell piece{rest, c.writer, c.readers};
+			cell piece{rest, c.writer, c.readers, c.partial};
 			piece.region.hi[k] = cut.lo[k];
+			clip_partial(piece);
 			outside.push_back(std::move(piece));
 			rest.lo[k] = cut.lo[k];
 		}
 		if(cut.hi[k] < rest.hi[k]) {
-			cell piece{rest, c.writer, c.readers};
+			cell piece{rest, c.writer, c.readers, c.partial};
 			piece.region.lo[k] = cut.hi[k];
+			clip_partial(piece);
 			outside.push_back(std::move(piece));
 			rest.hi[k] = cut.hi[k];
 		}
 	}
 	c.region = rest;
+	clip_partial(c);
 	inside.push_back(std::move(c));
+}
+
+void dep_tracker::clip_partial(cell& c) {
+	if(c.partial.empty()) return;
+	size_t out = 0;
+	for(size_t i = 0; i < c.partial.size(); ++i) {
+		partial_read p = c.partial[i];
+		if(!overlaps(p.region, c.region)) continue;
+		p.region = intersect(p.region, c.region);
+		if(p.region == c.region) {
+			c.readers.insert(p.task);
+			continue;
+		}
+		c.partial[out++] = p;
+	}
+	c.partial.resize(out);
+	// a task now a full reader needs no partial entries
+	if(!c.partial.empty())
+		c.partial.erase(std::remove_if(c.partial.begin(), c.partial.end(),
+		                    [&](const partial_read& p) { return std::binary_search(c.readers.begin(), c.readers.end(), p.task); }),
+		    c.partial.end());
 }
 
 // true (and the merged box in `out`) when two cells' union is a box
@@ -160,7 +229,7 @@ void dep_tracker::settle(state& s, const box& touched) {
 		again = false;
 		near.clear();
 		const int ax = s.axis;
-		const int64_t reach = s.extents.empty() ? 0 : s.extents.rbegin()->first;
+		const int64_t reach = dep_tracker::reach(s);
 		key from{std::numeric_limits<int64_t>::min(), std::numeric_limits<int64_t>::min(), std::numeric_limits<int64_t>::min()};
 		from[0] = grown.lo[ax] - reach + 1;
 		for(auto it = s.cells.lower_bound(from); it != s.cells.end() && it->first[0] < grown.hi[ax]; ++it) {
@@ -172,7 +241,7 @@ void dep_tracker::settle(state& s, const box& touched) {
 				const cell& x = near[a]->second;
 				const cell& y = near[b]->second;
 				box u;
-				if(x.writer != y.writer || x.readers != y.readers || !mergeable(x.region, y.region, u)) continue;
+				if(x.writer != y.writer || x.readers != y.readers || !x.partial.empty() || !y.partial.empty() || !mergeable(x.region, y.region, u)) continue;
 				cell m = take(s, near[a]);
 				take(s, near[b]);
 				m.region = u;
@@ -189,49 +258,59 @@ void dep_tracker::read(int64_t chunk, int64_t task, const box& region_in, std::v
 	state& s = get(chunk);
 	const box region = compat_ ? s.region : intersect(region_in, s.region);
 	if(region.is_empty()) return;
-	// scratch lists reused across calls (the planner is single-threaded per context; thread_local
-	// keeps contexts on different threads apart)
-	static thread_local std::vector<cell> hit, inside, outside;
-	hit.clear();
-	inside.clear();
-	outside.clear();
-	// cells inside the box only gain a reader (in place); cells it cuts are split
+	// cells the box encloses gain a full reader, cells it cuts a partial one; the map is not
+	// touched (no split, no coalescing)
 	const int ax = s.axis;
-	const int64_t reach = s.extents.empty() ? 0 : s.extents.rbegin()->first;
+	const int64_t reach = dep_tracker::reach(s);
 	key from{std::numeric_limits<int64_t>::min(), std::numeric_limits<int64_t>::min(), std::numeric_limits<int64_t>::min()};
 	from[0] = region.lo[ax] - reach + 1;
 	int64_t probes = 0;
-	for(auto it = s.cells.lower_bound(from); it != s.cells.end() && it->first[0] < region.hi[ax];) {
+	static thread_local std::vector<key> split_later;
+	static thread_local std::vector<cell> inside, outside;
+	split_later.clear();
+	for(auto it = s.cells.lower_bound(from); it != s.cells.end() && it->first[0] < region.hi[ax]; ++it) {
 		++probes;
 		cell& c = it->second;
-		if(!overlaps(c.region, region)) {
-			++it;
-			continue;
-		}
+		if(!overlaps(c.region, region)) continue;
 		++s.hits;
 		if(c.writer >= 0) deps.push_back(c.writer);
 		if(encloses(region, c.region)) {
-			const auto r = std::lower_bound(c.readers.begin(), c.readers.end(), task);
-			if(r == c.readers.end() || *r != task) c.readers.insert(r, task);
-			++it;
+			c.readers.insert(task);
 			continue;
 		}
-		const auto cur = it++;
-		hit.push_back(take(s, cur));
+		if(std::binary_search(c.readers.begin(), c.readers.end(), task)) continue;
+		const box part = intersect(region, c.region);
+		bool covered = false;
+		for(const auto& p : c.partial)
+			if(p.task == task && encloses(p.region, part)) covered = true;
+		if(covered) continue;
+		if(c.partial.size() < kMaxPartial) {
+			c.partial.push_back({task, part});
+			continue;
+		}
+		// too many partial readers on one cell (band reads of one big chunk): cut the box out of
+		// it, so the cell map converges to the read pattern and the lists stay short
+		split_later.push_back(it->first);
 	}
 	s.probes += probes;
-	if(hit.empty()) return;
-	for(auto& c : hit) split(std::move(c), region, inside, outside);
-	for(auto& c : inside) {
-		const auto it = std::lower_bound(c.readers.begin(), c.readers.end(), task);
-		if(it == c.readers.end() || *it != task) c.readers.insert(it, task);
-		insert(s, std::move(c));
+	for(const key& k : split_later) {
+		const auto it = s.cells.find(k);
+		cell c = take(s, it);
+		split(std::move(c), region, inside, outside);
+		for(auto& piece : inside) {
+			piece.readers.insert(task);
+			insert(s, std::move(piece));
+		}
+		for(auto& piece : outside) insert(s, std::move(piece));
+		inside.clear();
+		outside.clear();
 	}
-	for(auto& c : outside) insert(s, std::move(c));
-	hit.clear();
-	inside.clear();
-	outside.clear();
-	settle(s, region);
+	if(!split_later.empty()) {
+		split_later.clear();
+		settle(s, region);
+		return;
+	}
+	reindex(s);
 }
 
 void dep_tracker::write(int64_t chunk, int64_t task, const box& region_in, std::vector<int64_t>& deps) {
@@ -247,6 +326,8 @@ void dep_tracker::write(int64_t chunk, int64_t task, const box& region_in, std::
 		if(c.writer >= 0) deps.push_back(c.writer);
 		for(const auto r : c.readers)
 			if(r != task) deps.push_back(r);
+		for(const auto& p : c.partial)
+			if(p.task != task && overlaps(p.region, region)) deps.push_back(p.task);
 		split(std::move(c), region, inside, outside);
 	}
 	for(auto& c : outside) insert(s, std::move(c));
@@ -269,10 +350,12 @@ bool dep_tracker::matches(int64_t chunk, const snapshot& snap, int64_t delta) co
 	for(auto x = a.cells.begin(), y = b.cells.begin(); x != a.cells.end(); ++x, ++y) {
 		const cell& c = x->second;
 		const cell& d = y->second;
-		if(x->first != y->first || c.region != d.region || c.readers.size() != d.readers.size()) return false;
+		if(x->first != y->first || c.region != d.region || c.readers.size() != d.readers.size() || c.partial.size() != d.partial.size()) return false;
 		if(c.writer != (d.writer < 0 ? d.writer : d.writer + delta)) return false;
 		for(size_t k = 0; k < c.readers.size(); ++k)
 			if(c.readers[k] != d.readers[k] + delta) return false;
+		for(size_t k = 0; k < c.partial.size(); ++k)
+			if(c.partial[k].task != d.partial[k].task + delta || c.partial[k].region != d.partial[k].region) return false;
 	}
 	return true;
 }
@@ -284,6 +367,7 @@ void dep_tracker::restore(int64_t chunk, const snapshot& snap, int64_t delta) {
 	for(auto& [k, c] : a.cells) {
 		if(c.writer >= 0) c.writer += delta;
 		for(auto& r : c.readers) r += delta;
+		for(auto& p : c.partial) p.task += delta;
 	}
 }
 

@@ -20,10 +20,12 @@
 // accesses of one chunk by S superblocks cost O(log S) each instead of O(S^2).
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <map>
 #include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include "geometry.hpp"
@@ -60,10 +62,57 @@ class dep_tracker {
 	void restore(int64_t chunk, const snapshot& s, int64_t delta);
 
   private:
+	// Ascending task ids. Up to kInline live in the cell itself: the cells of band and halo
+	// accesses carry one to three readers, and splitting a cell copies its list, so an inline
+	// list keeps the planner's hot path free of heap traffic (the allocator was a quarter of
+	// the planning time at 1024 superblocks per chunk).
+	class reader_list {
+	  public:
+		reader_list() = default;
+		reader_list(const reader_list&) = default;
+		reader_list& operator=(const reader_list&) = default;
+		reader_list(reader_list&& o) noexcept { *this = std::move(o); }
+		reader_list& operator=(reader_list&& o) noexcept {
+			n_ = o.n_;
+			heap_on_ = o.heap_on_;
+			heap_ = std::move(o.heap_);
+			if(!heap_on_) std::copy(o.inline_, o.inline_ + n_, inline_);
+			o.n_ = 0;
+			o.heap_on_ = false;
+			o.heap_.clear();
+			return *this;
+		}
+		int64_t* begin() { return heap_on_ ? heap_.data() : inline_; }
+		int64_t* end() { return begin() + n_; }
+		const int64_t* begin() const { return heap_on_ ? heap_.data() : inline_; }
+		const int64_t* end() const { return begin() + n_; }
+		size_t size() const { return n_; }
+		int64_t operator[](size_t i) const { return begin()[i]; }
+		void insert(int64_t task); // keeps the order, ignores a task already present
+		bool operator==(const reader_list& o) const;
+		bool operator!=(const reader_list& o) const { return !(*this == o); }
+
+	  private:
+		static constexpr uint32_t kInline = 6;
+		int64_t inline_[kInline] = {};
+		uint32_t n_ = 0;
+		bool heap_on_ = false;
+		std::vector<int64_t> heap_;
+	};
+	// Readers of part of a cell: (task, the box it read, inside the cell). A read never splits
+	// cells; a later write depends on a partial reader only when their boxes overlap, which is
+	// the edge set the split cells gave, without restructuring the map on every halo read.
+	struct partial_read {
+		int64_t task;
+		box region;
+		bool operator==(const partial_read& o) const { return task == o.task && region == o.region; }
+	};
+	static constexpr size_t kMaxPartial = 8; // past this a partial read splits the cell
 	struct cell {
 		box region;
 		int64_t writer = -1;
-		std::vector<int64_t> readers; // ascending
+		reader_list readers;               // read the whole cell
+		std::vector<partial_read> partial; // read part of it (ascending task, then first come)
 	};
 	using key = std::array<int64_t, kMaxRank>; // low corner, index axis first
 	struct state {
@@ -71,7 +120,8 @@ class dep_tracker {
 		bool filled = false;
 		int axis = 0;                        // index axis
 		std::map<key, cell> cells;           // disjoint, covering `region`
-		std::map<int64_t, int64_t> extents;  // cell extent along `axis` -> count
+		// (cell extent along `axis`, count), ascending extent; a handful of distinct values
+		std::vector<std::pair<int64_t, int64_t>> extents;
 		int64_t probes = 0, hits = 0;        // scan efficiency since the last axis check
 	};
 
@@ -88,12 +138,19 @@ class dep_tracker {
 	state& get(int64_t chunk);
 	const state& get(int64_t chunk) const;
 	static key key_of(const state& s, const box& b);
+	static int64_t reach(const state& s) { return s.extents.empty() ? 0 : s.extents.back().first; }
+	static void count_extent(state& s, int64_t e, int64_t by);
 	static void insert(state& s, cell&& c);
 	static cell take(state& s, std::map<key, cell>::iterator it);
+	// map nodes taken out of a cell map, kept per thread for the next insert (splitting and
+	// coalescing cells then reuses nodes instead of going through the allocator)
+	static std::vector<std::map<key, cell>::node_type>& spare_nodes();
 	// moves every cell overlapping `q` out of the map into `out`
 	static void extract(state& s, const box& q, std::vector<cell>& out);
 	static void reindex(state& s);
 	static void split(cell&& c, const box& cut, std::vector<cell>& inside, std::vector<cell>& outside);
+	// partial readers of c clipped to c's region (a clip covering all of it makes a full reader)
+	static void clip_partial(cell& c);
 	void settle(state& s, const box& touched);
 };
 

@@ -52,7 +52,6 @@ int64_t planner::emit(task&& t) {
 	std::sort(t.deps.begin(), t.deps.end());
 	t.deps.erase(std::unique(t.deps.begin(), t.deps.end()), t.deps.end());
 	t.id = next_task_++;
-	task_worker_.push_back(t.worker);
 	plan_.push_back(std::move(t));
 	return next_task_ - 1;
 }
@@ -61,6 +60,21 @@ int64_t planner::new_temp(const box& region, device_id home, dtype type) {
 	const int64_t id = next_chunk_++;
 	chunks_[id] = chunk_meta{chunk_desc{id, region, home}, type, true};
 	return id;
+}
+
+void planner::emit_delete_temp(int worker, device_id dev, int64_t temp) {
+	const auto it = temp_users_.find(temp);
+	task d;
+	d.worker = worker;
+	d.resource = dev;
+	d.kind = task_kind::del;
+	d.deps = it->second; // emit() sorts its own copy
+	d.chunk = temp;
+	emit(std::move(d));
+	it->second.clear();
+	if(spare_users_.size() < 4096) spare_users_.push_back(std::move(it->second));
+	temp_users_.erase(it);
+	if(!cfg_.retain_plan) chunks_.erase(temp);
 }
 
 int64_t planner::emit_create(int worker, device_id dev, int64_t chunk_id, fill_kind fill, reduce_op op) {
@@ -566,16 +580,7 @@ std::pair<int64_t, int64_t> planner::plan_launch(const std::string& kernel, cons
 			}
 			if(w.temp) dead.push_back(w.source);
 		}
-		for(const int64_t t : dead) {
-			task d;
-			d.worker = worker;
-			d.resource = dev;
-			d.kind = task_kind::del;
-			d.deps = temp_users_.at(t);
-			d.chunk = t;
-			emit(std::move(d));
-			temp_users_.erase(t);
-		}
+		for(const int64_t t : dead) emit_delete_temp(worker, dev, t);
 	}
 
 	// hierarchical reduction: device -> worker -> root w0d0 -> destination chunks
@@ -600,6 +605,8 @@ std::pair<int64_t, int64_t> planner::plan_launch(const std::string& kernel, cons
 			r.kind = task_kind::reduce;
 			r.op = op;
 			r.output = out;
+			r.deps.reserve(in.size() + 1);
+			r.inputs.reserve(in.size());
 			r.deps.push_back(create);
 			for(const auto& p : in) {
 				r.inputs.push_back(p.chunk);
@@ -667,15 +674,8 @@ std::pair<int64_t, int64_t> planner::plan_launch(const std::string& kernel, cons
 				transfer(member[static_cast<size_t>(w)].chunk, target.id, intersect(target.region, b), {ar[static_cast<size_t>(w)]}, {});
 			}
 			for(const int64_t id : temps) {
-				const auto& m = chunk(id);
-				task d;
-				d.worker = m.desc.home.worker;
-				d.resource = m.desc.home;
-				d.kind = task_kind::del;
-				d.deps = temp_users_.at(id);
-				d.chunk = id;
-				emit(std::move(d));
-				temp_users_.erase(id);
+				const device_id home = chunk(id).desc.home;
+				emit_delete_temp(home.worker, home, id);
 			}
 			continue;
 		}
@@ -718,15 +718,8 @@ std::pair<int64_t, int64_t> planner::plan_launch(const std::string& kernel, cons
 			transfer(fin, target.id, intersect(target.region, b), {fin_id}, {});
 		}
 		for(const int64_t id : temps) {
-			const auto& m = chunk(id);
-			task d;
-			d.worker = m.desc.home.worker;
-			d.resource = m.desc.home;
-			d.kind = task_kind::del;
-			d.deps = temp_users_.at(id);
-			d.chunk = id;
-			emit(std::move(d));
-			temp_users_.erase(id);
+			const device_id home = chunk(id).desc.home;
+			emit_delete_temp(home.worker, home, id);
 		}
 	}
 	return {first, next_task_};

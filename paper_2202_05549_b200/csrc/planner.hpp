@@ -96,7 +96,6 @@ class planner {
 	const std::deque<task>& plan() const { return plan_; } // tasks [plan_base(), next_id()); appends never move them
 	int64_t plan_base() const { return plan_base_; }
 	int64_t next_id() const { return next_task_; }
-	int worker_of(int64_t task) const { return task_worker_[static_cast<size_t>(task)]; }
 	struct access_rec {
 		int64_t task, chunk;
 		box region;
@@ -114,13 +113,13 @@ class planner {
 	int64_t next_chunk_ = 0;
 	int64_t next_task_ = 0;
 	std::unordered_map<int64_t, chunk_meta> chunks_;
-	std::vector<int> task_worker_;
 	std::deque<task> plan_;
 	int64_t plan_base_ = 0;    // id of plan_.front()
 	int64_t pending_from_ = 0; // first id not yet handed to the executor
 	std::map<std::pair<int, int>, uint64_t> tags_;
 	uint64_t collectives_ = 0; // allreduce group ids, in plan order
 	std::unordered_map<int64_t, std::vector<int64_t>> temp_users_;
+	std::vector<std::vector<int64_t>> spare_users_;
 	std::vector<std::unique_ptr<kernel_entry>> local_kernels_;
 	std::vector<access_rec> accesses_;
 
@@ -153,7 +152,19 @@ class planner {
 
 	int64_t emit(task&& t);
 	int64_t new_temp(const box& region, device_id home, dtype type);
-	void touch(int64_t temp, int64_t t) { temp_users_[temp].push_back(t); }
+	// users of a launch's temporaries (the delete task waits for them); the lists' storage is
+	// recycled across temporaries
+	void touch(int64_t temp, int64_t t) {
+		auto [it, fresh] = temp_users_.try_emplace(temp);
+		if(fresh && !spare_users_.empty()) {
+			it->second = std::move(spare_users_.back());
+			spare_users_.pop_back();
+		}
+		it->second.push_back(t);
+	}
+	// the delete task of a temporary: waits for its users; the temporary's metadata is dropped
+	// with it unless the plan is retained for inspection (mt_chunk_meta)
+	void emit_delete_temp(int worker, device_id dev, int64_t temp);
 	void record(int64_t chunk, int64_t t, bool write, const box& region, bool check_filled, std::vector<int64_t>& out);
 	int64_t transfer(int64_t src, int64_t dst, const box& region, std::vector<int64_t> src_deps, std::vector<int64_t> dst_deps);
 	int64_t emit_create(int worker, device_id dev, int64_t chunk, fill_kind fill, reduce_op op);

@@ -120,14 +120,16 @@ def _np_assign(p, c):
     return best
 
 
-@pytest.mark.parametrize("lim,d", [(8191, 16), (8191, 5), (1 << 20, 16), (255, 16), (1024, 16), (1025, 16), (4096, 1)])
-def test_kmeans_assign_signed_values(lim, d):
+@pytest.mark.parametrize("lim,d,k", [(8191, 16, 48), (8191, 5, 48), (1 << 20, 16, 48), (255, 16, 48), (1024, 16, 48), (1025, 16, 48), (4096, 1, 48),
+                                     (2, 16, 50), (1, 3, 37), (300, 16, 256)])
+def test_kmeans_assign_signed_values(lim, d, k):
     """negative coordinates, |x| at the u32 tier's limit (max distance just below 2^32), a
     padded d < 16, and values past the limit (int64 path); the FP32 tier (sum|x| max|c| <= 2^24:
     lim 255, exactly 2^24 at lim 1024 with d 16, and d 1) and just past its bound (lim 1025);
-    ties included (duplicate centroids)"""
+    ties included (duplicate centroids; lim 1-2: most points tie between many centroids, inside
+    and across the centred tier's centroid groups, and k not a multiple of the group size)"""
     rng = np.random.default_rng(7)
-    n, k = 20_011, 48
+    n = 20_011
     p = rng.integers(-lim, lim + 1, size=(n, d), dtype=np.int64).astype(np.int32)
     c = rng.integers(-lim, lim + 1, size=(k, d), dtype=np.int64).astype(np.int32)
     c[7] = c[3]

@@ -43,3 +43,25 @@ def test_nbody_tiled_bit_exact(n, d):
         got = ctx.read(f)
     want = nbody_ref(pos)
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_nbody_tiled_slow_paths_bit_exact():
+    """magnitudes that push dist2 * sqrt(dist2) past 2^1021 (reciprocal slow path, subnormal
+    result) and dist2 to infinity (square-root slow path): the branch-free groups fall back to
+    the intrinsics and stay bit-identical to the IEEE loop"""
+    n, d = 1000, 3
+    rng = np.random.default_rng(7)
+    scale = 10.0 ** rng.choice([0.0, 100.0, 102.0, 102.5, 103.0, 150.0, 160.0], size=(n, 1))
+    pos = rng.standard_normal((n, d)) * scale
+    with mb.context(workers=1, devices=1, num_gpus=1) as ctx:
+        dv = ctx.devices
+        p = ctx.create_array([n, d], "f64", ctx.dist.single([n, d], dv[0]), 0)
+        f = ctx.create_array([n, d], "f64", ctx.dist.single([n, d], dv[0]), 0)
+        ctx.write(p, pos)
+        ctx.launch("nbody_like", [n], [64], ctx.dist.block_work([n], [64], [-(-n // 64) * 64], dv), [n, d, Arr(f), Arr(p)],
+                   "global i => write force[i,:], read pos[:,:]")
+        got = ctx.read(f)
+    with np.errstate(over="ignore", invalid="ignore"):
+        want = nbody_ref(pos)
+    assert not np.isnan(want).any()
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
