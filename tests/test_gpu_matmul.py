@@ -129,6 +129,31 @@ def test_gemm_tf32_matches_fp64(m, n, k):
     assert rel_r.max() <= 1e-4, (rel_r.max(), np.abs(rel).max())
 
 
+@pytest.mark.parametrize("n", [4096, 8192])
+def test_gemm_tf32_bit_identical_to_cublas(n):
+    """on the C3 ramp operands the tcgen05 TF32 contraction equals cuBLAS TF32 (torch.matmul with
+    allow_tf32) bit for bit: the residual error against fp64 is the tensor cores' own f32
+    accumulation, not this kernel's (profiles/round2/tf32_vs_cublas.json: also all 2^30 elements
+    at 32768^3)"""
+    import torch
+    i = torch.arange(n, dtype=torch.int64, device="cuda")
+
+    def ramp(mod, off):
+        return (((i[:, None] * 31 + i[None, :] * 17 + off) % mod).to(torch.float64) / mod).to(torch.float32)
+
+    a, b = ramp(1000, 7), ramp(997, 7)
+    ours = torch.empty(n, n, device="cuda", dtype=torch.float32)
+    assert _tf32_fn()(a.data_ptr(), b.data_ptr(), ours.data_ptr(), n, n, n, n, n, n, torch.cuda.current_stream().cuda_stream) == 0
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        theirs = a @ b.T
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    torch.cuda.synchronize()
+    assert torch.equal(ours.view(torch.int32), theirs.view(torch.int32))
+
+
 def test_gemm_tf32_nn_reference_layout():
     """mt_gemm_tf32_nn: B row-major K x N (the reference `matmul` layout), transposed and rounded
     in the preparation pass; ragged sizes and a row pitch wider than the matrix"""
