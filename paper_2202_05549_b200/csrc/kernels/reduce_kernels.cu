@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(1024, 1) histogram_pair_kernel(const int32_t* 
 // old value the thread's own atomic returned: adding 1 to byte b of `old` changes bytes b..3 by
 // the carry chain, and each bin k in that chain gets (its true increment) - (its stored change)
 // added to the global partial, which is 0 except when a byte wraps.
+template <int U>
 __global__ void __launch_bounds__(1024, 2) histogram_quad_kernel(const int32_t* x, int64_t n_local, int bins, unsigned long long* hist) {
 	extern __shared__ uint32_t w[];
 	const int words = (bins + 3) / 4;
@@ -232,22 +233,52 @@ __global__ void __launch_bounds__(1024, 2) histogram_quad_kernel(const int32_t* 
 			}
 		}
 	};
+	// the common case without per-element branches: one range test per four values (unsigned
+	// max), four atomics, their wrap tests folded into one predicate (byte k of `old` is 0xFF iff
+	// ~old has no bit of the byte's mask), and one rarely taken branch that books the wraps
+	const auto add4 = [&](const int4 q) {
+		const uint32_t v[4] = {static_cast<uint32_t>(q.x), static_cast<uint32_t>(q.y), static_cast<uint32_t>(q.z), static_cast<uint32_t>(q.w)};
+		if(max(max(v[0], v[1]), max(v[2], v[3])) >= static_cast<uint32_t>(bins)) {
+			add(q.x);
+			add(q.y);
+			add(q.z);
+			add(q.w);
+			return;
+		}
+		uint32_t old[4];
+		bool wrap = false;
+#pragma unroll
+		for(int e = 0; e < 4; ++e) {
+			const uint32_t inc = 1u << ((v[e] & 3u) << 3);
+			old[e] = atomicAdd(&w[v[e] >> 2], inc);
+			wrap |= (~old[e] & (inc * 0xFFu)) == 0;
+		}
+		if(__builtin_expect(wrap, 0)) {
+#pragma unroll
+			for(int e = 0; e < 4; ++e) {
+				const uint32_t sh = (v[e] & 3u) * 8;
+				if(((old[e] >> sh) & 0xFFu) != 0xFFu) continue;
+				const uint32_t nw = old[e] + (1u << sh);
+				for(int kb = v[e] & 3; kb < 4; ++kb) {
+					const int bin = static_cast<int>(v[e] & ~3u) + kb;
+					const int delta = static_cast<int>((nw >> (8 * kb)) & 0xFFu) - static_cast<int>((old[e] >> (8 * kb)) & 0xFFu);
+					const long long fix = (kb == static_cast<int>(v[e] & 3) ? 1 : 0) - delta;
+					if(fix != 0 && bin < bins) atomicAdd(hist + bin, static_cast<unsigned long long>(fix));
+					if(delta != -255) break;
+				}
+			}
+		}
+	};
 	const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
 	const int64_t nvec = n_local / 4;
 	const int4* xv = reinterpret_cast<const int4*>(x);
-	constexpr int U = 4;
 	int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
 	for(; t + (U - 1) * stride < nvec; t += U * stride) {
 		int4 q[U];
 #pragma unroll
 		for(int u = 0; u < U; ++u) q[u] = __ldcs(xv + t + u * stride);
 #pragma unroll
-		for(int u = 0; u < U; ++u) {
-			add(q[u].x);
-			add(q[u].y);
-			add(q[u].z);
-			add(q[u].w);
-		}
+		for(int u = 0; u < U; ++u) add4(q[u]);
 	}
 	for(; t < nvec; t += stride) {
 		const int4 q = __ldcs(xv + t);
@@ -645,11 +676,16 @@ int launch_histogram(const mt_launch_ctx* c, void* stream) {
 		// u8 counters: two CTAs per SM up to 110K bins (65536 bins: 2.67 vs 2.85 ms for the u16
 		// single-CTA kernel), one CTA per SM up to 220K bins
 		const size_t smem = static_cast<size_t>((bins + 3) / 4) * sizeof(uint32_t);
-		ensure_smem(histogram_quad_kernel, static_cast<int>(((kHistQuadMaxBins + 3) / 4) * 4));
+		static const int unroll = [] {
+			const char* e = std::getenv("MTB_HIST_U"); // A/B runs: 16-byte loads in flight per thread, 2 (default) or 4
+			return e && std::atoi(e) == 4 ? 4 : 2;
+		}();
+		const auto kern = unroll == 4 ? histogram_quad_kernel<4> : histogram_quad_kernel<2>;
+		ensure_smem(kern, static_cast<int>(((kHistQuadMaxBins + 3) / 4) * 4));
 		const int per_sm = bins <= kHistPairMaxBins ? 2 : 1;
 		int64_t blocks = (n_local / 4 + 1023) / 1024;
 		blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, per_sm * 148));
-		histogram_quad_kernel<<<static_cast<unsigned>(blocks), 1024, smem, s>>>(x, n_local, static_cast<int>(bins), hist);
+		kern<<<static_cast<unsigned>(blocks), 1024, smem, s>>>(x, n_local, static_cast<int>(bins), hist);
 	} else if(bins <= kHistPairMaxBins && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
 		const size_t smem = static_cast<size_t>((bins + 1) / 2) * sizeof(uint32_t);
 		ensure_smem(histogram_pair_kernel, static_cast<int>(((kHistPairMaxBins + 1) / 2) * 4));

@@ -58,6 +58,8 @@ def main():
         ctx.delete_array(h)
         ctx.synchronize()
 
+    if args.km_n <= 0:
+        return
     n, k, d = args.km_n, 256, 16
     pts = ctx.create_array([n, d], "i32", ctx.dist.single([n, d], dev[0]), 0)
     asg = ctx.create_array([n], "i32", ctx.dist.single([n], dev[0]), 0)
