@@ -182,7 +182,9 @@ typedef struct mt_config {
 	                                   instead of send-to-root / root reduce / send-back
 	                                   (planner.cpp:389-517); 0: the reference's tree */
 	int32_t drop_executed_tasks;    /* 1: forget tasks once handed to the executor (long runs; mt_plan_export
-	                                   then sees only tasks not yet flushed); 0: retain the whole plan */
+	                                   then sees only tasks not yet flushed, and a launch's temporaries are
+	                                   unknown to mt_chunk_meta once their delete task is planned);
+	                                   0: retain the whole plan */
 	uint64_t disk_capacity;         /* disk tier below the pinned-host tier (memory.cpp:113-159): host copies
 	                                   of evicted chunks move to a spill file when the host tier is full;
 	                                   0 = no disk tier */
