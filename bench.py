@@ -838,6 +838,29 @@ def run_ooc(rows, cols, chunk_rows, capacity_gib, host_gib, iters, warmup, looka
 C1_PER_FLUSH = 10
 
 
+def same_size_copy_gbs(nbytes, iters=200):
+    """a plain device copy of one array of the C1 grid (torch copy_, back to back, CUDA events):
+    what the copy peak's 1 GiB figure becomes at this size (the read and written 64 MiB sit in
+    and around the L2), the line the C1 step is compared with beside the HBM peak"""
+    import torch
+    a = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda").uniform_()
+    b = torch.empty_like(a)
+    for _ in range(20):
+        b.copy_(a)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        b.copy_(a)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / iters
+    del a, b
+    torch.cuda.empty_cache()
+    return {"achieved": 2 * nbytes / (us / 1e6) / 1e9, "unit": "GB/s", "us_per_copy": us,
+            "what": f"torch copy_ of {nbytes >> 20} MiB device to device, {iters} back to back"}
+
+
 def run_c1(iters, ref_iters, hbm, cpu, strip=0, chunks=4):
     """BASELINE configs[0] (the reference's CPU scenario): heat2d 4096^2 f32, row-block stencil
     distribution into 4 chunks, one distributed launch per iteration, on one GPU (4 logical
@@ -868,12 +891,14 @@ def run_c1(iters, ref_iters, hbm, cpu, strip=0, chunks=4):
         st = ctx.exec_stats()
         hits = ctx.plan_cache_hits()
     gbs = BYTES_PER_CELL * rows * cols / (ms / 1e3) / 1e9
+    same = same_size_copy_gbs(rows * cols * 4)
     out = {"workload": f"heat2d {rows}x{cols} f32, 4 chunks (stencil_dist halo [1,0]), {iters} iterations, one launch per iteration "
                        f"(mt_launch_repeat with the a/b swap), handed to the executor every {C1_PER_FLUSH} launches"
                        + (f"; 3 superblocks per chunk ({strip}-row halo-facing strips, interior)" if strip else ""),
            "value": rows * cols / (ms / 1e3), "unit": "cell-updates/s", "ms_per_iter": ms,
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-                        "note": "step time incl. planning, halo copies and graph launch; the 64 MiB grid is kept L2-resident between steps (outputs stored with the default policy, dead inputs read evict-first), so the HBM figure is a reference line, not a ceiling"},
+                        "note": "step time incl. planning, halo copies and graph launch; the 64 MiB grid is kept L2-resident between steps (outputs stored with the default policy, dead inputs read evict-first), so the HBM figure is a reference line, not a ceiling",
+                        "same_size_copy": same, "frac_of_same_size_copy": gbs / same["achieved"] if same else None},
            "graph_replays": st.get("graph_replays"), "plan_cache_hits": hits, "fused_halo_copies": st.get("fused_copies"),
            "halo_copies": st.get("copies")}
     if cpu:
