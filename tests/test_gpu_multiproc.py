@@ -50,10 +50,9 @@ def _heat_rank(rank, world, port, rows, cols, iters, q, halo=1):
     dist.destroy_process_group()
 
 
-def _two_process_heat(rows, cols, iters, halo=1):
+def _two_process_heat(rows, cols, iters, halo=1, world=2):
     import paper_2202_05549_b200 as mb
     from paper_2202_05549_b200 import Arr
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -306,3 +305,10 @@ def test_missing_peer_message_times_out():
     for p in procs:
         p.join(timeout=120)
     assert res[0] == "ExecutionError"
+
+
+def test_four_process_heat_matches_single_process():
+    """four ranks: the interior ones exchange halo rows with two neighbours each; enough steps
+    to wrap every peer ring several times"""
+    stats = _two_process_heat(512, 1024, 40, world=4)
+    assert all(s["bytes_sent"] > 0 and s["bytes_received"] > 0 for s in stats)
