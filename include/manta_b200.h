@@ -280,6 +280,11 @@ uint64_t mt_plan_cache_hits(mt_ctx* ctx);
 /* access records of non-temporary chunks in emission order (needs cfg.record_accesses);
  * used to check that the dependency DAG orders every pair of conflicting accesses */
 int mt_plan_accesses(mt_ctx* ctx, mt_access* out, int64_t cap, int64_t* n_out);
+/* parse_annotation (annotation.cpp:105-391) as canonical text: {"bindings": [[space, [vars]]...],
+ * "accesses": [[argument, mode, op, [["single", E] | ["slice", E|null, E|null]...]]...]} with
+ * E = [constant, [[variable, coefficient]...]] (folded terms, first-occurrence order). Parse errors
+ * return MT_EPARSE. *len = text length; written with its terminator when cap > *len. */
+int mt_annotation_describe(const char* text, char* out, int64_t cap, int64_t* len);
 /* chunk_meta (planner.hpp:41-45): temp flag, dtype, descriptor */
 int mt_chunk_meta(mt_ctx* ctx, int64_t chunk, mt_chunk_desc* desc, int32_t* dtype, int32_t* temp);
 /* executor attached to a context (NULL when cfg.execute == 0) */

@@ -541,10 +541,69 @@ struct mt_ctx {
 	bool has_exec = false;
 };
 
+namespace {
+// the reference's access_annotation (annotation.hpp:15-87) in the canonical text of
+// mt_annotation_describe (capi.cpp), for the parser-parity test
+void describe_expr(std::string& o, const linear_expr& e) {
+	o += "[" + std::to_string(e.constant) + ",[";
+	for(size_t t = 0; t < e.terms.size(); ++t) {
+		if(t) o += ",";
+		o += "[\"" + e.terms[t].first + "\"," + std::to_string(e.terms[t].second) + "]";
+	}
+	o += "]]";
+}
+
+std::string describe(const access_annotation& a) {
+	static const char* space[] = {"global", "block", "local"};
+	static const char* kind[] = {"read", "write", "readwrite", "reduce"};
+	static const char* op[] = {"+", "*", "min", "max"};
+	std::string o = "{\"bindings\":[";
+	for(size_t b = 0; b < a.bindings.size(); ++b) {
+		if(b) o += ",";
+		o += "[\"" + std::string(space[static_cast<int>(a.bindings[b].space)]) + "\",[";
+		for(size_t v = 0; v < a.bindings[b].variables.size(); ++v) o += std::string(v ? "," : "") + "\"" + a.bindings[b].variables[v] + "\"";
+		o += "]]";
+	}
+	o += "],\"accesses\":[";
+	for(size_t i = 0; i < a.accesses.size(); ++i) {
+		const auto& acc = a.accesses[i];
+		if(i) o += ",";
+		o += "[\"" + acc.argument + "\",\"" + kind[static_cast<int>(acc.mode.kind)] + "\",\"" + op[static_cast<int>(acc.mode.op)] + "\",[";
+		for(size_t k = 0; k < acc.indices.size(); ++k) {
+			const auto& ix = acc.indices[k];
+			if(k) o += ",";
+			if(ix.kind == index_spec::kind_t::single) {
+				o += "[\"single\",";
+				describe_expr(o, *ix.single);
+				o += "]";
+				continue;
+			}
+			o += "[\"slice\",";
+			if(ix.slice_lower) describe_expr(o, *ix.slice_lower);
+			else o += "null";
+			o += ",";
+			if(ix.slice_upper) describe_expr(o, *ix.slice_upper);
+			else o += "null";
+			o += "]";
+		}
+		o += "]]";
+	}
+	return o + "]}";
+}
+} // namespace
+
 extern "C" {
 
 const char* mr_last_error(void) { return g_last_error.c_str(); }
 const char* mr_version(void) { return "manta-reference (proj/, C++20 CPU executor)"; }
+
+int mr_annotation_describe(const char* text, char* out, int64_t cap, int64_t* len) {
+	return guarded([&] {
+		const std::string s = describe(parse_annotation(text ? text : ""));
+		*len = static_cast<int64_t>(s.size());
+		if(out && cap > static_cast<int64_t>(s.size())) std::memcpy(out, s.c_str(), s.size() + 1);
+	});
+}
 
 int mr_dist_tile(const mt_rect* domain, const int64_t* extents, const int64_t* halo, const mt_device* devices, int32_t ndev, int64_t first_id,
     mt_chunk_desc* out, int64_t cap, int64_t* n_out) {

@@ -190,6 +190,7 @@ _SIGS = {
     "scenario_run": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, P(C.c_int64),
                                P(C.c_int32)]),
     "kernel_info": (C.c_int, [C.c_int32, C.c_char_p, C.c_int32, P(ParamSpec), C.c_int32, P(C.c_int32)]),
+    "annotation_describe": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int64, P(C.c_int64)]),
 }
 # entry points the oracle shim may lack
 _OPTIONAL = {"exec_stats", "exec_last_stream", "kernel_info", "host_threads", "ctx_kernel_register", "fuzz_scenario_json", "scenario_plan", "scenario_dot",

@@ -292,6 +292,58 @@ mt_exec& need_exec(mt_ctx* ctx) {
 
 } // namespace
 
+namespace {
+// canonical text of a parsed annotation (bindings, accesses, folded linear expressions), the
+// same rendering ref_shim.cpp gives the reference's access_annotation
+void describe_expr(std::string& o, const mtb::lin_expr& e, const mtb::annotation& a) {
+	o += "[" + std::to_string(e.constant) + ",[";
+	for(size_t t = 0; t < e.terms.size(); ++t) {
+		if(t) o += ",";
+		o += "[\"" + a.vars[static_cast<size_t>(e.terms[t].slot)].name + "\"," + std::to_string(e.terms[t].coeff) + "]";
+	}
+	o += "]]";
+}
+
+std::string describe(const mtb::annotation& a) {
+	static const char* space[] = {"global", "block", "local"};
+	static const char* kind[] = {"read", "write", "readwrite", "reduce"};
+	static const char* op[] = {"+", "*", "min", "max"};
+	std::string o = "{\"bindings\":[";
+	for(size_t v = 0; v < a.vars.size(); ++v) {
+		const auto& b = a.vars[v];
+		if(b.axis == 0) o += std::string(v ? "]]," : "") + "[\"" + space[static_cast<int>(b.space)] + "\",[";
+		else o += ",";
+		o += "\"" + b.name + "\"";
+	}
+	if(!a.vars.empty()) o += "]]";
+	o += "],\"accesses\":[";
+	for(size_t i = 0; i < a.accesses.size(); ++i) {
+		const auto& acc = a.accesses[i];
+		if(i) o += ",";
+		o += "[\"" + acc.argument + "\",\"" + kind[static_cast<int>(acc.mode.kind)] + "\",\"" + op[static_cast<int>(acc.mode.op)] + "\",[";
+		for(size_t k = 0; k < acc.indices.size(); ++k) {
+			const auto& ix = acc.indices[k];
+			if(k) o += ",";
+			if(!ix.is_slice) {
+				o += "[\"single\",";
+				describe_expr(o, ix.single, a);
+				o += "]";
+				continue;
+			}
+			o += "[\"slice\",";
+			if(ix.has_lower) describe_expr(o, ix.lower, a);
+			else o += "null";
+			o += ",";
+			if(ix.has_upper) describe_expr(o, ix.upper, a);
+			else o += "null";
+			o += "]";
+		}
+		o += "]]";
+	}
+	return o + "]}";
+}
+} // namespace
+
 extern "C" {
 
 const char* mt_last_error(void) { return g_err.c_str(); }
@@ -543,6 +595,14 @@ int mt_plan_export(mt_ctx* ctx, int64_t first, int64_t last, mt_task* tasks, int
 int64_t mt_plan_size(mt_ctx* ctx) { return ctx->plan->next_id(); }
 
 uint64_t mt_plan_cache_hits(mt_ctx* ctx) { return ctx->plan->plan_cache_hits(); }
+
+int mt_annotation_describe(const char* text, char* out, int64_t cap, int64_t* len) {
+	return guarded([&] {
+		const std::string s = describe(mtb::parse_annotation(text ? text : ""));
+		*len = static_cast<int64_t>(s.size());
+		if(out && cap > static_cast<int64_t>(s.size())) std::memcpy(out, s.c_str(), s.size() + 1);
+	});
+}
 
 int mt_plan_accesses(mt_ctx* ctx, mt_access* out, int64_t cap, int64_t* n_out) {
 	return guarded([&] {

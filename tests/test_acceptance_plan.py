@@ -11,6 +11,11 @@
   side is the region the planner records for that superblock's execute task (mt_plan_accesses),
   through a launch of a synthesized gather kernel over a work list whose middle superblock is
   the random one.
+* c2 (acceptance.cpp:104-156): the three reference annotations parse to their exact trees
+  (restated below), and the parsed trees equal the reference parser's (mt_annotation_describe vs
+  the shim's mr_annotation_describe over the same canonical rendering) on the c1 annotations,
+  every annotation of the bundled scenarios and 100 fuzz scenarios, and malformed texts (same
+  error class).
 * c6 (acceptance.cpp:247-287): a halo-1 stencil on 2 workers x 2 devices with 4 superblocks moves
   exactly 4 copies and 2 send/recv pairs per iteration and creates no temporaries (both
   dependency modes).
@@ -227,3 +232,79 @@ def test_c6_halo_stencil_transfers_per_iteration(compat):
                 assert not ctx.chunk_meta(t["src"])[2] and not ctx.chunk_meta(t["dst"])[2]
         a, b = b, a
     ctx.close()
+
+
+def _describe(lib, text):
+    buf = C.create_string_buffer(1 << 16)
+    n = C.c_int64(0)
+    lib.check(lib.annotation_describe(text.encode(), buf, len(buf), C.byref(n)))
+    return buf.value.decode()
+
+
+def _e(const=0, **terms):
+    return [const, [[v, c] for v, c in terms.items()]]
+
+
+def test_c2_reference_annotations_parse_to_exact_trees():
+    import json
+    i, j = _e(i=1), _e(j=1)
+    cases = {
+        "global i => read A[i-1:i+1], write B[i]": {
+            "bindings": [["global", ["i"]]],
+            "accesses": [["A", "read", "+", [["slice", _e(-1, i=1), _e(1, i=1)]]], ["B", "write", "+", [["single", i]]]]},
+        "global [i, j] => read A[i,:], read B[:,j], write C[i,j]": {
+            "bindings": [["global", ["i", "j"]]],
+            "accesses": [["A", "read", "+", [["single", i], ["slice", None, None]]], ["B", "read", "+", [["slice", None, None], ["single", j]]],
+                         ["C", "write", "+", [["single", i], ["single", j]]]]},
+        "global [i, j] => read A[i,j], reduce(+) sum[i]": {
+            "bindings": [["global", ["i", "j"]]],
+            "accesses": [["A", "read", "+", [["single", i], ["single", j]]], ["sum", "reduce", "+", [["single", i]]]]},
+    }
+    lib = mb.lib()
+    for text, tree in cases.items():
+        assert json.loads(_describe(lib, text)) == tree, text
+
+
+def test_annotation_trees_match_reference_parser(ref):
+    import json
+    import os
+    lib = mb.lib()
+    texts = []
+    rng = random.Random(20240801)
+    texts += [_random_case(rng)[0] for _ in range(1000)]
+    scen = os.path.join(os.path.dirname(__file__), "..", "paper_2202_05549_b200", "scenarios")
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    for d in (scen, gold):
+        if os.path.isdir(d):
+            for f in sorted(os.listdir(d)):
+                if f.endswith(".json"):
+                    try:
+                        sc = json.load(open(os.path.join(d, f)))
+                    except ValueError:
+                        continue
+                    for one in ([sc] if isinstance(sc, dict) and "launches" in sc else sc.values() if isinstance(sc, dict) else []):
+                        if isinstance(one, dict):
+                            texts += [l["annotation"] for l in one.get("launches", []) if isinstance(l, dict) and "annotation" in l]
+    n = C.c_int64(0)
+    buf = C.create_string_buffer(1 << 20)
+    for seed in range(1, 101):
+        ref.check(ref.fuzz_scenario_json(seed * 0x9E3779B97F4A7C15 % (1 << 63), buf, len(buf), C.byref(n)))
+        texts += [l["annotation"] for l in json.loads(buf.value)["launches"]]
+    texts += ["global [i, j] => read A[i*j]", "global i => read A[i", "global i => frob A[i]", "global i, global i => read A[i]",
+              "global i => read A[2*i+3*i-5*i]", "global [i, j] => readwrite A[-i+-j:]", "global i => reduce(min) m[0], reduce(*) p[i:i]",
+              "block b, local l => write X[4*b+l]", "global i =>", "=> read A[i]", "global i => read A[k]", "global i => read A[i, ]"]
+    assert len(texts) > 1100
+    errors = 0
+    for text in texts:
+        got = want = None
+        try:
+            got = _describe(lib, text)
+        except mb.MantaError as e:
+            got = type(e).__name__
+        try:
+            want = _describe(ref, text)
+        except mb.MantaError as e:
+            want = type(e).__name__
+        assert got == want, text
+        errors += got.endswith("Error")
+    assert 8 <= errors <= 20, errors  # the malformed texts fail in both parsers, the rest parse
