@@ -2059,17 +2059,18 @@ void executor::peer_import(const std::vector<std::vector<uint8_t>>& blobs) {
 
 // ---- fused single-segment path --------------------------------------------------------------
 //
-// A message that fits one ring slot (every halo row: 256 KiB at C2) moves with ONE kernel per
-// side instead of staging copies, allocations and separate flag kernels:
-//   send (peer tx stream): every CTA waits for the slot to be free (only from the kSlots-th
-//        message on), copies its rows of the region straight from the chunk into the peer's
-//        slot over NVLink (st.global to the IPC-mapped peer memory), fences at system scope;
-//        the last CTA to finish release-stores the slot's ready flag in the peer's memory.
-//   recv (peer rx stream): every CTA acquire-waits on the ready flag, copies its rows from the
-//        slot (ld.global.cg: the peer's stores landed in this GPU's L2) into the chunk; the
-//        last CTA release-stores the consumption counter back into the sender's memory.
+// A message that fits one ring slot (every halo row: 256 KiB at C2) moves with one copy kernel
+// per side, no staging copies or allocations:
+//   send (peer tx stream): from the kSlots-th message on, a one-thread kernel waits for the slot
+//        to be free; the copy kernel's CTAs copy their rows of the region straight from the
+//        chunk into the peer's slot over NVLink (st.global to the IPC-mapped peer memory) and
+//        fence at system scope; the last CTA to finish release-stores the slot's ready flag in
+//        the peer's memory.
+//   recv (peer rx stream): a one-thread kernel acquire-waits on the ready flag; the copy
+//        kernel's CTAs copy their rows from the slot (ld.global.cg: the peer's stores landed in
+//        this GPU's L2) into the chunk; the last CTA release-stores the consumption counter back
+//        into the sender's memory.
 // Larger messages keep the segmented ring below (stage, per-segment wait / copy / flag).
-
 struct box_rows {
 	char* base;          // region start inside the chunk
 	int64_t rows;        // e0 * e1 (rank 3: planes x rows; rank 2: rows; rank 1: 1)
@@ -2096,27 +2097,6 @@ box_rows rows_of(void* chunk_ptr, const box& chunk, const box& region, size_t el
 	b.per_plane = ext[1];
 	b.row_bytes = ext[2] * e;
 	return b;
-}
-
-__device__ __forceinline__ uint64_t now_ns() {
-	uint64_t t;
-	asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-	return t;
-}
-
-__device__ void wait_flag_geq(const uint64_t* flag, uint64_t value, uint64_t timeout_ns) {
-	const uint64_t t0 = now_ns();
-	for(;;) {
-		uint64_t v;
-		asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-		if(v >= value) return;
-		__nanosleep(32);
-		if(now_ns() - t0 > timeout_ns) {
-			printf("manta-b200: peer message wait timed out (flag %p: %llu < %llu)\n", flag, static_cast<unsigned long long>(v),
-			    static_cast<unsigned long long>(value));
-			__trap();
-		}
-	}
 }
 
 // packed message (row-major region) <-> rows of a chunk; `to_packed` chooses the direction
@@ -2162,19 +2142,17 @@ __device__ void last_cta_release(unsigned* done, uint64_t* flag, uint64_t value)
 	}
 }
 
-__global__ void fused_send_k(box_rows src, char* slot, const uint64_t* consumed, uint64_t need, uint64_t* ready, uint64_t value, unsigned* done,
-    uint64_t timeout_ns) {
-	if(need) {
-		if(threadIdx.x == 0) wait_flag_geq(consumed, need, timeout_ns);
-		__syncthreads();
-	}
+// The waits themselves run in a one-thread spin_until_geq kernel ahead of these on the same
+// stream: a copy kernel whose CTAs all spun would hold tens of CTAs per pending message
+// resident, and ranks sharing a GPU (MPS) or a GPU busy with a large kernel could fill every
+// SM with waiters while the kernels they wait for queue behind them (4 ranks under MPS
+// deadlocked that way). One waiting thread per message cannot exhaust the SMs.
+__global__ void fused_send_k(box_rows src, char* slot, uint64_t* ready, uint64_t value, unsigned* done) {
 	move_any<false>(src, slot, true);
 	last_cta_release(done, ready, value);
 }
 
-__global__ void fused_recv_k(box_rows dst, char* slot, const uint64_t* ready, uint64_t value, uint64_t* consumed, unsigned* done, uint64_t timeout_ns) {
-	if(threadIdx.x == 0) wait_flag_geq(ready, value, timeout_ns);
-	__syncthreads();
+__global__ void fused_recv_k(box_rows dst, char* slot, uint64_t* consumed, uint64_t value, unsigned* done) {
 	move_any<true>(dst, slot, false);
 	last_cta_release(done, consumed, value);
 }
@@ -2198,8 +2176,12 @@ void executor::remote_send(const task& t) {
 		const uint64_t q = link.tx_seq++;
 		const uint64_t slot = q % kSlots;
 		const uint64_t need = q >= static_cast<uint64_t>(kSlots) ? q + 1 - kSlots : 0;
-		fused_send_k<<<fused_grid(bytes), 256, 0, s>>>(rows_of(src.ptr, src.region, t.region, elem), link.tx_ring + slot * kSlotBytes, link.tx_consumed,
-		    need, link.tx_ready + slot, q + 1, link.tx_done, peer_timeout_ns());
+		if(need) {
+			spin_until_geq<<<1, 1, 0, s>>>(link.tx_consumed, need, peer_timeout_ns());
+			++ctr_.message_ops;
+		}
+		fused_send_k<<<fused_grid(bytes), 256, 0, s>>>(rows_of(src.ptr, src.region, t.region, elem), link.tx_ring + slot * kSlotBytes, link.tx_ready + slot,
+		    q + 1, link.tx_done);
 		++ctr_.message_ops;
 	} else {
 		// contiguous staging of the region, then one ring segment at a time
@@ -2238,9 +2220,10 @@ void executor::remote_recv(const task& t) {
 	if(bytes <= kSlotBytes) {
 		const uint64_t q = link.rx_seq++;
 		const uint64_t slot = q % kSlots;
-		fused_recv_k<<<fused_grid(bytes), 256, 0, s>>>(rows_of(dst.ptr, dst.region, t.region, elem), link.rx_ring + slot * kSlotBytes, link.rx_ready + slot,
-		    q + 1, link.rx_consumed, link.rx_done, peer_timeout_ns());
-		++ctr_.message_ops;
+		spin_until_geq<<<1, 1, 0, s>>>(link.rx_ready + slot, q + 1, peer_timeout_ns());
+		fused_recv_k<<<fused_grid(bytes), 256, 0, s>>>(rows_of(dst.ptr, dst.region, t.region, elem), link.rx_ring + slot * kSlotBytes, link.rx_consumed,
+		    q + 1, link.rx_done);
+		ctr_.message_ops += 2;
 	} else {
 		void* stage = nullptr;
 		check_cuda(cudaMallocFromPoolAsync(&stage, bytes, G.pool, s), "cudaMallocFromPoolAsync");

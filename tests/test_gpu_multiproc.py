@@ -81,11 +81,12 @@ def _two_process_heat(rows, cols, iters, halo=1, world=2):
 
 def test_two_process_heat_matches_single_process():
     """10 iterations: each rank sends and receives one halo row per iteration, so the 4-slot ring
-    wraps twice; every message is one fused kernel per side (exec_stats message_ops)"""
+    wraps twice; every message is one copy kernel per side, preceded by a one-thread wait kernel
+    for every receive and for every send past the ring's 4 slots (exec_stats message_ops)"""
     stats = _two_process_heat(256, 512, 10)
     for st in stats:
         assert st["messages"] == 22  # (ramp + 10 iterations) x (1 send + 1 receive) per rank
-        assert st["message_ops"] == st["messages"]
+        assert st["message_ops"] == 22 + 11 + (11 - 4)
 
 
 def test_two_process_heat_large_halo_segments():
