@@ -681,7 +681,7 @@ def run_reference_arm(args):
     }))
 
 
-# FP64-pipe instructions per pair interaction of nbody_tiled_k<3, 4>: DADD 9 + DMUL 10 + DFMA 10
+# FP64-pipe instructions per pair interaction of nbody_tiled_k<3, 8>: DADD 9 + DMUL 10 + DFMA 10
 # (the two MUFU seeds run on the XU pipe); ncu sm__sass_thread_inst_executed_op_{dadd,dmul,dfma}
 # in the ratio 9:10:10, profiles/round2/ncu/nbody_summary.txt
 NBODY_DP_PER_PAIR = 29

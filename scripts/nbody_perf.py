@@ -10,6 +10,7 @@ import paper_2202_05549_b200 as mb  # noqa: E402
 from paper_2202_05549_b200 import Arr  # noqa: E402
 
 n, d = int(sys.argv[1]) if len(sys.argv) > 1 else 65536, 3
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 with mb.context(workers=1, devices=1, num_gpus=1) as ctx:
     dv = ctx.devices
     p = ctx.create_array([n, d], "f64", ctx.dist.single([n, d], dv[0]), 0)
@@ -24,8 +25,8 @@ with mb.context(workers=1, devices=1, num_gpus=1) as ctx:
     step()
     ctx.synchronize()
     ctx.mark(0)
-    for _ in range(3):
+    for _ in range(steps):
         step()
     ctx.mark(1)
-    ms = ctx.elapsed_ms() / 3
+    ms = ctx.elapsed_ms() / steps
     print(f"nbody n={n} d={d}: {ms:.2f} ms/step, {n * (n - 1) / (ms / 1e3) / 1e9:.1f} G pair-interactions/s")
