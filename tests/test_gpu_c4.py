@@ -29,6 +29,33 @@ def test_histogram_paths(okern, bins):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("bins", [256, 16385, 65536, 110001, 220000])
+def test_histogram_out_of_range_values(okern, bins):
+    """values below 0 and at or above `bins` are skipped (oracle_histogram), mixed into the
+    in-range ones at every position of the 16-byte loads (the batched kernels test four values
+    at a time and fall back per element), plus a hot bin that wraps the shared counters; n not a
+    multiple of 4 (the scalar tail)"""
+    n = 5_000_003
+    rng = np.random.default_rng(bins)
+    x = rng.integers(0, bins, size=n, dtype=np.int64)
+    x[rng.random(n) < 0.02] = bins + rng.integers(0, 1000, size=1)[0]
+    x[rng.random(n) < 0.02] = -1 - rng.integers(0, 1 << 30, size=1)[0]
+    x[::7] = 3  # hot bin
+    x[-5:] = [bins, -1, 0, bins - 1, (1 << 31) - 1]
+    x = x.astype(np.int32)
+    with mb.context(workers=1, devices=1, num_gpus=1) as ctx:
+        d = ctx.devices
+        xa = ctx.create_array([n], "i32", ctx.dist.single([n], d[0]), 0)
+        h = ctx.create_array([bins], "i64", ctx.dist.single([bins], d[0]), 0)
+        ctx.write(xa, x)
+        ctx.launch("histogram", [n], [128], ctx.dist.block_work([n], [128], [-(-n // 128) * 128], d), [n, bins, Arr(xa), Arr(h)],
+                   "global i => read x[i], reduce(+) hist[:]")
+        got = ctx.read(h)
+    want = np.empty(bins, np.int64)
+    okern.oracle_histogram(x.ctypes.data_as(I32), C.c_int64(n), C.c_int64(bins), want.ctypes.data_as(I64))
+    assert np.array_equal(got, want)
+
+
 def test_histogram_u16_overflow():
     """every element in one bin: the packed-u16 counters wrap many times"""
     n, bins = 1 << 20, 65536
