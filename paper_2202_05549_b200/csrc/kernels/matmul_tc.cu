@@ -57,8 +57,12 @@ constexpr int kTileRing = 4; // dynamic scheduler: tile ids in flight per CTA
 // of the single-CTA kernel from L2 (the tile shape cuBLAS picks at 32768^3,
 // nvjet_tst_256x256_64x4_2x1_2cta).
 __host__ __device__ constexpr int pair_stages(int nsub) { return nsub == 1 ? STAGES2 : 4; }
+// epilogue staging (CTA-pair kernels): per epilogue warp a 32 x 32 f32 block, rows padded to 36
+// floats (16-byte aligned rows, conflict-free 128-bit shared stores and loads)
+constexpr int kEpiPitch = 36;
+constexpr size_t kEpiBytes = 4 * 32 * kEpiPitch * sizeof(float);
 __host__ __device__ constexpr size_t pair_smem_bytes(int nsub) {
-	return 1024 + static_cast<size_t>(pair_stages(nsub)) * (A_STAGE_BYTES + nsub * B2_STAGE_BYTES) + 256;
+	return 1024 + static_cast<size_t>(pair_stages(nsub)) * (A_STAGE_BYTES + nsub * B2_STAGE_BYTES) + 256 + kEpiBytes;
 }
 static_assert(pair_smem_bytes(2) <= 227 * 1024, "wide pair stages");
 static_assert((2 * STAGES2 + 4 + 2 * kTileRing) * 8 + 4 * kTileRing + 4 <= 256, "barrier area");
@@ -75,6 +79,7 @@ struct gemm_args {
 	uint64_t hint_a, hint_b; // L2 cache policies of the operand loads
 	int no_store;            // diagnostics (MTB_GEMM_NOSTORE): skip the C stores
 	int n_major;             // diagnostics (MTB_GEMM_NMAJOR): rasterise N-first
+	int epi_rowwise;         // A/B (MTB_GEMM_EPI=0): the per-row epilogue stores instead of the transposed ones
 	unsigned* sched;         // dynamic tile counter (zeroed per launch); null: static round robin
 	unsigned long long* trace; // diagnostics (MTB_GEMM_TRACE): per tile {cluster, start ns, end ns} of the MMA issue
 };
@@ -614,6 +619,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	} else {
 		// ---- epilogue (both CTAs): warps 2..5, own TMEM lanes = own 128 rows ----
 		const int quarter = warp & 3;
+		float* epi = reinterpret_cast<float*>(smem + kStages * kStageBytes + 256) + quarter * 32 * kEpiPitch;
 		for(int local = 0, ts = first_unit;; ++local, ts += unit_stride) {
 			int t = ts;
 			if(dyn) {
@@ -626,15 +632,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			const int acc = local % kAcc;
 			mbar_wait(&tmem_full[acc], (local / kAcc) & 1);
 			tc_fence_after();
-			const int64_t row = static_cast<int64_t>(mu) * 2 * BM + rank * BM + quarter * 32 + lane;
+			const int64_t row0 = static_cast<int64_t>(mu) * 2 * BM + rank * BM + quarter * 32; // this warp's first row
+			const int64_t row = row0 + lane;
 			const bool row_ok = row < p.m && !p.no_store;
 			float* crow = p.c + row * p.ldc;
 			const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kAccCols);
+			// transposed stores: a 32 x 32 block goes through shared memory so that each 128-bit
+			// store instruction writes four whole 128-byte row segments (lanes 8r..8r+7 one row)
+			// instead of one 16-byte piece of 32 different rows
+			const bool block_rows = !p.epi_rowwise && !p.no_store && row0 + 32 <= p.m && (p.ldc & 3) == 0
+			                        && (reinterpret_cast<uintptr_t>(p.c) & 15) == 0;
 #pragma unroll 1
 			for(int c = 0; c < kAccCols; c += 32) {
 				uint32_t r[32];
 				tmem_ld32(taddr + static_cast<uint32_t>(c), r);
 				const int64_t col0 = static_cast<int64_t>(nb) * kAccCols + c;
+				if(block_rows && col0 + 32 <= p.n) {
+#pragma unroll
+					for(int v = 0; v < 8; ++v)
+						*reinterpret_cast<float4*>(epi + lane * kEpiPitch + 4 * v) =
+						    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]), __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+					__syncwarp();
+					const int rr = lane >> 3, cc = (lane & 7) * 4;
+#pragma unroll
+					for(int v = 0; v < 8; ++v) {
+						const float4 f = *reinterpret_cast<const float4*>(epi + (4 * v + rr) * kEpiPitch + cc);
+						*reinterpret_cast<float4*>(p.c + (row0 + 4 * v + rr) * p.ldc + col0 + cc) = f;
+					}
+					__syncwarp();
+					continue;
+				}
 				if(!row_ok) continue;
 				if(col0 + 32 <= p.n && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0)) {
 #pragma unroll
@@ -738,6 +765,7 @@ int run_gemm(const void* a, int64_t a_rows, int64_t lda, int64_t a_row0, const v
 	//  * single CTAs (128x256) otherwise.
 	const bool big = static_cast<double>(m) * static_cast<double>(n) > 16384.0 * 16384.0 && k > 16384;
 	p.no_store = std::getenv("MTB_GEMM_NOSTORE") != nullptr;
+	p.epi_rowwise = std::getenv("MTB_GEMM_EPI") && std::atoi(std::getenv("MTB_GEMM_EPI")) == 0;
 	if(const char* e = std::getenv("MTB_GEMM_TRACE")) p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(e, nullptr, 0));
 	p.n_major = std::getenv("MTB_GEMM_NMAJOR") != nullptr;
 	const bool force_pair = std::getenv("MTB_GEMM_FORCE_PAIR") != nullptr;
