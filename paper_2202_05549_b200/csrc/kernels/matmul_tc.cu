@@ -43,7 +43,12 @@ constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;  // 32 KB
 constexpr uint32_t STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr uint32_t TMEM_COLS = 512;                // two 256-column f32 accumulators
 constexpr int GROUP_M = 16;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+// epilogue staging: per epilogue warp a 32 x 32 f32 block, rows padded to 36 floats (16-byte
+// aligned rows, conflict-free 128-bit shared stores and loads); the C stores then go out as whole
+// 128-byte row segments (see the epilogues)
+constexpr int kEpiPitch = 36;
+constexpr size_t kEpiBytes = 4 * 32 * kEpiPitch * sizeof(float);
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/ + kEpiBytes;
 // CTA pair (cta_group::2): a 256x256 tile per pair; per CTA per stage its 128 A rows and its
 // 128 of the 256 Bt rows, so 32 KB per stage and 6 stages in flight
 constexpr int STAGES2 = 6;
@@ -57,10 +62,6 @@ constexpr int kTileRing = 4; // dynamic scheduler: tile ids in flight per CTA
 // of the single-CTA kernel from L2 (the tile shape cuBLAS picks at 32768^3,
 // nvjet_tst_256x256_64x4_2x1_2cta).
 __host__ __device__ constexpr int pair_stages(int nsub) { return nsub == 1 ? STAGES2 : 4; }
-// epilogue staging (CTA-pair kernels): per epilogue warp a 32 x 32 f32 block, rows padded to 36
-// floats (16-byte aligned rows, conflict-free 128-bit shared stores and loads)
-constexpr int kEpiPitch = 36;
-constexpr size_t kEpiBytes = 4 * 32 * kEpiPitch * sizeof(float);
 __host__ __device__ constexpr size_t pair_smem_bytes(int nsub) {
 	return 1024 + static_cast<size_t>(pair_stages(nsub)) * (A_STAGE_BYTES + nsub * B2_STAGE_BYTES) + 256 + kEpiBytes;
 }
@@ -396,6 +397,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	} else {
 		// ---- epilogue: warps 2..5, TMEM lanes 32*(warp%4) .. +31 ----
 		const int quarter = warp & 3;
+		float* epi = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + quarter * 32 * kEpiPitch;
 		for(int local = 0, ts = blockIdx.x;; ++local, ts += gridDim.x) {
 			int t = ts;
 			if(dyn) {
@@ -408,16 +410,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 			const int acc = local & 1;
 			mbar_wait(&tmem_full[acc], (local >> 1) & 1);
 			tc_fence_after();
-			const int64_t row = static_cast<int64_t>(mb) * BM + quarter * 32 + lane;
+			const int64_t row0 = static_cast<int64_t>(mb) * BM + quarter * 32; // this warp's first row
+			const int64_t row = row0 + lane;
 			const bool row_ok = row < p.m;
 			float* crow = p.c + row * p.ldc;
 			const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
+			const bool block_rows = !p.epi_rowwise && !p.no_store && row0 + 32 <= p.m && (p.ldc & 3) == 0
+			                        && (reinterpret_cast<uintptr_t>(p.c) & 15) == 0;
 #pragma unroll 1
 			for(int c = 0; c < BN; c += 32) {
 				uint32_t r[32];
 				tmem_ld32(taddr + static_cast<uint32_t>(c), r);
 				const int64_t col0 = static_cast<int64_t>(nb) * BN + c;
-				if(!row_ok) continue;
+				if(block_rows && col0 + 32 <= p.n) { // transposed through shared memory (CTA-pair kernel)
+#pragma unroll
+					for(int v = 0; v < 8; ++v)
+						*reinterpret_cast<float4*>(epi + lane * kEpiPitch + 4 * v) =
+						    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]), __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+					__syncwarp();
+					const int rr = lane >> 3, cc = (lane & 7) * 4;
+#pragma unroll
+					for(int v = 0; v < 8; ++v) {
+						const float4 f = *reinterpret_cast<const float4*>(epi + (4 * v + rr) * kEpiPitch + cc);
+						*reinterpret_cast<float4*>(p.c + (row0 + 4 * v + rr) * p.ldc + col0 + cc) = f;
+					}
+					__syncwarp();
+					continue;
+				}
+				if(!row_ok || p.no_store) continue;
 				if(col0 + 32 <= p.n && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0)) {
 #pragma unroll
 					for(int v = 0; v < 8; ++v) {
