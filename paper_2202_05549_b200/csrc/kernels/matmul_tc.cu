@@ -89,6 +89,32 @@ struct gemm_args {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+	asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+	float4 f;
+	asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w) : "r"(addr) : "memory");
+	return f;
+}
+
+// one 32 x 32 f32 block of C from the epilogue warp's registers (lane = row, r = its 32 columns)
+// through its shared staging block (32 rows of kEpiPitch floats at `epi`, a shared address), so
+// that every 128-bit global store writes four whole 128-byte row segments
+__device__ __forceinline__ void store_block_transposed(uint32_t epi, const uint32_t (&r)[32], float* c, int64_t ldc, int64_t row0, int64_t col0, int lane, int pitch) {
+#pragma unroll
+	for(int v = 0; v < 8; ++v) sts128(epi + static_cast<uint32_t>((lane * pitch + 4 * v) * 4), r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+	__syncwarp();
+	const int rr = lane >> 3, cc = (lane & 7) * 4;
+	float4 f[8];
+#pragma unroll
+	for(int v = 0; v < 8; ++v) f[v] = lds128(epi + static_cast<uint32_t>(((4 * v + rr) * pitch + cc) * 4));
+#pragma unroll
+	for(int v = 0; v < 8; ++v) *reinterpret_cast<float4*>(c + (row0 + 4 * v + rr) * ldc + col0 + cc) = f[v];
+	__syncwarp();
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 	asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -397,7 +423,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	} else {
 		// ---- epilogue: warps 2..5, TMEM lanes 32*(warp%4) .. +31 ----
 		const int quarter = warp & 3;
-		float* epi = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + quarter * 32 * kEpiPitch;
+		const uint32_t epi = smem_u32(smem + STAGES * STAGE_BYTES + 256) + static_cast<uint32_t>(quarter * 32 * kEpiPitch * 4);
 		for(int local = 0, ts = blockIdx.x;; ++local, ts += gridDim.x) {
 			int t = ts;
 			if(dyn) {
@@ -423,18 +449,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 				tmem_ld32(taddr + static_cast<uint32_t>(c), r);
 				const int64_t col0 = static_cast<int64_t>(nb) * BN + c;
 				if(block_rows && col0 + 32 <= p.n) { // transposed through shared memory (CTA-pair kernel)
-#pragma unroll
-					for(int v = 0; v < 8; ++v)
-						*reinterpret_cast<float4*>(epi + lane * kEpiPitch + 4 * v) =
-						    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]), __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-					__syncwarp();
-					const int rr = lane >> 3, cc = (lane & 7) * 4;
-#pragma unroll
-					for(int v = 0; v < 8; ++v) {
-						const float4 f = *reinterpret_cast<const float4*>(epi + (4 * v + rr) * kEpiPitch + cc);
-						*reinterpret_cast<float4*>(p.c + (row0 + 4 * v + rr) * p.ldc + col0 + cc) = f;
-					}
-					__syncwarp();
+store_block_transposed(epi, r, p.c, p.ldc, row0, col0, lane, kEpiPitch);
 					continue;
 				}
 				if(!row_ok || p.no_store) continue;
@@ -639,7 +654,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 	} else {
 		// ---- epilogue (both CTAs): warps 2..5, own TMEM lanes = own 128 rows ----
 		const int quarter = warp & 3;
-		float* epi = reinterpret_cast<float*>(smem + kStages * kStageBytes + 256) + quarter * 32 * kEpiPitch;
+		const uint32_t epi = smem_u32(smem + kStages * kStageBytes + 256) + static_cast<uint32_t>(quarter * 32 * kEpiPitch * 4);
 		for(int local = 0, ts = first_unit;; ++local, ts += unit_stride) {
 			int t = ts;
 			if(dyn) {
@@ -668,18 +683,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 				tmem_ld32(taddr + static_cast<uint32_t>(c), r);
 				const int64_t col0 = static_cast<int64_t>(nb) * kAccCols + c;
 				if(block_rows && col0 + 32 <= p.n) {
-#pragma unroll
-					for(int v = 0; v < 8; ++v)
-						*reinterpret_cast<float4*>(epi + lane * kEpiPitch + 4 * v) =
-						    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]), __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-					__syncwarp();
-					const int rr = lane >> 3, cc = (lane & 7) * 4;
-#pragma unroll
-					for(int v = 0; v < 8; ++v) {
-						const float4 f = *reinterpret_cast<const float4*>(epi + (4 * v + rr) * kEpiPitch + cc);
-						*reinterpret_cast<float4*>(p.c + (row0 + 4 * v + rr) * p.ldc + col0 + cc) = f;
-					}
-					__syncwarp();
+store_block_transposed(epi, r, p.c, p.ldc, row0, col0, lane, kEpiPitch);
 					continue;
 				}
 				if(!row_ok) continue;
