@@ -245,3 +245,35 @@ def test_bf16_reduce_tree(testkernels):
         parts.append(acc)
     want = _bf16(_bf16(parts[0] + parts[1]) + _bf16(parts[2] + parts[3]))
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_stencil1d_boundary_and_interior_known_answers():
+    """test_kernels.cpp:66-86: ones in, (left+mid+right)/3 out with zero padding: 2/3 at both
+    ends, 1 inside"""
+    import numpy as np
+    n = 16
+    with mb.context(workers=1, devices=1, num_gpus=1) as ctx:
+        d = ctx.devices
+        a = ctx.create_array([n], "f32", ctx.dist.single([n], d[0]), 1)
+        b = ctx.create_array([n], "f32", ctx.dist.single([n], d[0]), 0)
+        ctx.launch("stencil1d", [n], [4], ctx.dist.block_work([n], [4], [n], d), [n, Arr(b), Arr(a)], "global i => read input[i-1:i+1], write output[i]")
+        out = ctx.read(b)
+    assert out[0] == np.float32(2.0) / np.float32(3.0) and out[-1] == out[0]
+    assert (out[1:-1] == 1.0).all()
+
+
+def test_matmul_identity_times_m_returns_m():
+    """test_kernels.cpp:88-107: I x M == M byte for byte (the reference matmul id)"""
+    import numpy as np
+    n = 8
+    with mb.context(workers=1, devices=1, num_gpus=1) as ctx:
+        d = ctx.devices
+        mk = lambda: ctx.create_array([n, n], "f32", ctx.dist.single([n, n], d[0]), 0)  # noqa: E731
+        a, b, c = mk(), mk(), mk()
+        ctx.write(a, np.eye(n, dtype=np.float32))
+        m = np.arange(n * n, dtype=np.float32).reshape(n, n)
+        ctx.write(b, m)
+        ctx.launch("matmul", [n, n], [2, 2], ctx.dist.block_work([n, n], [2, 2], [4, 4], d), [n, n, n, Arr(c), Arr(a), Arr(b)],
+                   "global [i, j] => write C[i,j], read A[i,:], read B[:,j]")
+        got = ctx.read(c)
+    assert got.tobytes() == m.tobytes()
