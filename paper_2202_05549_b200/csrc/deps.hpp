@@ -73,6 +73,7 @@ class dep_tracker {
 		reader_list& operator=(const reader_list&) = default;
 		reader_list(reader_list&& o) noexcept { *this = std::move(o); }
 		reader_list& operator=(reader_list&& o) noexcept {
+			if(this == &o) return *this;
 			n_ = o.n_;
 			heap_on_ = o.heap_on_;
 			heap_ = std::move(o.heap_);
